@@ -1,0 +1,217 @@
+/* qdwhg.h — C ABI of libqdwhg, the B200-native (sm_100a) QDWHpartial hot path.
+ *
+ * Drop-in boundary for the reference's core/ driver entry points
+ * (/root/reference/proj/core/include/qdwh):
+ *
+ *   qdwhg_polar              <- qdwh::polar_decompose          polar.hpp:60
+ *   qdwhg_partial_eig        <- qdwh::qdwh_partial_eig         partial.hpp:55-57
+ *   qdwhg_partial_svd        <- qdwh::qdwh_partial_svd         partial.hpp:85-86
+ *   qdwhg_partial_eig_request <- spectrum-fraction front end for partial EIG
+ *                               (shift map B = cI - A / A - cI)
+ *   qdwhg_partial_svd_request <- absolute-cut / top-k front end for partial SVD
+ *   qdwhg_run_fixed_iterations <- qdwh::run_fixed_iterations  polar.hpp:74-75
+ *   qdwhg_qdwh_chol_step     <- qdwh::qdwh_chol_step           polar.hpp:56
+ *   qdwhg_qdwh_qr_step       <- qdwh::qdwh_qr_step             polar.hpp:53
+ *   qdwhg_qr_factor          <- qdwh::qr_factor                kernels.hpp:18
+ *   qdwhg_cholesky           <- qdwh::cholesky                 kernels.hpp:25
+ *   qdwhg_sym_eig_dense      <- qdwh::sym_eig_dense            kernels.hpp:33
+ *   qdwhg_svd_dense          <- qdwh::svd_dense                kernels.hpp:42
+ *   qdwhg_two_norm_estimate  <- qdwh::two_norm_estimate        kernels.hpp:46
+ *   qdwhg_lanczos_min_bound  <- qdwh::lanczos_min_bound        kernels.hpp:51
+ *   qdwhg_halley_weights     <- qdwh::halley_weights           polar.hpp:22
+ *   qdwhg_iterations_to_converge <- qdwh::iterations_to_converge polar.hpp:30
+ *   qdwhg_choose_shift       <- qdwh::choose_shift             partial.hpp:23
+ *
+ * Conventions (mirroring the reference):
+ *   - matrices are column-major FP64 with an explicit leading dimension;
+ *   - every matrix pointer may be HOST or DEVICE memory (on the handle's
+ *     device); the kind is detected per pointer.  Device pointers skip the
+ *     host<->device copies (the benchmark's "value" path), host pointers are
+ *     the end-to-end path;
+ *   - outputs are caller-allocated; vector outputs hold k_cap columns and the
+ *     number actually returned is info->k (QDWHG_CAPACITY if k > k_cap);
+ *   - exceptions of the reference map to status codes; an empty spectrum is
+ *     NOT an error (status OK, info->k == 0), as in partial.cpp:52,73,90,140,152;
+ *   - a handle is used by one thread at a time; calls are synchronous.
+ */
+#ifndef QDWHG_H
+#define QDWHG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum qdwhg_status {
+  QDWHG_OK = 0,
+  QDWHG_INVALID_ARGUMENT = 1,      /* std::invalid_argument                      */
+  QDWHG_NOT_POSITIVE_DEFINITE = 2, /* qdwh::NotPositiveDefinite, matrix.hpp:13-16 */
+  QDWHG_NOT_CONVERGED = 3,         /* qdwh::NotConverged, matrix.hpp:19-22        */
+  QDWHG_CAPACITY = 4,              /* k exceeds the caller's k_cap                 */
+  QDWHG_CUDA_ERROR = 5,
+  QDWHG_NCCL_ERROR = 6,
+  QDWHG_INTERNAL = 7
+} qdwhg_status;
+
+typedef struct qdwhg_handle qdwhg_handle;
+
+typedef struct qdwhg_options {
+  int32_t device;        /* CUDA ordinal; -1 = current device */
+  int32_t reserved0;
+  uint64_t arena_bytes;  /* 0 = grow on demand */
+  uint64_t flags;        /* reserved, 0 */
+} qdwhg_options;
+
+#define QDWHG_MAX_TRACE 64
+#define QDWHG_NUM_STAGES 8
+/* stage_seconds[]: 0 bound (Lanczos / power iteration), 1 QDWH iterations,
+ * 2 subspace QR + diag scan, 3 Q2 formation, 4 Rayleigh-Ritz products,
+ * 5 small EIG/SVD, 6 back-transform, 7 host<->device transfers */
+
+typedef struct qdwhg_eig_info { /* partial.hpp:29-52 */
+  double mu;               /* Lanczos lower bound used as scale          */
+  double shift;            /* plan.s                                     */
+  double tol;
+  double c_shift;          /* request front end: spectral shift c (0 for raw calls) */
+  int64_t rank_index;      /* 1-based deficiency index, 0 when none      */
+  int64_t subspace_size;   /* ell                                        */
+  int64_t k;               /* values returned                            */
+  int64_t k_found;         /* values found before a request's top-k cut  */
+  int64_t iters_qr, iters_chol, borderline;
+  int32_t no_savings, randomized;
+  int32_t n_trace, reserved;
+  double ell_trace[QDWHG_MAX_TRACE];
+  double seconds;          /* device time of the call                    */
+  double flops;            /* algorithmic FP64 flops   */
+  double stage_seconds[QDWHG_NUM_STAGES];
+} qdwhg_eig_info;
+
+typedef struct qdwhg_svd_info { /* partial.hpp:59-81 */
+  double alpha;            /* two-norm estimate used for scaling */
+  double threshold;        /* relative threshold s               */
+  double tol;
+  double cut;              /* absolute cut s*alpha               */
+  int64_t rank_index, subspace_size, k, k_found;
+  int64_t iters_qr, iters_chol;
+  int32_t no_savings, randomized;
+  int32_t n_trace, reserved;
+  double ell_trace[QDWHG_MAX_TRACE];
+  double seconds, flops;
+  double stage_seconds[QDWHG_NUM_STAGES];
+} qdwhg_svd_info;
+
+typedef struct qdwhg_polar_config { /* polar.hpp:34-40 */
+  double ell0;           /* 1e-15 */
+  int64_t max_iters;     /* 60 */
+  double conv_eps;       /* 2.220446049250313e-16 */
+  double chol_switch_c;  /* 100 */
+  int32_t force_variant; /* 0 Auto, 1 QrOnly, 2 CholeskyOnly */
+  int32_t reserved;
+} qdwhg_polar_config;
+
+typedef struct qdwhg_polar_info { /* polar.hpp:42-50 */
+  double alpha;
+  int64_t iters_qr, iters_chol;
+  int32_t converged, n_trace;
+  double ell_trace[QDWHG_MAX_TRACE];
+  double seconds, flops;
+} qdwhg_polar_info;
+
+typedef enum qdwhg_which {
+  QDWHG_NEGATIVE = 0, /* reference semantics: eigenvalues < 0 of A            */
+  QDWHG_LARGEST = 1,  /* eigenvalues > c of A   (B = c I - A)                  */
+  QDWHG_SMALLEST = 2  /* eigenvalues < c of A   (B = A - c I)                  */
+} qdwhg_which;
+
+typedef struct qdwhg_eig_request {
+  int32_t which;       /* qdwhg_which */
+  int32_t iters;       /* 2 or 3 (choose_shift, partial.cpp:26-30) */
+  double c;            /* spectral shift (ignored for NEGATIVE) */
+  int64_t k;           /* keep the k extreme values by count; 0 = all found */
+  double tol;          /* 0.01 */
+  int32_t randomize;
+  int32_t reserved;
+  uint64_t seed;
+} qdwhg_eig_request;
+
+typedef struct qdwhg_svd_request {
+  int32_t mode;        /* 0: relative s (keep sigma > s*alpha, reference);
+                          1: absolute cut (keep sigma > value; s = value/alpha) */
+  int32_t randomize;
+  double value;
+  int64_t k;           /* keep the k largest by count; 0 = all found */
+  double tol;
+  uint64_t seed;
+} qdwhg_svd_request;
+
+/* ---- handle ------------------------------------------------------------ */
+qdwhg_status qdwhg_create(qdwhg_handle** h, const qdwhg_options* opts);
+qdwhg_status qdwhg_destroy(qdwhg_handle* h);
+const char* qdwhg_last_error(const qdwhg_handle* h);
+qdwhg_status qdwhg_get_launch_count(const qdwhg_handle* h, uint64_t* launches);
+qdwhg_status qdwhg_synchronize(qdwhg_handle* h);
+
+/* ---- drivers ------------------------------------------------------------ */
+qdwhg_status qdwhg_partial_eig(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                               int64_t qdwh_iters, int32_t use_randomization, double tol,
+                               uint64_t seed, double* lambda, double* V, int64_t ldv,
+                               int64_t k_cap, qdwhg_eig_info* info);
+qdwhg_status qdwhg_partial_eig_request(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                               const qdwhg_eig_request* req, double* lambda, double* V,
+                               int64_t ldv, int64_t k_cap, qdwhg_eig_info* info);
+qdwhg_status qdwhg_partial_svd(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                               int64_t lda, double s, double tol, int32_t use_randomization,
+                               uint64_t seed, double* sigma, double* U, int64_t ldu, double* V,
+                               int64_t ldv, int64_t k_cap, qdwhg_svd_info* info);
+qdwhg_status qdwhg_partial_svd_request(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                               int64_t lda, const qdwhg_svd_request* req, double* sigma,
+                               double* U, int64_t ldu, double* V, int64_t ldv, int64_t k_cap,
+                               qdwhg_svd_info* info);
+qdwhg_status qdwhg_polar(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                         const qdwhg_polar_config* cfg, double* Up, int64_t ldu, double* H,
+                         int64_t ldh, qdwhg_polar_info* info);
+
+/* ---- QDWH iteration pieces ----------------------------------------------- */
+/* variant: 0 QrFirst, 1 CholeskyOnly.  trace_out (optional) receives iters+1 values. */
+qdwhg_status qdwhg_run_fixed_iterations(qdwhg_handle* h, int64_t m, int64_t n, const double* X0,
+                                        int64_t ldx, double ell0, int64_t iters, int32_t variant,
+                                        double* X, int64_t ldo, double* trace_out);
+qdwhg_status qdwhg_qdwh_chol_step(qdwhg_handle* h, int64_t m, int64_t n, const double* X,
+                                  int64_t ldx, double ell, double* out, int64_t ldo);
+qdwhg_status qdwhg_qdwh_qr_step(qdwhg_handle* h, int64_t m, int64_t n, const double* X,
+                                int64_t ldx, double ell, double* out, int64_t ldo);
+
+/* ---- dense kernels ---------------------------------------------------- */
+qdwhg_status qdwhg_qr_factor(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                             double* Q, int64_t ldq, double* R, int64_t ldr);
+qdwhg_status qdwhg_cholesky(qdwhg_handle* h, int64_t n, const double* Z, int64_t ldz, double* W,
+                            int64_t ldw);
+qdwhg_status qdwhg_sym_eig_dense(qdwhg_handle* h, int64_t n, const double* S, int64_t lds,
+                                 double* values, double* V, int64_t ldv);
+qdwhg_status qdwhg_svd_dense(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                             double* U, int64_t ldu, double* sigma, double* V, int64_t ldv);
+qdwhg_status qdwhg_two_norm_estimate(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                                     int64_t lda, double* out);
+qdwhg_status qdwhg_lanczos_min_bound(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                                     int64_t steps, double* out);
+/* C = alpha op(A) op(B) + beta C on DEVICE pointers (the DMMA engine itself). */
+qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+                        int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double beta, double* C, int64_t ldc);
+/* Counter-based N(0,1) matrix on the device (kernels.cpp:441-447 scheme, device libm). */
+qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64_t seed, double* A,
+                                   int64_t lda);
+
+/* ---- host scalars (bit-identical to the reference: same libm calls) ---- */
+qdwhg_status qdwhg_halley_weights(double ell, double out5[5]); /* a, b, c, ell_in, ell_out */
+qdwhg_status qdwhg_iterations_to_converge(double ell0, double eps, int64_t max_iters,
+                                          int64_t* out);
+qdwhg_status qdwhg_choose_shift(int64_t qdwh_iters, double* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QDWHG_H */

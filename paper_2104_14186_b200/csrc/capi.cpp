@@ -1,0 +1,697 @@
+// C ABI of libqdwhg (include/qdwhg.h): handle, device arena, host/device
+// pointer detection, exception -> status mapping, and the thin wrappers that
+// stage inputs into padded device buffers, run the device drivers and copy
+// results out.  The reference's C++ entry points it replaces are cited in the
+// header.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/qdwhg.h"
+#include "drivers.hpp"
+
+namespace qdwhg {
+
+// ---------------------------------------------------------------- arena
+Arena::~Arena() {
+  for (auto& c : chunks_) cudaFree(c.base);
+}
+size_t Arena::reserved() const {
+  size_t s = 0;
+  for (auto& c : chunks_) s += c.cap;
+  return s;
+}
+void Arena::reserve(size_t bytes) {
+  if (reserved() >= bytes) return;
+  void* p = nullptr;
+  QDWHG_CUDA(cudaMalloc(&p, bytes - reserved()));
+  chunks_.push_back({static_cast<char*>(p), bytes - reserved()});
+}
+void* Arena::alloc_bytes(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  if (bytes == 0) bytes = 256;
+  while (true) {
+    if (cur_.chunk < chunks_.size()) {
+      Chunk& c = chunks_[cur_.chunk];
+      if (cur_.off + bytes <= c.cap) {
+        void* p = c.base + cur_.off;
+        cur_.off += bytes;
+        size_t used = cur_.off;
+        for (size_t i = 0; i < cur_.chunk; ++i) used += chunks_[i].cap;
+        high_ = std::max(high_, used);
+        return p;
+      }
+      ++cur_.chunk;
+      cur_.off = 0;
+      continue;
+    }
+    // grow: new chunk at least 1 GiB or the request
+    const size_t cap = std::max<size_t>(bytes, size_t(1) << 30);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, cap);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw CapacityError("device workspace exhausted (" + std::to_string(cap >> 20) + " MiB chunk)");
+    }
+    chunks_.push_back({static_cast<char*>(p), cap});
+  }
+}
+DMat Arena::alloc(int64_t rows, int64_t cols) {
+  DMat m;
+  m.ld = round_ld(std::max<int64_t>(rows, 1));
+  m.rows = rows;
+  m.cols = cols;
+  m.base = static_cast<double*>(alloc_bytes(sizeof(double) * m.ld * std::max<int64_t>(cols, 1)));
+  return m;
+}
+
+std::vector<double> host_gaussian(int64_t count, uint64_t seed) {
+  // kernels.cpp:16-32 restated (splitmix64 + Box-Muller on counters 2i, 2i+1);
+  // glibc log/cos, so bit-identical to the reference's gaussian_matrix.
+  std::vector<double> out(count);
+  for (int64_t i = 0; i < count; ++i) {
+    auto h = [&](uint64_t c) {
+      uint64_t z = seed + (c + 1) * 0x9E3779B97F4A7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      return z ^ (z >> 31);
+    };
+    const double u1 = static_cast<double>((h(2 * (uint64_t)i) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>((h(2 * (uint64_t)i + 1) >> 11) + 1) * 0x1.0p-53;
+    out[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  }
+  return out;
+}
+
+}  // namespace qdwhg
+
+using namespace qdwhg;
+
+struct qdwhg_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Arena arena;
+  Ctx ctx;
+  std::string err;
+};
+
+namespace {
+
+template <class F>
+qdwhg_status guard(qdwhg_handle* h, F&& f) {
+  try {
+    if (h) {
+      QDWHG_CUDA(cudaSetDevice(h->device));
+      h->arena.reset();
+    }
+    f();
+    return QDWHG_OK;
+  } catch (const qdwhg::NotPositiveDefinite& e) {
+    if (h) h->err = e.what();
+    return QDWHG_NOT_POSITIVE_DEFINITE;
+  } catch (const qdwhg::NotConverged& e) {
+    if (h) h->err = e.what();
+    return QDWHG_NOT_CONVERGED;
+  } catch (const qdwhg::CapacityError& e) {
+    if (h) h->err = e.what();
+    return QDWHG_CAPACITY;
+  } catch (const qdwhg::CudaError& e) {
+    if (h) h->err = e.what();
+    return QDWHG_CUDA_ERROR;
+  } catch (const std::invalid_argument& e) {
+    if (h) h->err = e.what();
+    return QDWHG_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    if (h) h->err = e.what();
+    return QDWHG_INTERNAL;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void check_ld(int64_t rows, int64_t ld, const char* what) {
+  if (ld < std::max<int64_t>(rows, 1))
+    throw InvalidArgument(std::string(what) + ": leading dimension smaller than rows");
+}
+
+// Stage a caller matrix (host or device) into a fresh padded device buffer.
+DMat stage_in(Ctx& ctx, const double* p, int64_t m, int64_t n, int64_t ld, double* h2d_seconds) {
+  DMat d = ctx.arena->alloc(m, n);
+  if (m == 0 || n == 0) return d;
+  if (is_device_ptr(p)) {
+    QDWHG_CUDA(cudaMemcpy2DAsync(d.ptr(), d.ld * 8, p, ld * 8, m * 8, n, cudaMemcpyDeviceToDevice,
+                                 ctx.stream));
+  } else {
+    cudaEvent_t e0, e1;
+    if (h2d_seconds) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, ctx.stream);
+    }
+    QDWHG_CUDA(cudaMemcpy2DAsync(d.ptr(), d.ld * 8, p, ld * 8, m * 8, n, cudaMemcpyHostToDevice,
+                                 ctx.stream));
+    if (h2d_seconds) {
+      cudaEventRecord(e1, ctx.stream);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      *h2d_seconds += ms * 1e-3;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
+  return d;
+}
+
+void stage_out(Ctx& ctx, const DMat& d, double* p, int64_t ld) {
+  if (!p || d.rows == 0 || d.cols == 0) return;
+  const cudaMemcpyKind kind = is_device_ptr(p) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  QDWHG_CUDA(cudaMemcpy2DAsync(p, ld * 8, d.ptr(), d.ld * 8, d.rows * 8, d.cols, kind, ctx.stream));
+}
+
+void copy_vec_out(Ctx& ctx, const std::vector<double>& v, double* p) {
+  if (!p || v.empty()) return;
+  if (is_device_ptr(p))
+    QDWHG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * 8, cudaMemcpyHostToDevice, ctx.stream));
+  else
+    std::memcpy(p, v.data(), v.size() * 8);
+}
+
+void fill_trace(const std::vector<double>& t, int32_t* n, double* dst) {
+  *n = (int32_t)std::min<size_t>(t.size(), QDWHG_MAX_TRACE);
+  for (int32_t i = 0; i < *n; ++i) dst[i] = t[i];
+}
+
+template <class Info>
+void finish_clock(StageClock& clk, Info* info, double h2d) {
+  double total = 0.0;
+  clk.finish(info->stage_seconds, &total);
+  info->stage_seconds[7] += h2d;
+  info->seconds = total + h2d;
+}
+
+}  // namespace
+
+extern "C" {
+
+qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
+  if (!out) return QDWHG_INVALID_ARGUMENT;
+  *out = nullptr;
+  qdwhg_handle* h = new qdwhg_handle();
+  qdwhg_status st = guard(nullptr, [&] {
+    int dev = opts ? opts->device : -1;
+    if (dev < 0) QDWHG_CUDA(cudaGetDevice(&dev));
+    h->device = dev;
+    QDWHG_CUDA(cudaSetDevice(dev));
+    QDWHG_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    int sms = 148;
+    QDWHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    h->ctx.stream = h->stream;
+    h->ctx.arena = &h->arena;
+    h->ctx.num_sms = sms;
+    QDWHG_CUDA(cudaMalloc(&h->ctx.dscratch, 1 << 16));
+    QDWHG_CUDA(cudaMallocHost(&h->ctx.hscratch, 1 << 16));
+    QDWHG_CUDA(cudaMalloc(&h->ctx.dflag, 256));
+    if (opts && opts->arena_bytes) h->arena.reserve(opts->arena_bytes);
+  });
+  if (st != QDWHG_OK) {
+    delete h;
+    return st;
+  }
+  *out = h;
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_destroy(qdwhg_handle* h) {
+  if (!h) return QDWHG_OK;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  cudaFree(h->ctx.dscratch);
+  cudaFreeHost(h->ctx.hscratch);
+  cudaFree(h->ctx.dflag);
+  cudaStreamDestroy(h->stream);
+  delete h;
+  return QDWHG_OK;
+}
+
+const char* qdwhg_last_error(const qdwhg_handle* h) { return h ? h->err.c_str() : ""; }
+
+qdwhg_status qdwhg_get_launch_count(const qdwhg_handle* h, uint64_t* launches) {
+  if (!h || !launches) return QDWHG_INVALID_ARGUMENT;
+  *launches = h->ctx.gemm_launches + h->ctx.other_launches;
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_synchronize(qdwhg_handle* h) {
+  return guard(h, [&] { QDWHG_CUDA(cudaStreamSynchronize(h->stream)); });
+}
+
+// ---------------------------------------------------------------- drivers
+qdwhg_status qdwhg_partial_eig(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                               int64_t qdwh_iters, int32_t use_randomization, double tol,
+                               uint64_t seed, double* lambda, double* V, int64_t ldv,
+                               int64_t k_cap, qdwhg_eig_info* info) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !A) throw InvalidArgument("qdwh_partial_eig: empty matrix");
+    check_ld(n, lda, "qdwh_partial_eig");
+    qdwhg_eig_info tmp{};
+    qdwhg_eig_info* inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    const double s = choose_shift((size_t)qdwh_iters);
+    Ctx& ctx = h->ctx;
+    double h2d = 0.0;
+    StageClock clk(ctx);
+    DMat Ad = stage_in(ctx, A, n, n, lda, &h2d);
+    EigOut r = partial_eig(ctx, Ad, s, (size_t)qdwh_iters, use_randomization != 0, tol, seed, &clk);
+    const int64_t k = (int64_t)r.lambda.size();
+    if (k > k_cap) throw CapacityError("k exceeds k_cap");
+    if (k > 0) {
+      copy_vec_out(ctx, r.lambda, lambda);
+      check_ld(n, ldv, "V");
+      stage_out(ctx, r.V, V, ldv);
+    }
+    clk.mark(7);
+    finish_clock(clk, inf, h2d);
+    inf->mu = r.mu;
+    inf->shift = r.shift;
+    inf->tol = r.tol;
+    inf->rank_index = (int64_t)r.rank_index;
+    inf->subspace_size = (int64_t)r.subspace_size;
+    inf->k = inf->k_found = k;
+    inf->iters_qr = (int64_t)r.iters_qr;
+    inf->iters_chol = (int64_t)r.iters_chol;
+    inf->borderline = (int64_t)r.borderline;
+    inf->no_savings = r.no_savings;
+    inf->randomized = r.randomized;
+    inf->flops = r.flops;
+    fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
+}
+
+qdwhg_status qdwhg_partial_eig_request(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                               const qdwhg_eig_request* req, double* lambda, double* V,
+                               int64_t ldv, int64_t k_cap, qdwhg_eig_info* info) {
+  if (!h || !req) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !A) throw InvalidArgument("eig_request: empty matrix");
+    check_ld(n, lda, "eig_request");
+    qdwhg_eig_info tmp{};
+    qdwhg_eig_info* inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    const int iters = req->iters ? req->iters : 3;
+    const double s = choose_shift((size_t)iters);
+    const double tol = req->tol > 0 ? req->tol : 0.01;
+    Ctx& ctx = h->ctx;
+    double h2d = 0.0;
+    StageClock clk(ctx);
+    DMat Ad = stage_in(ctx, A, n, n, lda, &h2d);
+    // shift map: LARGEST -> B = cI - A, SMALLEST -> B = A - cI
+    double sign = 1.0;
+    if (req->which == QDWHG_LARGEST) {
+      axpby_identity(ctx, Ad, -1.0, req->c, Ad);
+      sign = -1.0;
+    } else if (req->which == QDWHG_SMALLEST) {
+      axpby_identity(ctx, Ad, 1.0, -req->c, Ad);
+    } else if (req->which != QDWHG_NEGATIVE) {
+      throw InvalidArgument("eig_request: unknown 'which'");
+    }
+    EigOut r = partial_eig(ctx, Ad, s, (size_t)iters, req->randomize != 0, tol, req->seed, &clk);
+    const double c = (req->which == QDWHG_NEGATIVE) ? 0.0 : req->c;
+    int64_t kf = (int64_t)r.lambda.size();
+    int64_t k = kf;
+    // lambda_B ascending (most negative first) == most extreme of A first
+    if (req->k > 0) k = std::min<int64_t>(k, req->k);
+    if (k > k_cap) throw CapacityError("k exceeds k_cap");
+    std::vector<double> lam(k);
+    for (int64_t i = 0; i < k; ++i) lam[i] = (req->which == QDWHG_LARGEST) ? c - r.lambda[i]
+                                            : (req->which == QDWHG_SMALLEST) ? c + r.lambda[i]
+                                                                             : r.lambda[i];
+    (void)sign;
+    if (k > 0) {
+      copy_vec_out(ctx, lam, lambda);
+      check_ld(n, ldv, "V");
+      stage_out(ctx, r.V.sub(0, 0, n, k), V, ldv);
+    }
+    clk.mark(7);
+    finish_clock(clk, inf, h2d);
+    inf->mu = r.mu;
+    inf->shift = r.shift;
+    inf->tol = r.tol;
+    inf->c_shift = c;
+    inf->rank_index = (int64_t)r.rank_index;
+    inf->subspace_size = (int64_t)r.subspace_size;
+    inf->k = k;
+    inf->k_found = kf;
+    inf->iters_qr = (int64_t)r.iters_qr;
+    inf->iters_chol = (int64_t)r.iters_chol;
+    inf->borderline = (int64_t)r.borderline;
+    inf->no_savings = r.no_savings;
+    inf->randomized = r.randomized;
+    inf->flops = r.flops;
+    fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
+}
+
+static qdwhg_status svd_common(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                               double s, double s_abs, int64_t kreq, double tol, int32_t randomize,
+                               uint64_t seed, double* sigma, double* U, int64_t ldu, double* V,
+                               int64_t ldv, int64_t k_cap, qdwhg_svd_info* info) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("qdwh_partial_svd: empty matrix");
+    check_ld(m, lda, "qdwh_partial_svd");
+    qdwhg_svd_info tmp{};
+    qdwhg_svd_info* inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    Ctx& ctx = h->ctx;
+    double h2d = 0.0;
+    StageClock clk(ctx);
+    DMat Ad = stage_in(ctx, A, m, n, lda, &h2d);
+    SvdOut r = partial_svd(ctx, Ad, s, s_abs, tol, randomize != 0, seed, &clk);
+    const int64_t kf = (int64_t)r.sigma.size();
+    int64_t k = kf;
+    if (kreq > 0) k = std::min(k, kreq);
+    if (k > k_cap) throw CapacityError("k exceeds k_cap");
+    if (k > 0) {
+      std::vector<double> sg(r.sigma.begin(), r.sigma.begin() + k);
+      copy_vec_out(ctx, sg, sigma);
+      if (U) {
+        check_ld(m, ldu, "U");
+        stage_out(ctx, r.U.sub(0, 0, m, k), U, ldu);
+      }
+      if (V) {
+        check_ld(n, ldv, "V");
+        stage_out(ctx, r.V.sub(0, 0, n, k), V, ldv);
+      }
+    }
+    clk.mark(7);
+    finish_clock(clk, inf, h2d);
+    inf->alpha = r.alpha;
+    inf->threshold = r.threshold;
+    inf->tol = r.tol;
+    inf->cut = r.threshold * r.alpha;
+    inf->rank_index = (int64_t)r.rank_index;
+    inf->subspace_size = (int64_t)r.subspace_size;
+    inf->k = k;
+    inf->k_found = kf;
+    inf->iters_qr = (int64_t)r.iters_qr;
+    inf->iters_chol = (int64_t)r.iters_chol;
+    inf->no_savings = r.no_savings;
+    inf->randomized = r.randomized;
+    inf->flops = r.flops;
+    fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
+}
+
+qdwhg_status qdwhg_partial_svd(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                               int64_t lda, double s, double tol, int32_t use_randomization,
+                               uint64_t seed, double* sigma, double* U, int64_t ldu, double* V,
+                               int64_t ldv, int64_t k_cap, qdwhg_svd_info* info) {
+  return svd_common(h, m, n, A, lda, s, 0.0, 0, tol, use_randomization, seed, sigma, U, ldu, V, ldv,
+                    k_cap, info);
+}
+
+qdwhg_status qdwhg_partial_svd_request(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                               int64_t lda, const qdwhg_svd_request* req, double* sigma,
+                               double* U, int64_t ldu, double* V, int64_t ldv, int64_t k_cap,
+                               qdwhg_svd_info* info) {
+  if (!req) return QDWHG_INVALID_ARGUMENT;
+  const double tol = req->tol > 0 ? req->tol : 0.01;
+  if (req->mode == 1) {
+    if (!(req->value > 0.0)) {
+      if (h) h->err = "svd_request: absolute cut must be positive";
+      return QDWHG_INVALID_ARGUMENT;
+    }
+    return svd_common(h, m, n, A, lda, 0.0, req->value, req->k, tol, req->randomize, req->seed,
+                      sigma, U, ldu, V, ldv, k_cap, info);
+  }
+  return svd_common(h, m, n, A, lda, req->value, 0.0, req->k, tol, req->randomize, req->seed, sigma,
+                    U, ldu, V, ldv, k_cap, info);
+}
+
+qdwhg_status qdwhg_polar(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                         const qdwhg_polar_config* cfg, double* Up, int64_t ldu, double* H,
+                         int64_t ldh, qdwhg_polar_info* info) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("polar_decompose: empty matrix");
+    check_ld(m, lda, "polar_decompose");
+    Ctx& ctx = h->ctx;
+    StageClock clk(ctx);
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    {
+      const MatStats st = mat_stats(ctx, Ad, false);
+      if (st.nonfinite > 0) throw InvalidArgument("polar_decompose: non-finite entry");
+    }
+    PolarCfg pc;
+    if (cfg) {
+      pc.ell0 = cfg->ell0;
+      pc.max_iters = (size_t)cfg->max_iters;
+      pc.conv_eps = cfg->conv_eps;
+      pc.chol_switch_c = cfg->chol_switch_c;
+      pc.force_variant = cfg->force_variant;
+    }
+    DMat Upd = ctx.arena->alloc(m, n);
+    DMat Hd = ctx.arena->alloc(n, n);
+    PolarOut r = polar_decompose(ctx, Ad, pc, Upd, Hd);
+    stage_out(ctx, Upd, Up, ldu);
+    stage_out(ctx, Hd, H, ldh);
+    clk.mark(7);
+    if (info) {
+      std::memset(info, 0, sizeof(*info));
+      double total = 0;
+      clk.finish(nullptr, &total);
+      info->seconds = total;
+      info->alpha = r.alpha;
+      info->iters_qr = (int64_t)r.iters_qr;
+      info->iters_chol = (int64_t)r.iters_chol;
+      info->converged = 1;
+      info->flops = r.flops;
+      fill_trace(r.trace, &info->n_trace, info->ell_trace);
+    }
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+// ---------------------------------------------------------------- pieces
+qdwhg_status qdwhg_run_fixed_iterations(qdwhg_handle* h, int64_t m, int64_t n, const double* X0,
+                                        int64_t ldx, double ell0, int64_t iters, int32_t variant,
+                                        double* X, int64_t ldo, double* trace_out) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !X0) throw InvalidArgument("run_fixed_iterations: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Xd = stage_in(ctx, X0, m, n, ldx, nullptr);
+    if (mat_stats(ctx, Xd, false).nonfinite > 0)
+      throw InvalidArgument("run_fixed_iterations: non-finite entry");
+    FixedIterResult r = run_fixed_iterations(ctx, Xd, ell0, (size_t)std::max<int64_t>(iters, 0),
+                                             variant == 0);
+    stage_out(ctx, Xd, X, ldo);
+    if (trace_out)
+      for (size_t i = 0; i < r.trace.size(); ++i) trace_out[i] = r.trace[i];
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_qdwh_chol_step(qdwhg_handle* h, int64_t m, int64_t n, const double* X,
+                                  int64_t ldx, double ell, double* out, int64_t ldo) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    Ctx& ctx = h->ctx;
+    DMat Xd = stage_in(ctx, X, m, n, ldx, nullptr);
+    if (mat_stats(ctx, Xd, false).nonfinite > 0) throw InvalidArgument("qdwh_chol_step: non-finite entry");
+    DMat Od = ctx.arena->alloc(m, n);
+    qdwh_chol_step(ctx, Xd, halley_weights(ell), Od);
+    stage_out(ctx, Od, out, ldo);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_qdwh_qr_step(qdwhg_handle* h, int64_t m, int64_t n, const double* X,
+                                int64_t ldx, double ell, double* out, int64_t ldo) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    Ctx& ctx = h->ctx;
+    DMat Xd = stage_in(ctx, X, m, n, ldx, nullptr);
+    if (mat_stats(ctx, Xd, false).nonfinite > 0) throw InvalidArgument("qdwh_qr_step: non-finite entry");
+    DMat Od = ctx.arena->alloc(m, n);
+    qdwh_qr_step(ctx, Xd, halley_weights(ell), Od);
+    stage_out(ctx, Od, out, ldo);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_qr_factor(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                             double* Q, int64_t ldq, double* R, int64_t ldr) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("qr_factor: empty matrix");
+    if (m < n) throw InvalidArgument("qr_factor: requires rows >= cols");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0) throw InvalidArgument("qr_factor: non-finite entry");
+    QrWork qw;
+    geqrf(ctx, Ad, qw);
+    if (Q) {
+      DMat Qd = ctx.arena->alloc(m, m);
+      orgqr_cols(ctx, qw, m, n, 0, Qd);
+      stage_out(ctx, Qd, Q, ldq);
+    }
+    stage_out(ctx, Ad, R, ldr);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_cholesky(qdwhg_handle* h, int64_t n, const double* Z, int64_t ldz, double* W,
+                            int64_t ldw) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !Z) throw InvalidArgument("cholesky: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Zd = stage_in(ctx, Z, n, n, ldz, nullptr);
+    if (mat_stats(ctx, Zd, false).nonfinite > 0) throw InvalidArgument("cholesky: non-finite entry");
+    DMat Wi = ctx.arena->alloc(n, n);
+    potrf_upper_and_inverse(ctx, Zd, Wi);
+    stage_out(ctx, Zd, W, ldw);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_sym_eig_dense(qdwhg_handle* h, int64_t n, const double* S, int64_t lds,
+                                 double* values, double* V, int64_t ldv) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !S) throw InvalidArgument("sym_eig_dense: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Sd = stage_in(ctx, S, n, n, lds, nullptr);
+    const MatStats st = mat_stats(ctx, Sd, true);
+    if (st.nonfinite > 0) throw InvalidArgument("sym_eig_dense: non-finite entry");
+    if (st.asym > 1e3 * (double)n * 2.220446049250313e-16 * std::max(1.0, std::sqrt(st.fro2)))
+      throw InvalidArgument("sym_eig_dense: input not symmetric within tolerance");
+    DMat Vd = ctx.arena->alloc(n, n);
+    std::vector<double> vals;
+    syev(ctx, Sd, vals, Vd);
+    copy_vec_out(ctx, vals, values);
+    stage_out(ctx, Vd, V, ldv);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_svd_dense(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                             double* U, int64_t ldu, double* sigma, double* V, int64_t ldv) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("svd_dense: empty matrix");
+    if (m < n) throw InvalidArgument("svd_dense: requires rows >= cols on the device path");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0) throw InvalidArgument("svd_dense: non-finite entry");
+    DMat Ud = ctx.arena->alloc(m, n), Vd = ctx.arena->alloc(n, n);
+    std::vector<double> sg;
+    svd_polar(ctx, Ad, Ud, sg, Vd);
+    copy_vec_out(ctx, sg, sigma);
+    stage_out(ctx, Ud, U, ldu);
+    stage_out(ctx, Vd, V, ldv);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_two_norm_estimate(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                                     int64_t lda, double* out) {
+  if (!h || !out) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("two_norm_estimate: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0)
+      throw InvalidArgument("two_norm_estimate: non-finite entry");
+    *out = two_norm_estimate(ctx, Ad);
+  });
+}
+
+qdwhg_status qdwhg_lanczos_min_bound(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                                     int64_t steps, double* out) {
+  if (!h || !out) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !A) throw InvalidArgument("lanczos_min_bound: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, n, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0)
+      throw InvalidArgument("lanczos_min_bound: non-finite entry");
+    *out = lanczos_min_bound(ctx, Ad, (int)steps);
+  });
+}
+
+qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+                        int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+                        int64_t ldb, double beta, double* C, int64_t ldc) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    DMat Ad, Bd, Cd;
+    Ad.base = const_cast<double*>(A);
+    Ad.ld = lda;
+    Ad.rows = trans_a ? k : m;
+    Ad.cols = trans_a ? m : k;
+    Bd.base = const_cast<double*>(B);
+    Bd.ld = ldb;
+    Bd.rows = trans_b ? n : k;
+    Bd.cols = trans_b ? k : n;
+    Cd.base = C;
+    Cd.ld = ldc;
+    Cd.rows = m;
+    Cd.cols = n;
+    if (!is_device_ptr(A) || !is_device_ptr(B) || !is_device_ptr(C))
+      throw InvalidArgument("qdwhg_gemm: operands must be device pointers");
+    gemm(h->ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cd);
+    QDWHG_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64_t seed, double* A,
+                                   int64_t lda) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (!is_device_ptr(A)) throw InvalidArgument("qdwhg_gaussian_matrix: A must be a device pointer");
+    DMat Ad;
+    Ad.base = A;
+    Ad.ld = lda;
+    Ad.rows = m;
+    Ad.cols = n;
+    gaussian_fill(h->ctx, Ad, seed);
+    QDWHG_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+qdwhg_status qdwhg_halley_weights(double ell, double out5[5]) {
+  return guard(nullptr, [&] {
+    const WeightStep w = halley_weights(ell);
+    out5[0] = w.a;
+    out5[1] = w.b;
+    out5[2] = w.c;
+    out5[3] = w.ell_in;
+    out5[4] = w.ell_out;
+  });
+}
+
+qdwhg_status qdwhg_iterations_to_converge(double ell0, double eps, int64_t max_iters,
+                                          int64_t* out) {
+  return guard(nullptr, [&] { *out = (int64_t)iterations_to_converge(ell0, eps, (size_t)max_iters); });
+}
+
+qdwhg_status qdwhg_choose_shift(int64_t qdwh_iters, double* s) {
+  return guard(nullptr, [&] { *s = choose_shift((size_t)qdwh_iters); });
+}
+
+}  // extern "C"

@@ -1,0 +1,511 @@
+// QDWH iteration, polar decomposition and the QDWHpartial drivers on device
+// views.  Control flow, constants, seeds and edge cases restate the reference
+// (file:line cited per function); all matrix work runs in our sm_100a kernels.
+#include "drivers.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <sstream>
+
+namespace qdwhg {
+
+constexpr double kEps = 2.220446049250313e-16;
+extern const int kJacobiMaxN;
+void syev_jacobi(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+void permute_cols(Ctx& ctx, const DMat& V, const std::vector<int>& order, const DMat& Vout);
+
+// ----------------------------------------------------------------- scalars
+WeightStep halley_weights(double ell) {  // polar.cpp:12-27 (same libm calls, same order)
+  if (!(ell > 0.0) || ell > 1.0) throw InvalidArgument("halley_weights: ell must be in (0, 1]");
+  const double l2 = ell * ell;
+  const double dd = std::cbrt(4.0 * (1.0 - l2)) * std::pow(ell, -4.0 / 3.0);
+  const double sqd = std::sqrt(1.0 + dd);
+  const double inner = 8.0 - 4.0 * dd + 8.0 * (2.0 - l2) / (l2 * sqd);
+  WeightStep w;
+  w.a = sqd + std::sqrt(inner) / 2.0;
+  w.b = (w.a - 1.0) * (w.a - 1.0) / 4.0;
+  w.c = w.a + w.b - 1.0;
+  w.ell_in = ell;
+  w.ell_out = ell * (w.a + w.b * l2) / (1.0 + w.c * l2);
+  return w;
+}
+
+size_t iterations_to_converge(double ell0, double eps, size_t max_iters) {  // polar.cpp:40-51
+  double ell = ell0;
+  for (size_t k = 0; k < max_iters; ++k) {
+    if (std::abs(ell - 1.0) < eps) return k;
+    ell = halley_weights(ell).ell_out;
+  }
+  if (std::abs(ell - 1.0) < eps) return max_iters;
+  std::ostringstream msg;
+  msg << "ell recurrence from " << ell0 << " not within " << eps << " of 1 after " << max_iters
+      << " steps (ell = " << ell << ")";
+  throw NotConverged(msg.str());
+}
+
+double choose_shift(size_t iters) {  // partial.cpp:26-30
+  if (iters == 2) return 0.875;
+  if (iters == 3) return 0.2;
+  throw InvalidArgument("choose_shift: unsupported plan, tabulated iteration counts are 2 and 3");
+}
+
+// ----------------------------------------------------------------- stage clock
+StageClock::StageClock(Ctx& c) : ctx(c) {
+  cudaEvent_t e;
+  QDWHG_CUDA(cudaEventCreate(&e));
+  QDWHG_CUDA(cudaEventRecord(e, ctx.stream));
+  ev.push_back(e);
+  owner.push_back(-1);
+}
+StageClock::~StageClock() {
+  for (auto e : ev) cudaEventDestroy(e);
+}
+void StageClock::mark(int stage) {
+  cudaEvent_t e;
+  QDWHG_CUDA(cudaEventCreate(&e));
+  QDWHG_CUDA(cudaEventRecord(e, ctx.stream));
+  ev.push_back(e);
+  owner.push_back(stage);
+}
+void StageClock::finish(double* stage_seconds, double* total) {
+  QDWHG_CUDA(cudaEventSynchronize(ev.back()));
+  for (size_t i = 1; i < ev.size(); ++i) {
+    float ms = 0.f;
+    QDWHG_CUDA(cudaEventElapsedTime(&ms, ev[i - 1], ev[i]));
+    if (stage_seconds && owner[i] >= 0 && owner[i] < 8) stage_seconds[owner[i]] += ms * 1e-3;
+  }
+  if (total) {
+    float ms = 0.f;
+    QDWHG_CUDA(cudaEventElapsedTime(&ms, ev.front(), ev.back()));
+    *total = ms * 1e-3;
+  }
+}
+
+// ----------------------------------------------------------------- QDWH steps
+void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout) {
+  // polar.cpp:82-128:  Z = I + c sym(X^T X);  W = chol(Z);  X+ = (b/c) X + (a - b/c) X W^-1 W^-T
+  const int64_t m = X.rows, n = X.cols;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat Z = ctx.arena->alloc(n, n);
+  DMat Winv = ctx.arena->alloc(n, n);
+  GemmExtra syrk;
+  syrk.out = OutMode::LowerMirror;  // symmetric by construction (one dot product per pair)
+  syrk.diag_add = 1.0;
+  gemm(ctx, Op::T, Op::N, w.c, X, X, 0.0, Z, syrk);
+  try {
+    potrf_upper_and_inverse(ctx, Z, Winv);
+  } catch (...) {
+    ctx.arena->release_to(mark);
+    throw;
+  }
+  DMat Y = ctx.arena->alloc(m, n);
+  GemmExtra t1;
+  t1.krange = KRange::BUpper;  // W^-1 upper
+  gemm(ctx, Op::N, Op::N, 1.0, X, Winv, 0.0, Y, t1);
+  const double bc = w.b / w.c;
+  const double coef = w.a - bc;
+  GemmExtra t2;
+  t2.krange = KRange::BLower;  // (W^-1)^T lower
+  t2.cin = &X;                 // fused weight update (b/c) X + (a - b/c) G
+  gemm(ctx, Op::N, Op::T, coef, Y, Winv, bc, Xout, t2);
+  ctx.arena->release_to(mark);
+}
+
+void qdwh_qr_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout) {
+  // polar.cpp:53-80: QR of [sqrt(c) X; I], X+ = (b/c) X + ((a - b/c)/sqrt(c)) Q1 Q2^T
+  const int64_t m = X.rows, n = X.cols;
+  const double sc = std::sqrt(w.c);
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat S = ctx.arena->alloc(m + n, n);
+  axpby_identity(ctx, X, sc, 0.0, S.sub(0, 0, m, n));
+  fill(ctx, S.sub(m, 0, n, n), 0.0, 1.0);
+  QrWork qw;
+  geqrf(ctx, S, qw);
+  DMat Q = ctx.arena->alloc(m + n, n);
+  orgqr_cols(ctx, qw, m + n, n, 0, Q);
+  const double bc = w.b / w.c;
+  const double coef = (w.a - bc) / sc;
+  GemmExtra e;
+  e.cin = &X;
+  gemm(ctx, Op::N, Op::T, coef, Q.sub(0, 0, m, n), Q.sub(m, 0, n, n), bc, Xout, e);
+  ctx.arena->release_to(mark);
+}
+
+static bool is_symmetric(Ctx& ctx, const DMat& X) {
+  if (X.rows != X.cols) return false;
+  const MatStats st = mat_stats(ctx, X, true);
+  return st.asym <= 1e3 * (double)X.rows * kEps * std::max(1.0, std::sqrt(st.fro2));
+}
+
+FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_t iters,
+                                     bool qr_first) {
+  // polar.cpp:179-215
+  if (!(ell0 > 0.0) || ell0 > 1.0)
+    throw InvalidArgument("run_fixed_iterations: ell0 must be in (0, 1]");
+  if (iters < 1) throw InvalidArgument("run_fixed_iterations: iters must be >= 1");
+  const bool symmetric = is_symmetric(ctx, X);
+  FixedIterResult r;
+  r.ell = ell0;
+  r.trace.push_back(ell0);
+  for (size_t k = 0; k < iters; ++k) {
+    const WeightStep w = halley_weights(r.ell);
+    if (qr_first && k == 0) {
+      qdwh_qr_step(ctx, X, w, X);
+      ++r.iters_qr;
+    } else {
+      qdwh_chol_step(ctx, X, w, X);
+      ++r.iters_chol;
+    }
+    if (symmetric) symmetrize_scale(ctx, X, 1.0, 0.0, X);
+    r.ell = w.ell_out;
+    r.trace.push_back(r.ell);
+  }
+  return r;
+}
+
+PolarOut polar_decompose(Ctx& ctx, const DMat& A, const PolarCfg& cfg, const DMat& Up,
+                         const DMat& H) {
+  // polar.cpp:130-177
+  const int64_t m = A.rows, n = A.cols;
+  if (m < n) throw InvalidArgument("polar_decompose: requires rows >= cols");
+  if (!(cfg.ell0 > 0.0) || cfg.ell0 > 1.0)
+    throw InvalidArgument("polar_decompose: ell0 must be in (0, 1]");
+  PolarOut out;
+  out.alpha = two_norm_estimate(ctx, A);
+  axpby_identity(ctx, A, 1.0 / out.alpha, 0.0, Up);
+  double ell = cfg.ell0 / 1.10;
+  out.trace.push_back(ell);
+  const double stop = 5.0 * cfg.conv_eps;
+  const double md = (double)m, nd = (double)n;
+  while (std::abs(ell - 1.0) >= stop) {
+    if (out.iters_qr + out.iters_chol >= cfg.max_iters) {
+      std::ostringstream msg;
+      msg << "polar_decompose: no convergence after " << cfg.max_iters << " iterations (ell = " << ell
+          << ")";
+      throw NotConverged(msg.str());
+    }
+    const WeightStep w = halley_weights(ell);
+    bool use_chol = w.c <= cfg.chol_switch_c;
+    if (cfg.force_variant == 1) use_chol = false;
+    if (cfg.force_variant == 2) use_chol = true;
+    if (use_chol) {
+      try {
+        qdwh_chol_step(ctx, Up, w, Up);
+        ++out.iters_chol;
+        out.flops += 3 * md * nd * nd + nd * nd * nd / 3;
+      } catch (const NotPositiveDefinite&) {
+        if (cfg.force_variant == 2) throw;
+        qdwh_qr_step(ctx, Up, w, Up);
+        ++out.iters_qr;
+        out.flops += 6 * md * nd * nd + 8.0 / 3.0 * nd * nd * nd;
+      }
+    } else {
+      qdwh_qr_step(ctx, Up, w, Up);
+      ++out.iters_qr;
+      out.flops += 6 * md * nd * nd + 8.0 / 3.0 * nd * nd * nd;
+    }
+    ell = w.ell_out;
+    out.trace.push_back(ell);
+  }
+  if (H.base) {
+    // H = sym(Up^T A)  (polar.cpp:175)
+    gemm(ctx, Op::T, Op::N, 1.0, Up, A, 0.0, H);
+    symmetrize_scale(ctx, H, 1.0, 0.0, H);
+    out.flops += 2 * md * nd * nd;
+  }
+  return out;
+}
+
+// ----------------------------------------------------------------- dense EIG / SVD
+static double device_trace(Ctx& ctx, const DMat& A) {
+  std::vector<double> d;
+  diag_to_host(ctx, A, d);
+  double t = 0.0;
+  for (double x : d) t += x;
+  return t;
+}
+
+// Spectral divide-and-conquer (fullsolve.cpp:22-72 strategy) for blocks larger
+// than the single-CTA Jacobi: polar of A - sigma I gives the spectral projector
+// C = (I - Up)/2 onto eigenvalues below sigma; a randomized QR of C splits the
+// space; recurse on the two Rayleigh quotients.
+static void syev_dc(Ctx& ctx, const DMat& A, std::vector<double>& vals, const DMat& Vout,
+                    int depth) {
+  const int64_t n = A.rows;
+  if (n <= kJacobiMaxN) {
+    syev_jacobi(ctx, A, vals, Vout);
+    return;
+  }
+  const Arena::Mark mark = ctx.arena->mark();
+  const double sigma0 = device_trace(ctx, A) / (double)n;
+  DMat Sh = ctx.arena->alloc(n, n);
+  const MatStats st = mat_stats(ctx, A, false);
+  const double fro = std::sqrt(st.fro2);
+  // candidate split points: the mean, then points between mean and the Gershgorin-free
+  // Frobenius bound if the mean splits nothing off
+  const double spread = fro / std::sqrt((double)n);
+  const double cand[5] = {sigma0, sigma0 + 0.5 * spread, sigma0 - 0.5 * spread,
+                          sigma0 + 0.25 * spread, sigma0 - 0.25 * spread};
+  DMat Up = ctx.arena->alloc(n, n);
+  int64_t k = 0;
+  double sigma = sigma0;
+  for (int attempt = 0; attempt < 5; ++attempt) {
+    sigma = cand[attempt];
+    axpby_identity(ctx, A, 1.0, -sigma, Sh);
+    const MatStats ss = mat_stats(ctx, Sh, false);
+    if (std::sqrt(ss.fro2) <= 10.0 * (double)n * kEps * std::max(1.0, std::abs(sigma))) {
+      // constant-diagonal block (fullsolve.cpp:31-38)
+      vals.assign(n, sigma);
+      fill(ctx, Vout, 0.0, 1.0);
+      ctx.arena->release_to(mark);
+      return;
+    }
+    PolarCfg cfg;
+    cfg.ell0 = 1e-15;
+    DMat none;
+    polar_decompose(ctx, Sh, cfg, Up, none);
+    // C = sym((I - Up)/2), k = round(trace C)
+    symmetrize_scale(ctx, Up, -0.5, 0.5, Up);
+    k = std::llround(device_trace(ctx, Up));
+    if (k > 0 && k < n) break;
+  }
+  if (k <= 0 || k >= n) throw NotConverged("syev: spectral divide-and-conquer found no split");
+  DMat Om = ctx.arena->alloc(n, n);
+  gaussian_fill(ctx, Om, 0x73706c6974ull + (uint64_t)depth);  // kSplitSeed, fullsolve.cpp:14
+  DMat CO = ctx.arena->alloc(n, n);
+  gemm(ctx, Op::N, Op::N, 1.0, Up, Om, 0.0, CO);
+  QrWork qw;
+  geqrf(ctx, CO, qw);
+  DMat Q = ctx.arena->alloc(n, n);
+  orgqr_cols(ctx, qw, n, n, 0, Q);
+  const DMat Vlo = Q.sub(0, 0, n, k), Vhi = Q.sub(0, k, n, n - k);
+  DMat T = ctx.arena->alloc(n, n);
+  std::vector<double> vlo, vhi;
+  DMat Alo = ctx.arena->alloc(k, k), Ahi = ctx.arena->alloc(n - k, n - k);
+  {
+    gemm(ctx, Op::N, Op::N, 1.0, A, Vlo, 0.0, T.sub(0, 0, n, k));
+    gemm(ctx, Op::T, Op::N, 1.0, Vlo, T.sub(0, 0, n, k), 0.0, Alo);
+    symmetrize_scale(ctx, Alo, 1.0, 0.0, Alo);
+    gemm(ctx, Op::N, Op::N, 1.0, A, Vhi, 0.0, T.sub(0, 0, n, n - k));
+    gemm(ctx, Op::T, Op::N, 1.0, Vhi, T.sub(0, 0, n, n - k), 0.0, Ahi);
+    symmetrize_scale(ctx, Ahi, 1.0, 0.0, Ahi);
+  }
+  DMat Wlo = ctx.arena->alloc(k, k), Whi = ctx.arena->alloc(n - k, n - k);
+  syev_dc(ctx, Alo, vlo, Wlo, depth + 1);
+  syev_dc(ctx, Ahi, vhi, Whi, depth + 1);
+  gemm(ctx, Op::N, Op::N, 1.0, Vlo, Wlo, 0.0, Vout.sub(0, 0, n, k));
+  gemm(ctx, Op::N, Op::N, 1.0, Vhi, Whi, 0.0, Vout.sub(0, k, n, n - k));
+  vals = vlo;
+  vals.insert(vals.end(), vhi.begin(), vhi.end());
+  ctx.arena->release_to(mark);
+}
+
+void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
+  syev_dc(ctx, S, vals, Vout, 0);
+}
+
+void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V) {
+  // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order
+  const int64_t m = A.rows, n = A.cols;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat Up = ctx.arena->alloc(m, n);
+  DMat H = ctx.arena->alloc(n, n);
+  PolarCfg cfg;
+  cfg.ell0 = 1e-15;
+  polar_decompose(ctx, A, cfg, Up, H);
+  std::vector<double> vals;
+  DMat W = ctx.arena->alloc(n, n);
+  syev(ctx, H, vals, W);
+  // reverse to descending
+  std::vector<int> order(n);
+  for (int64_t j = 0; j < n; ++j) order[j] = (int)(n - 1 - j);
+  sigma.resize(n);
+  for (int64_t j = 0; j < n; ++j) sigma[j] = std::max(0.0, vals[order[j]]);
+  permute_cols(ctx, W, order, V);  // V(:, j) = W(:, n-1-j)
+  gemm(ctx, Op::N, Op::N, 1.0, Up, V, 0.0, U);
+  ctx.arena->release_to(mark);
+}
+
+// ----------------------------------------------------------------- drivers
+static void check_finite(Ctx& ctx, const DMat& A, const char* who, MatStats* out = nullptr,
+                         bool asym = false) {
+  if (A.rows == 0 || A.cols == 0) throw InvalidArgument(std::string(who) + ": empty matrix");
+  const MatStats st = mat_stats(ctx, A, asym);
+  if (st.nonfinite > 0) throw InvalidArgument(std::string(who) + ": non-finite entry");
+  if (out) *out = st;
+}
+
+EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomize, double tol,
+                   uint64_t seed, StageClock* clk) {
+  // partial.cpp:40-99
+  const int64_t n = A.rows;
+  if (A.cols != n) throw InvalidArgument("qdwh_partial_eig: matrix not square");
+  MatStats st;
+  check_finite(ctx, A, "qdwh_partial_eig", &st, true);
+  if (st.asym > 1e3 * (double)n * kEps * std::max(1.0, std::sqrt(st.fro2)))
+    throw InvalidArgument("qdwh_partial_eig: input not symmetric within tolerance");
+  EigOut out;
+  out.shift = s;
+  out.tol = tol;
+  out.randomized = randomize;
+  out.mu = lanczos_min_bound(ctx, A, 30);
+  if (clk) clk->mark(0);
+  if (out.mu >= 0.0) return out;  // partial.cpp:52
+  const double scale = std::abs(out.mu);
+  DMat As = ctx.arena->alloc(n, n);
+  symmetrize_scale(ctx, A, 1.0 / scale, 0.0, As);
+  DMat X = ctx.arena->alloc(n, n);
+  axpby_identity(ctx, As, 1.0 - s, -s, X);
+  FixedIterResult it = run_fixed_iterations(ctx, X, s, iters, false);
+  out.trace = it.trace;
+  out.iters_qr = it.iters_qr;
+  out.iters_chol = it.iters_chol;
+  if (clk) clk->mark(1);
+  // B = (r(A~) + I)/2 (partial.cpp:67-69)
+  axpby_identity(ctx, X, 0.5, 0.5, X);
+  DMat B = X;
+  if (randomize) {
+    DMat Om = ctx.arena->alloc(n, n);
+    gaussian_fill(ctx, Om, seed);
+    B = ctx.arena->alloc(n, n);
+    gemm(ctx, Op::N, Op::N, 1.0, X, Om, 0.0, B);
+  }
+  QrWork qw;
+  geqrf(ctx, B, qw);
+  std::vector<double> d;
+  diag_to_host(ctx, B, d);
+  if (clk) clk->mark(2);
+  size_t ind = 0;  // detect_deficiency_index, partial.cpp:32-38
+  for (size_t i = 0; i < d.size(); ++i)
+    if (std::abs(d[i]) < tol) {
+      ind = i + 1;
+      break;
+    }
+  const double nd = (double)n;
+  out.flops = it.iters_chol * (10.0 / 3.0) * nd * nd * nd + 4.0 / 3.0 * nd * nd * nd +
+              (randomize ? 2 * nd * nd * nd : 0.0);
+  if (ind == 0) return out;
+  out.rank_index = ind;
+  const int64_t ell = n - (int64_t)ind + 1;
+  out.subspace_size = ell;
+  out.no_savings = ell > n / 2;
+  DMat Q2 = ctx.arena->alloc(n, ell);
+  orgqr_cols(ctx, qw, n, n, (int64_t)ind - 1, Q2);
+  if (clk) clk->mark(3);
+  DMat AQ = ctx.arena->alloc(n, ell);
+  gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ);
+  DMat S = ctx.arena->alloc(ell, ell);
+  gemm(ctx, Op::T, Op::N, 1.0, Q2, AQ, 0.0, S);
+  symmetrize_scale(ctx, S, 1.0, 0.0, S);
+  if (clk) clk->mark(4);
+  std::vector<double> vals;
+  DMat W = ctx.arena->alloc(ell, ell);
+  syev(ctx, S, vals, W);
+  if (clk) clk->mark(5);
+  double max_abs_ritz = 0.0;
+  for (double v : vals) max_abs_ritz = std::max(max_abs_ritz, std::abs(v));
+  const double floor = -nd * kEps * max_abs_ritz;
+  int64_t k = 0;
+  while (k < ell && vals[k] < 0.0) ++k;
+  const double l = (double)ell;
+  out.flops += 2 * nd * nd * l - 2 * l * l * l / 3 + 2 * nd * nd * l + 2 * nd * l * l + 9 * l * l * l;
+  if (k == 0) return out;
+  out.lambda.resize(k);
+  for (int64_t i = 0; i < k; ++i) {
+    out.lambda[i] = scale * vals[i];
+    if (vals[i] >= floor) ++out.borderline;
+  }
+  out.V = ctx.arena->alloc(n, k);
+  gemm(ctx, Op::N, Op::N, 1.0, Q2, W.sub(0, 0, ell, k), 0.0, out.V);
+  out.flops += 2 * nd * l * (double)k;
+  if (clk) clk->mark(6);
+  return out;
+}
+
+SvdOut partial_svd(Ctx& ctx, const DMat& A, double s, double s_abs, double tol, bool randomize,
+                   uint64_t seed, StageClock* clk) {
+  // partial.cpp:101-158
+  const int64_t m = A.rows, n = A.cols;
+  check_finite(ctx, A, "qdwh_partial_svd");
+  if (m < n) throw InvalidArgument("qdwh_partial_svd: requires rows >= cols");
+  SvdOut out;
+  out.tol = tol;
+  out.randomized = randomize;
+  out.alpha = two_norm_estimate(ctx, A);
+  if (s_abs > 0.0) s = s_abs / out.alpha;
+  if (!(s > 0.0) || s >= 1.0)
+    throw InvalidArgument("qdwh_partial_svd: threshold s must be in (0, 1)");
+  out.threshold = s;
+  if (clk) clk->mark(0);
+  DMat X = ctx.arena->alloc(m, n);
+  axpby_identity(ctx, A, 1.0 / out.alpha, 0.0, X);
+  const size_t iters = iterations_to_converge(s, 5.0 * kEps);
+  if (iters > 0) {
+    FixedIterResult it = run_fixed_iterations(ctx, X, s, iters, s < 1e-3);
+    out.trace = it.trace;
+    out.iters_qr = it.iters_qr;
+    out.iters_chol = it.iters_chol;
+  } else {
+    out.trace.push_back(s);
+  }
+  if (clk) clk->mark(1);
+  // M = I - sym(X^T X) (partial.cpp:134-136)
+  DMat M = ctx.arena->alloc(n, n);
+  GemmExtra syrk;
+  syrk.out = OutMode::LowerMirror;
+  syrk.diag_add = 1.0;
+  gemm(ctx, Op::T, Op::N, -1.0, X, X, 0.0, M, syrk);
+  DMat B = M;
+  if (randomize) {
+    DMat Om = ctx.arena->alloc(n, n);
+    gaussian_fill(ctx, Om, seed);
+    B = ctx.arena->alloc(n, n);
+    gemm(ctx, Op::N, Op::N, 1.0, M, Om, 0.0, B);
+  }
+  QrWork qw;
+  geqrf(ctx, B, qw);
+  std::vector<double> d;
+  diag_to_host(ctx, B, d);
+  if (clk) clk->mark(2);
+  size_t ind = 0;
+  for (size_t i = 0; i < d.size(); ++i)
+    if (std::abs(d[i]) < tol) {
+      ind = i + 1;
+      break;
+    }
+  const double md = (double)m, nd = (double)n;
+  out.flops = out.iters_qr * (6 * md * nd * nd + 8.0 / 3.0 * nd * nd * nd) +
+              out.iters_chol * (3 * md * nd * nd + nd * nd * nd / 3) + md * nd * nd +
+              4.0 / 3.0 * nd * nd * nd + (randomize ? 2 * nd * nd * nd : 0.0);
+  if (ind == 0) return out;
+  out.rank_index = ind;
+  const int64_t ell = n - (int64_t)ind + 1;
+  out.subspace_size = ell;
+  out.no_savings = ell > n / 2;
+  DMat Q2 = ctx.arena->alloc(n, ell);
+  orgqr_cols(ctx, qw, n, n, (int64_t)ind - 1, Q2);
+  if (clk) clk->mark(3);
+  DMat Y = ctx.arena->alloc(m, ell);
+  gemm(ctx, Op::N, Op::N, 1.0, A, Q2, 0.0, Y);  // unscaled A (partial.cpp:147)
+  if (clk) clk->mark(4);
+  DMat Us = ctx.arena->alloc(m, ell), Vs = ctx.arena->alloc(ell, ell);
+  std::vector<double> sig;
+  svd_polar(ctx, Y, Us, sig, Vs);
+  if (clk) clk->mark(5);
+  const double cutoff = s * out.alpha;
+  int64_t k = 0;
+  while (k < (int64_t)sig.size() && sig[k] > cutoff) ++k;
+  const double l = (double)ell;
+  out.flops += 2 * nd * nd * l - 2 * l * l * l / 3 + 2 * md * nd * l + 6 * md * l * l + 20 * l * l * l;
+  if (k == 0) return out;
+  out.sigma.assign(sig.begin(), sig.begin() + k);
+  out.U = Us.sub(0, 0, m, k);
+  out.V = ctx.arena->alloc(n, k);
+  gemm(ctx, Op::N, Op::N, 1.0, Q2, Vs.sub(0, 0, ell, k), 0.0, out.V);
+  out.flops += 2 * nd * l * (double)k;
+  if (clk) clk->mark(6);
+  return out;
+}
+
+}  // namespace qdwhg

@@ -1,0 +1,92 @@
+// Host orchestration of the QDWHpartial algorithms on device views (DMat).
+// Each function restates the control flow of the reference driver it cites;
+// every O(n^2)/O(n^3) step is a device kernel, the host only handles scalars
+// (Halley weights, the diag(R) scan, counts) and launches.
+#pragma once
+#include <array>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace qdwhg {
+
+// polar.cpp:12-27 / 29-38 / 40-51, partial.cpp:26-30 (host scalars)
+struct WeightStep {
+  double a, b, c, ell_in, ell_out;
+};
+WeightStep halley_weights(double ell);
+size_t iterations_to_converge(double ell0, double eps, size_t max_iters = 60);
+double choose_shift(size_t iters);  // returns s
+
+struct StageClock {
+  explicit StageClock(Ctx& c);
+  ~StageClock();
+  void mark(int stage);  // everything since the previous mark is charged to `stage`
+  void finish(double* stage_seconds, double* total);
+  Ctx& ctx;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> owner;
+};
+
+// polar.cpp:82-128.  Xout may alias X.
+void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout);
+// polar.cpp:53-80.  Xout may alias X.
+void qdwh_qr_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout);
+
+struct FixedIterResult {
+  double ell = 0;
+  std::vector<double> trace;
+  size_t iters_qr = 0, iters_chol = 0;
+};
+// polar.cpp:179-215, in place on X.  qr_first: FixedVariant::QrFirst.
+FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_t iters,
+                                     bool qr_first);
+
+struct PolarOut {
+  double alpha = 0;
+  size_t iters_qr = 0, iters_chol = 0;
+  std::vector<double> trace;
+  double flops = 0;
+};
+struct PolarCfg {
+  double ell0 = 1e-15;
+  size_t max_iters = 60;
+  double conv_eps = 2.220446049250313e-16;
+  double chol_switch_c = 100.0;
+  int force_variant = 0;  // 0 Auto, 1 QrOnly, 2 CholeskyOnly
+};
+// polar.cpp:130-177.  Up (m x n) and H (n x n, optional: H.base == nullptr to skip).
+PolarOut polar_decompose(Ctx& ctx, const DMat& A, const PolarCfg& cfg, const DMat& Up,
+                         const DMat& H);
+
+// svd_dense (kernels.cpp:217-330) restated for the device as polar + EIG
+// (fullsolve.cpp:82-103): U (m x n), sigma descending (host), V (n x n).
+void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V);
+
+struct EigOut {
+  std::vector<double> lambda;  // ascending
+  DMat V;                      // n x k, in the arena
+  double mu = 0, shift = 0, tol = 0.01;
+  size_t rank_index = 0, subspace_size = 0, iters_qr = 0, iters_chol = 0, borderline = 0;
+  bool no_savings = false, randomized = false;
+  std::vector<double> trace;
+  double flops = 0;
+};
+// partial.cpp:40-99 (Alg. 1).
+EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomize, double tol,
+                   uint64_t seed, StageClock* clk);
+
+struct SvdOut {
+  std::vector<double> sigma;  // descending
+  DMat U, V;                  // m x k, n x k in the arena
+  double alpha = 0, threshold = 0, tol = 0.01;
+  size_t rank_index = 0, subspace_size = 0, iters_qr = 0, iters_chol = 0;
+  bool no_savings = false, randomized = false;
+  std::vector<double> trace;
+  double flops = 0;
+};
+// partial.cpp:101-158 (Alg. 2).  If s_abs > 0 the threshold is s = s_abs/alpha.
+SvdOut partial_svd(Ctx& ctx, const DMat& A, double s, double s_abs, double tol, bool randomize,
+                   uint64_t seed, StageClock* clk);
+
+}  // namespace qdwhg

@@ -1,0 +1,422 @@
+// FP64 tensor-core GEMM for sm_100a: TMA -> swizzled smem -> DMMA.8x8x4.
+//
+// One kernel serves every GEMM-shaped step of the QDWHpartial path:
+//   SYRK  Z = I + c*X^T X        (polar.cpp:85-93)        -> OutMode::LowerMirror, diag_add
+//   TRMM  Y = X W^-1, G = Y W^-T (polar.cpp:95-121)       -> KRange::BUpper / BLower
+//   fused weight update X+ = (b/c) X + (a-b/c) G (polar.cpp:122-127) -> alpha/beta/Cin epilogue
+//   WY updates of GEQRF/ORGQR, Rayleigh-Ritz products (partial.cpp:80,97,147,156)
+//
+// Structure (one CTA per output tile, WM*WN warps):
+//   lane 0 of warp 0 : TMA producer, STAGES-deep full/empty mbarrier ring
+//   all warps        : DMMA consumers, warp tile (BM/WM) x (BN/WN)
+// Shared-memory tiles are written by TMA with the 128-byte swizzle; the k
+// order inside each 16-wide k slab is permuted (same permutation for A and B,
+// so the product is unchanged) to make fragment loads bank-conflict free.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace qdwhg {
+
+namespace {
+
+constexpr int BK = 16;  // k per stage (one 128-byte swizzle row of doubles)
+
+struct GemmParams {
+  int M, N, K;
+  int a_c0, a_c1;  // TMA coordinate offsets of op(A) storage (contiguous, outer)
+  int b_c0, b_c1;
+  double alpha, beta, diag_add;
+  double* D;
+  int64_t ldd;
+  const double* Cin;
+  int64_t ldcin;
+  int kmode;   // KRange
+  int omode;   // OutMode
+  int tiles_m, tiles_n;
+  int splits;       // split-K factor (1 = fused epilogue)
+  double* partial;  // splits x (M x N) raw partials (ld = M) when splits > 1
+};
+
+template <bool KMAJ>
+QDWHG_DEV int frag_off(int mn, int k) {
+  if (KMAJ) {
+    // box {16 (k), BMN (mn)}: row = mn, 16 k per 128-byte row
+    return mn * 16 + ((((k >> 1) ^ (mn & 7)) << 1) | (k & 1));
+  } else {
+    // boxes {16 (mn), 16 (k)}: box = mn/16, row = k
+    const int c = mn & 15;
+    return (mn >> 4) * 256 + k * 16 + ((((c >> 1) ^ (k & 7)) << 1) | (c & 1));
+  }
+}
+
+template <bool PERM1>
+QDWHG_DEV int kperm(int t, int i) {
+  return PERM1 ? (2 * i + (t & 1) + 8 * (t >> 1)) : ((i & 1) + 2 * t + 8 * (i >> 1));
+}
+
+// Fragment offsets for mn = base_mn + 8*x (base_mn % 16 in [0,8), x compile-time):
+// one or two runtime bases per k-step plus compile-time immediates.
+struct FragBase {
+  int even, odd;
+};
+template <bool KMAJ>
+QDWHG_DEV FragBase frag_base(int base_mn, int k) {
+  FragBase b;
+  b.even = frag_off<KMAJ>(base_mn, k);
+  b.odd = frag_off<KMAJ>(base_mn + 8, k);
+  return b;
+}
+template <bool KMAJ>
+QDWHG_DEV int frag_at(const FragBase& b, int x) {
+  // K-major: +128 doubles per 8 rows; M-major: boxes of 16 rows (256 doubles), parity selects base
+  return KMAJ ? (b.even + 128 * x) : (((x & 1) ? b.odd : b.even) + 256 * (x >> 1));
+}
+
+// blockIdx -> (tm, tn); heaviest tiles first for triangular K ranges.
+QDWHG_DEV void tile_coords(const GemmParams& p, int bid, int& tm, int& tn) {
+  if (p.omode == (int)OutMode::LowerMirror) {
+    // enumerate lower tiles column by column: column tn holds tiles tm = tn..tiles_m-1
+    int c = 0, rem = bid;
+    while (rem >= p.tiles_m - c) {
+      rem -= p.tiles_m - c;
+      ++c;
+    }
+    tn = c;
+    tm = c + rem;
+    return;
+  }
+  tm = bid % p.tiles_m;
+  tn = bid / p.tiles_m;
+  switch ((KRange)p.kmode) {
+    case KRange::BUpper: tn = p.tiles_n - 1 - tn; break;
+    case KRange::ALower: tm = p.tiles_m - 1 - tm; break;
+    default: break;
+  }
+}
+
+template <int BM, int BN>
+QDWHG_DEV void k_range(const GemmParams& p, int m0, int n0, int& kb, int& ke) {
+  kb = 0;
+  ke = p.K;
+  switch ((KRange)p.kmode) {
+    case KRange::BUpper: ke = min(p.K, n0 + BN); break;   // op(B)(k,j) != 0 only for k <= j
+    case KRange::BLower: kb = min(p.K, n0); break;        // k >= j
+    case KRange::AUpper: kb = min(p.K, m0); break;        // op(A)(i,k) != 0 only for k >= i
+    case KRange::ALower: ke = min(p.K, m0 + BM); break;   // k <= i
+    default: break;
+  }
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool A_KMAJ, bool B_KMAJ>
+__global__ void __launch_bounds__(WM * WN * 32, 1)
+    gemm_dmma_kernel(const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  constexpr int NCW = WM * WN;           // consumer warps
+  constexpr int WTM = BM / WM, WTN = BN / WN;
+  constexpr int TM = WTM / 8, TN = WTN / 8;
+  constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
+  constexpr uint32_t STAGE_BYTES = (A_ELEMS + B_ELEMS) * 8;
+  constexpr bool PERM1 = A_KMAJ;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = sA + STAGES * A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_ELEMS);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int tm, tn;
+  tile_coords(p, blockIdx.x, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  int kb, ke;
+  k_range<BM, BN>(p, m0, n0, kb, ke);
+  int kt0 = kb / BK, kt1 = (ke + BK - 1) / BK;
+  if (p.splits > 1) {
+    const int nk = max(kt1 - kt0, 0);
+    const int per = (nk + p.splits - 1) / p.splits;
+    const int s0 = kt0 + blockIdx.z * per;
+    kt1 = min(kt1, s0 + per);
+    kt0 = min(s0, kt1);
+  }
+  const int nkt = max(kt1 - kt0, 0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  // Producer = lane 0 of warp 0 (no dedicated warp: 8 warps keep the 255-register
+  // budget; 9 would cap at 168 because 3 warps would share one SMSP).
+  auto issue = [&](int it) {
+    const int s = it % STAGES;
+    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+    const int k0 = (kt0 + it) * BK;
+    double* a_dst = sA + s * A_ELEMS;
+    double* b_dst = sB + s * B_ELEMS;
+    if (A_KMAJ) {
+      tma_load_2d(a_dst, &tmA, &full[s], p.a_c0 + k0, p.a_c1 + m0);
+    } else {
+#pragma unroll
+      for (int b = 0; b < BM / 16; ++b)
+        tma_load_2d(a_dst + b * 256, &tmA, &full[s], p.a_c0 + m0 + 16 * b, p.a_c1 + k0);
+    }
+    if (B_KMAJ) {
+      tma_load_2d(b_dst, &tmB, &full[s], p.b_c0 + k0, p.b_c1 + n0);
+    } else {
+#pragma unroll
+      for (int b = 0; b < BN / 16; ++b)
+        tma_load_2d(b_dst + b * 256, &tmB, &full[s], p.b_c0 + n0 + 16 * b, p.b_c1 + k0);
+    }
+  };
+  const bool producer = (threadIdx.x == 0);
+  if (producer && nkt > 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int it = 0; it < min(nkt, STAGES - 1); ++it) issue(it);
+  }
+
+  // ---------------- DMMA consumers
+  const int wm = warp % WM, wn = warp / WM;
+  const int g = lane >> 2, t = lane & 3;
+  const int am = wm * WTM + g, bn = wn * WTN + g;
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  FragBase fa_i[4], fb_i[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    fa_i[i] = frag_base<A_KMAJ>(am, kperm<PERM1>(t, i));
+    fb_i[i] = frag_base<B_KMAJ>(bn, kperm<PERM1>(t, i));
+  }
+
+  for (int it = 0; it < nkt; ++it) {
+    const int s = it % STAGES;
+    if (producer && it + STAGES - 1 < nkt) issue(it + STAGES - 1);
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const double* a_s = sA + s * A_ELEMS;
+    const double* b_s = sB + s * B_ELEMS;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const FragBase fa = fa_i[i], fb = fb_i[i];
+      // B fragments held, A fragments streamed (register pressure)
+      double bf[TN];
+#pragma unroll
+      for (int y = 0; y < TN; ++y) bf[y] = b_s[frag_at<B_KMAJ>(fb, y)];
+#pragma unroll
+      for (int x = 0; x < TM; ++x) {
+        const double af = a_s[frag_at<A_KMAJ>(fa, x)];
+#pragma unroll
+        for (int y = 0; y < TN; ++y) dmma_8x8x4(acc[x][y][0], acc[x][y][1], af, bf[y]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---------------- epilogue
+  if (p.splits > 1) {
+    double* P = p.partial + (size_t)blockIdx.z * p.M * p.N;
+#pragma unroll
+    for (int x = 0; x < TM; ++x)
+#pragma unroll
+      for (int y = 0; y < TN; ++y)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = m0 + wm * WTM + 8 * x + g;
+          const int j = n0 + wn * WTN + 8 * y + 2 * t + e;
+          if (i < p.M && j < p.N) P[i + (size_t)j * p.M] = acc[x][y][e];
+        }
+    return;
+  }
+  const bool lower = p.omode == (int)OutMode::LowerMirror;
+#pragma unroll
+  for (int x = 0; x < TM; ++x)
+#pragma unroll
+    for (int y = 0; y < TN; ++y)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = m0 + wm * WTM + 8 * x + g;
+        const int j = n0 + wn * WTN + 8 * y + 2 * t + e;
+        if (i >= p.M || j >= p.N) continue;
+        if (lower && i < j) continue;
+        double v = p.alpha * acc[x][y][e];
+        if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
+        if (i == j) v += p.diag_add;
+        p.D[i + (size_t)j * p.ldd] = v;
+        if (lower && i != j) p.D[j + (size_t)i * p.ldd] = v;
+      }
+}
+
+// Split-K reduction + epilogue: D = alpha * sum_z P_z + beta * Cin (+diag), with
+// the same LowerMirror semantics.
+__global__ void splitk_reduce_kernel(const GemmParams p) {
+  const int64_t total = (int64_t)p.M * p.N;
+  const bool lower = p.omode == (int)OutMode::LowerMirror;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % p.M), j = (int)(idx / p.M);
+    if (lower && i < j) continue;
+    double s = 0.0;
+    for (int z = 0; z < p.splits; ++z) s += p.partial[(size_t)z * total + idx];
+    double v = p.alpha * s;
+    if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
+    if (i == j) v += p.diag_add;
+    p.D[i + (size_t)j * p.ldd] = v;
+    if (lower && i != j) p.D[j + (size_t)i * p.ldd] = v;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    QDWHG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// Descriptor over the stored matrix of view `v`, extent clipped at the end of
+// the view so reads past the view are zero-filled by TMA.
+CUtensorMap make_desc(const DMat& v, int box0, int box1) {
+  CUtensorMap tm;
+  const uint64_t d0 = (uint64_t)std::max<int64_t>(v.r0 + v.rows, 1);
+  const uint64_t d1 = (uint64_t)std::max<int64_t>(v.c0 + v.cols, 1);
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {(cuuint64_t)v.ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)v.base, dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return tm;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, bool AK, bool BK_>
+void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
+  constexpr int threads = WM * WN * 32;
+  constexpr size_t smem = 1024 + (size_t)STAGES * (BM + BN) * BK * 8 + 2 * STAGES * 8;
+  auto kern = gemm_dmma_kernel<BM, BN, WM, WN, STAGES, AK, BK_>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const CUtensorMap ta = AK ? make_desc(A, 16, BM) : make_desc(A, 16, 16);
+  const CUtensorMap tb = BK_ ? make_desc(B, 16, BN) : make_desc(B, 16, 16);
+  int ntiles;
+  if (p.omode == (int)OutMode::LowerMirror)
+    ntiles = p.tiles_n * (p.tiles_n + 1) / 2;
+  else
+    ntiles = p.tiles_m * p.tiles_n;
+  dim3 grid(ntiles, 1, p.splits);
+  kern<<<grid, threads, smem, ctx.stream>>>(ta, tb, p);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.gemm_launches++;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+void dispatch_layout(Ctx& ctx, bool ak, bool bk, const DMat& A, const DMat& B, GemmParams& p) {
+  if (ak && bk) launch_cfg<BM, BN, WM, WN, STAGES, true, true>(ctx, A, B, p);
+  else if (ak && !bk) launch_cfg<BM, BN, WM, WN, STAGES, true, false>(ctx, A, B, p);
+  else if (!ak && bk) launch_cfg<BM, BN, WM, WN, STAGES, false, true>(ctx, A, B, p);
+  else launch_cfg<BM, BN, WM, WN, STAGES, false, false>(ctx, A, B, p);
+}
+
+}  // namespace
+
+void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, double beta,
+          const DMat& C, const GemmExtra& ex) {
+  const int64_t M = C.rows, N = C.cols;
+  const int64_t K = (ta == Op::N) ? A.cols : A.rows;
+  const int64_t am = (ta == Op::N) ? A.rows : A.cols;
+  const int64_t bk = (tb == Op::N) ? B.rows : B.cols;
+  const int64_t bn = (tb == Op::N) ? B.cols : B.rows;
+  if (am != M || bn != N || bk != K) throw InvalidArgument("gemm: shape mismatch");
+  if (M == 0 || N == 0) return;
+  if (ex.out == OutMode::LowerMirror && M != N) throw InvalidArgument("gemm: LowerMirror needs square C");
+  if ((A.ld % 2) || (B.ld % 2) || (reinterpret_cast<uintptr_t>(A.base) % 16) ||
+      (reinterpret_cast<uintptr_t>(B.base) % 16))
+    throw InvalidArgument("gemm: operands must be 16-byte aligned with even leading dimension");
+
+  GemmParams p{};
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  // TMA coordinates: (contiguous index, outer index) of the stored matrix
+  p.a_c0 = (int)A.r0;
+  p.a_c1 = (int)A.c0;
+  p.b_c0 = (int)B.r0;
+  p.b_c1 = (int)B.c0;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.diag_add = ex.diag_add;
+  p.D = C.ptr();
+  p.ldd = C.ld;
+  const DMat& cin = ex.cin ? *ex.cin : C;
+  p.Cin = cin.ptr();
+  p.ldcin = cin.ld;
+  p.kmode = (int)ex.krange;
+  p.omode = (int)ex.out;
+  const bool ak = (ta == Op::T);  // op(A) K-contiguous
+  const bool bkm = (tb == Op::N); // op(B) K-contiguous
+
+  // Tile choice: 128x128 when the grid fills the machine, else 64x64.
+  const bool big = ((M + 127) / 128) * ((N + 127) / 128) >= ctx.num_sms;
+  const int BMt = big ? 128 : 64;
+  p.tiles_m = (int)((M + BMt - 1) / BMt);
+  p.tiles_n = (int)((N + BMt - 1) / BMt);
+  int ntiles = (ex.out == OutMode::LowerMirror) ? p.tiles_n * (p.tiles_n + 1) / 2
+                                                 : p.tiles_m * p.tiles_n;
+  // split-K when the output grid leaves SMs idle and K is long
+  int splits = ex.split_k;
+  if (splits <= 0) {
+    splits = 1;
+    const int64_t ktiles = (K + BK - 1) / BK;
+    while (ntiles * splits * 2 <= 2 * ctx.num_sms && ktiles / (splits * 2) >= 16 && splits < 32)
+      splits *= 2;
+  }
+  p.splits = splits;
+  const Arena::Mark mark = ctx.arena->mark();
+  if (splits > 1) p.partial = static_cast<double*>(ctx.arena->alloc_bytes((size_t)splits * M * N * 8));
+
+  if (big)
+    dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, A, B, p);
+  else
+    dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, A, B, p);
+
+  if (splits > 1) {
+    const int64_t total = M * N;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * ctx.num_sms);
+    splitk_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(p);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+  }
+  ctx.arena->release_to(mark);
+}
+
+}  // namespace qdwhg

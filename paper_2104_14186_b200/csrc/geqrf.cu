@@ -1,0 +1,326 @@
+// Blocked Householder QR + trailing-column Q formation for the subspace
+// extraction of Alg. 1/2 (partial.cpp:71-79, 138-146) and the stacked QR of
+// the QR-based QDWH step (polar.cpp:56-72).  Reference kernels:
+// householder_qr kernels.cpp:41-80 and accumulate_q kernels.cpp:84-101.
+//
+// Same reflector convention as the reference (R_jj = -sign(x0)*||x||,
+// p = min(m-1, n) reflectors, tau = 0 for a zero column), stored LAPACK style
+// (v_jj = 1, tau' = tau * v0^2) so each nb-column panel becomes a compact-WY
+// block (I - V T V^T) and every update is a DMMA GEMM:
+//   panel:    geqr2_panel_kernel — cooperative persistent kernel, the panel
+//             lives in shared memory across up to 148 CTAs; ONE grid barrier
+//             per column (norm, pivot and all v^T a_c dot products reduced
+//             together with FP64 atomics);
+//   T:        Gram V^T V by GEMM, then larft_kernel (one CTA);
+//   trailing: C -= V T^T (V^T C)  — three GEMMs;
+//   ORGQR:    only the requested Q columns (Q2 = Q(:, ind-1:n)), reflector
+//             blocks applied last to first, skipping columns still equal to e_i.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace qdwhg {
+
+namespace {
+
+constexpr int kPanelThreads = 256;
+constexpr int kBW = 64;  // max panel width (one thread column per panel column)
+
+QDWHG_DEV unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+QDWHG_DEV void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Monotonic grid barrier (counter zeroed before launch; all CTAs co-resident
+// via cooperative launch).
+QDWHG_DEV void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    red_release_add(bar, 1u);
+    const unsigned target = epoch * nblocks;
+    while (ld_acquire(bar) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Partial sums for pivot column `col` over this CTA's rows:
+//   top[c]  = A(col, c)                       (row owner only)
+//   dbel[c] = sum_{r > col} A(r, col) A(r, c) (dbel[col] = sigma^2 below the pivot)
+// for c >= col, accumulated into buf = [top(BW) | dbel(BW)].
+QDWHG_DEV void panel_partials(const double* S, int RP, int nr, int rbeg, int b, int col, double* red,
+                              double* buf) {
+  const int c = threadIdx.x % kBW, rg = threadIdx.x / kBW;
+  double d = 0.0;
+  if (c < b && c >= col) {
+    const double* sc = S + c * RP;
+    const double* sp = S + col * RP;
+    int r0 = max(col + 1 - rbeg, 0);
+    for (int r = r0 + rg; r < nr; r += kPanelThreads / kBW) d += sp[r] * sc[r];
+  }
+  red[rg * kBW + c] = d;
+  __syncthreads();
+  if (rg == 0 && c < b && c >= col) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kPanelThreads / kBW; ++q) s += red[q * kBW + c];
+    if (s != 0.0) atomicAdd(&buf[kBW + c], s);
+    const int rl = col - rbeg;
+    if (rl >= 0 && rl < nr) atomicAdd(&buf[c], S[c * RP + rl]);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPanelThreads, 1)
+    geqr2_panel_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
+                       int b, int rpc, double* acc, unsigned* bar) {
+  extern __shared__ double smem[];
+  const int RP = rpc | 1;
+  double* S = smem;               // [b][RP] column-major panel rows of this CTA
+  double* red = S + kBW * RP;     // [4][kBW]
+  double* coef = red + (kPanelThreads / kBW) * kBW;  // [kBW] w_c
+  const int rbeg = blockIdx.x * rpc;
+  const int nr = max(0, min(rpc, mp - rbeg));
+  const int c = threadIdx.x % kBW, rg = threadIdx.x / kBW;
+  constexpr int NRG = kPanelThreads / kBW;
+  unsigned epoch = 0;
+
+  for (int cc = 0; cc < b; ++cc)
+    for (int r = threadIdx.x; r < nr; r += kPanelThreads) S[cc * RP + r] = A[(rbeg + r) + cc * lda];
+  __syncthreads();
+
+  panel_partials(S, RP, nr, rbeg, b, 0, red, acc);
+  grid_barrier(bar, gridDim.x, epoch);
+
+  for (int jj = 0; jj < b; ++jj) {
+    const double* buf = acc + (jj % 3) * (2 * kBW);
+    if (blockIdx.x == 0) {
+      double* z = acc + ((jj + 2) % 3) * (2 * kBW);
+      for (int i = threadIdx.x; i < 2 * kBW; i += kPanelThreads) z[i] = 0.0;
+    }
+    const double x0 = __ldcg(&buf[jj]);
+    const double sig2 = __ldcg(&buf[kBW + jj]);
+    const double normx = sqrt(x0 * x0 + sig2);
+    const bool reflect = (jj < mp - 1) && normx > 0.0;
+    double beta = x0, v0 = 1.0, taup = 0.0;
+    if (reflect) {
+      const double sign = x0 >= 0.0 ? 1.0 : -1.0;
+      beta = -sign * normx;
+      v0 = x0 - beta;
+      taup = (beta - x0) / beta;
+    }
+    if (threadIdx.x < kBW) {
+      const int cc = threadIdx.x;
+      double w = 0.0;
+      if (reflect && cc > jj && cc < b) w = taup * (__ldcg(&buf[cc]) + __ldcg(&buf[kBW + cc]) / v0);
+      coef[cc] = w;
+    }
+    __syncthreads();
+    // apply H_jj to this CTA's rows; column jj -> v' (to V), R_jj
+    if (c < b) {
+      const double* sj = S + jj * RP;
+      double* sc = S + c * RP;
+      const double inv_v0 = 1.0 / v0;
+      if (c > jj) {
+        const double w = coef[c];
+        if (w != 0.0) {
+          for (int r = rg; r < nr; r += NRG) {
+            const int rgl = rbeg + r;
+            if (rgl == jj) sc[r] -= w;
+            else if (rgl > jj) sc[r] -= w * (sj[r] * inv_v0);
+          }
+        }
+      } else if (c == jj) {
+        for (int r = rg; r < nr; r += NRG) {
+          const int rgl = rbeg + r;
+          double v;
+          if (rgl < jj) v = 0.0;
+          else if (rgl == jj) v = 1.0;
+          else v = reflect ? sj[r] * inv_v0 : 0.0;
+          V[rgl + (int64_t)jj * ldv] = v;
+        }
+      }
+    }
+    __syncthreads();
+    if (c == jj && rg == 0) {
+      const int rl = jj - rbeg;
+      if (rl >= 0 && rl < nr) S[jj * RP + rl] = beta;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) tau_out[jj] = taup;
+    if (jj + 1 < b) {
+      panel_partials(S, RP, nr, rbeg, b, jj + 1, red, acc + ((jj + 1) % 3) * (2 * kBW));
+      grid_barrier(bar, gridDim.x, epoch);
+    }
+  }
+  __syncthreads();
+  // write back R (upper part) with explicit zeros below the diagonal; V above diag = 0
+  for (int cc = 0; cc < b; ++cc)
+    for (int r = threadIdx.x; r < nr; r += kPanelThreads) {
+      const int rgl = rbeg + r;
+      A[rgl + cc * lda] = (rgl <= cc) ? S[cc * RP + r] : 0.0;
+    }
+}
+
+// T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise):
+// T(i,i) = tau_i, T(0:i, i) = -tau_i * T(0:i, 0:i) * G(0:i, i).
+__global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, double* T,
+                             int64_t ldt, int b) {
+  __shared__ double Ts[kBW][kBW + 1];
+  __shared__ double g[kBW];
+  const int t = threadIdx.x;
+  for (int i = t; i < kBW * kBW; i += blockDim.x) Ts[i % kBW][i / kBW] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < b; ++i) {
+    const double ti = tau[i];
+    if (t < i) g[t] = G[t + (int64_t)i * ldg];
+    __syncthreads();
+    if (t < i) {
+      double s = 0.0;
+      for (int k = t; k < i; ++k) s += Ts[t][k] * g[k];
+      Ts[t][i] = -ti * s;
+    }
+    if (t == i) Ts[i][i] = ti;
+    __syncthreads();
+  }
+  for (int i = t; i < b * b; i += blockDim.x) {
+    const int r = i % b, cc = i / b;
+    T[r + (int64_t)cc * ldt] = Ts[r][cc];
+  }
+}
+
+__global__ void diag_kernel(const double* R, int64_t ld, int64_t n, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = R[i + i * ld];
+}
+
+void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
+                  unsigned* bar) {
+  const int mp = (int)P.rows, b = (int)P.cols;
+  int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
+  int rpc = (mp + nblk - 1) / nblk;
+  const size_t smem = ((size_t)kBW * (rpc | 1) + (kPanelThreads / kBW) * kBW + kBW) * 8;
+  if (smem > 227 * 1024) throw InvalidArgument("geqrf: panel too tall for shared memory");
+  static bool set = false;
+  if (!set) {
+    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    set = true;
+  }
+  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+  double* Ap = P.ptr();
+  int64_t lda = P.ld;
+  double* Vptr = Vp.ptr();
+  int64_t ldv = Vp.ld;
+  void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, (void*)&mp, (void*)&b, &rpc, &acc, &bar};
+  QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)geqr2_panel_kernel, dim3(nblk),
+                                         dim3(kPanelThreads), args, smem, ctx.stream));
+  ctx.count();
+}
+
+}  // namespace
+
+void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
+  const int64_t m = A.rows, n = A.cols;
+  if (m < n) throw InvalidArgument("geqrf: requires rows >= cols");
+  const int nb = w.nb = kBW;
+  const int64_t npan = (n + nb - 1) / nb;
+  w.V = ctx.arena->alloc(m, n);
+  w.T = ctx.arena->alloc(nb, npan * nb);
+  double* tau_dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 64)));
+  double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW));
+  unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
+  DMat G = ctx.arena->alloc(nb, nb);
+  const Arena::Mark mark = ctx.arena->mark();
+  for (int64_t p = 0; p < npan; ++p) {
+    const int64_t j0 = p * nb;
+    const int64_t b = std::min<int64_t>(nb, n - j0);
+    const int64_t mp = m - j0;
+    const DMat Pn = A.sub(j0, j0, mp, b);
+    const DMat Vp = w.V.sub(j0, j0, mp, b);
+    panel_factor(ctx, Pn, Vp, tau_dev + j0, acc, bar);
+    // V above the panel block is zero (rows < j0 of these columns)
+    if (j0 > 0) fill(ctx, w.V.sub(0, j0, j0, b), 0.0, 0.0);
+    // T_p from Gram V^T V
+    const DMat Gp = G.sub(0, 0, b, b);
+    gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
+    const DMat Tp = w.T.sub(0, p * nb, b, b);
+    larft_kernel<<<1, 64, 0, ctx.stream>>>(Gp.ptr(), Gp.ld, tau_dev + j0, Tp.ptr(), Tp.ld, (int)b);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+    // trailing update C = (I - V T V^T)^T C = C - V T^T (V^T C)
+    const int64_t nc = n - j0 - b;
+    if (nc > 0) {
+      const DMat C = A.sub(j0, j0 + b, mp, nc);
+      DMat W1 = ctx.arena->alloc(b, nc);
+      DMat W2 = ctx.arena->alloc(b, nc);
+      gemm(ctx, Op::T, Op::N, 1.0, Vp, C, 0.0, W1);
+      GemmExtra e;
+      e.krange = KRange::ALower;  // op(A) = T^T lower
+      gemm(ctx, Op::T, Op::N, 1.0, Tp, W1, 0.0, W2, e);
+      gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, C);
+      ctx.arena->release_to(mark);
+    }
+  }
+  w.taus.assign(n, 0.0);
+  QDWHG_CUDA(cudaMemcpyAsync(w.taus.data(), tau_dev, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                             ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, const DMat& Q) {
+  const int64_t ncols = Q.cols;
+  const int nb = w.nb;
+  // Q = E(:, c0 : c0+ncols)
+  fill(ctx, Q, 0.0, 0.0);
+  {
+    // identity entries (c0 + i, i)
+    DMat D = Q.sub(c0, 0, std::min<int64_t>(ncols, m - c0), std::min<int64_t>(ncols, m - c0));
+    fill(ctx, D, 0.0, 1.0);
+  }
+  const int64_t npan = (n + nb - 1) / nb;
+  const Arena::Mark mark = ctx.arena->mark();
+  for (int64_t p = npan - 1; p >= 0; --p) {
+    const int64_t j0 = p * nb;
+    const int64_t b = std::min<int64_t>(nb, n - j0);
+    const int64_t mp = m - j0;
+    const int64_t i0 = std::max<int64_t>(0, j0 - c0);  // first affected Q column
+    if (i0 >= ncols) continue;
+    const int64_t nc = ncols - i0;
+    const DMat Vp = w.V.sub(j0, j0, mp, b);
+    const DMat Tp = w.T.sub(0, p * nb, b, b);
+    const DMat C = Q.sub(j0, i0, mp, nc);
+    DMat W1 = ctx.arena->alloc(b, nc);
+    DMat W2 = ctx.arena->alloc(b, nc);
+    gemm(ctx, Op::T, Op::N, 1.0, Vp, C, 0.0, W1);
+    GemmExtra e;
+    e.krange = KRange::AUpper;  // T upper
+    gemm(ctx, Op::N, Op::N, 1.0, Tp, W1, 0.0, W2, e);
+    gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, C);
+    ctx.arena->release_to(mark);
+  }
+}
+
+void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d) {
+  const int64_t n = std::min(R.rows, R.cols);
+  d.resize(n);
+  double* tmp = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 1)));
+  diag_kernel<<<std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148)), 256, 0, ctx.stream>>>(
+      R.ptr(), R.ld, n, tmp);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+  QDWHG_CUDA(cudaMemcpyAsync(d.data(), tmp, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+}  // namespace qdwhg

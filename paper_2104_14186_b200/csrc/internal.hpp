@@ -1,0 +1,173 @@
+// Internal host-side interfaces of libqdwhg (not exported).
+//
+// Every matrix the device code touches is a column-major FP64 view into a
+// 256-byte aligned allocation whose leading dimension is a multiple of 32
+// doubles (TMA needs 16-byte strides; 256 B keeps every column start
+// sector-aligned).  Views carry the parent base pointer plus a (r0, c0)
+// offset so the TMA descriptor can be encoded on the aligned base and the
+// offset applied in tensor coordinates.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace qdwhg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NotPositiveDefinite : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NotConverged : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CapacityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define QDWHG_CUDA(expr)                                                                   \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      throw ::qdwhg::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @ " + \
+                               __FILE__ + ":" + std::to_string(__LINE__));                 \
+  } while (0)
+
+// Column-major view: element (i, j) of the view is base[(r0 + i) + (c0 + j) * ld].
+struct DMat {
+  double* base = nullptr;
+  int64_t ld = 0;
+  int64_t r0 = 0, c0 = 0;
+  int64_t rows = 0, cols = 0;
+
+  double* ptr() const { return base + r0 + c0 * ld; }
+  DMat sub(int64_t i, int64_t j, int64_t m, int64_t n) const {
+    DMat s = *this;
+    s.r0 += i;
+    s.c0 += j;
+    s.rows = m;
+    s.cols = n;
+    return s;
+  }
+  DMat col_block(int64_t j, int64_t n) const { return sub(0, j, rows, n); }
+};
+
+inline int64_t round_ld(int64_t rows) { return ((rows + 31) / 32) * 32; }
+
+// Device arena owned by a handle: bump allocation over a list of cudaMalloc'd
+// chunks that persist across calls (no cudaMalloc in steady state).  Marks
+// rewind; stream order makes reuse after rewind safe (one stream per handle).
+class Arena {
+ public:
+  struct Mark {
+    size_t chunk = 0, off = 0;
+  };
+  ~Arena();
+  void* alloc_bytes(size_t bytes);
+  DMat alloc(int64_t rows, int64_t cols);
+  void reset() { cur_ = Mark{}; }
+  Mark mark() const { return cur_; }
+  void release_to(Mark m) { cur_ = m; }
+  size_t reserved() const;
+  size_t high_water() const { return high_; }
+  void reserve(size_t bytes);
+
+ private:
+  struct Chunk {
+    char* base;
+    size_t cap;
+  };
+  std::vector<Chunk> chunks_;
+  Mark cur_;
+  size_t high_ = 0;
+};
+
+enum class Op { N, T };
+// Which part of the K range can contribute for an output tile (triangular
+// operands store explicit zeros; skipping them is the TRMM saving).
+enum class KRange { Full, BUpper, BLower, AUpper, ALower };
+enum class OutMode { Full, LowerMirror };
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  Arena* arena = nullptr;
+  int num_sms = 148;
+  double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
+  double* hscratch = nullptr;   // pinned host mirror of dscratch
+  int* dflag = nullptr;         // device status flag
+  uint64_t gemm_launches = 0;   // our kernels launched (for bench accounting)
+  uint64_t other_launches = 0;
+  void count(int n = 1) { other_launches += n; }
+};
+
+// ------------------------------------------------------------------ gemm.cu
+// C = alpha * op(A) * op(B) + beta * Cin (+ diag_add on the diagonal of C).
+// Cin defaults to C itself.  M x N x K are the op() shapes.
+struct GemmExtra {
+  KRange krange = KRange::Full;
+  OutMode out = OutMode::Full;
+  const DMat* cin = nullptr;
+  double diag_add = 0.0;
+  int split_k = 0;  // 0 = automatic
+};
+void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, double beta,
+          const DMat& C, const GemmExtra& ex = {});
+
+// ------------------------------------------------------------------ blas1.cu
+void fill(Ctx& ctx, const DMat& X, double v, double diag);
+// Y = a*X + b*I (Y may alias X)
+void axpby_identity(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y);
+// Y = a * (X + X^T)/2 + diag*I  (square; Y must not alias X unless in place-safe mode)
+void symmetrize_scale(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y);
+void copy(Ctx& ctx, const DMat& X, const DMat& Y);
+void copy_from_host(Ctx& ctx, const double* h, int64_t ldh, const DMat& Y);
+void copy_to_host(Ctx& ctx, const DMat& X, double* h, int64_t ldh);
+// Reductions (results land in ctx.hscratch after sync): frobenius^2, max |x_ij - x_ji|,
+// nonfinite count.
+struct MatStats {
+  double fro2 = 0, asym = 0, nonfinite = 0, maxabs = 0;
+};
+MatStats mat_stats(Ctx& ctx, const DMat& X, bool want_asym);
+void gaussian_fill(Ctx& ctx, const DMat& X, uint64_t seed);
+void mirror_lower_to_upper(Ctx& ctx, const DMat& X);
+void zero_strict_lower(Ctx& ctx, const DMat& X);
+
+// ------------------------------------------------------------------ potrf.cu
+// In place: upper triangle of Z becomes W with Z = W^T W (strict lower zeroed).
+// Throws NotPositiveDefinite.  Winv (n x n) receives W^{-1} (upper, zeros below).
+void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv);
+
+// ------------------------------------------------------------------ geqrf.cu
+struct QrWork {
+  DMat V;               // m x n: unit-lower Householder vectors (explicit 1 / 0)
+  DMat T;               // nb x n: compact-WY T factors per panel, packed
+  std::vector<double> taus;
+  int nb = 64;
+};
+// In place Householder QR of A (m x n, m >= n): R in the upper triangle of A,
+// reflectors in work.V / work.T.  Reference convention (kernels.cpp:41-80):
+// p = min(m-1, n) reflectors, R_jj = -sign(x0) ||x||.
+void geqrf(Ctx& ctx, const DMat& A, QrWork& work);
+// Q(:, c0 : c0+ncols) of the m x m Q = H_0 H_1 ... H_{p-1} into Qout (m x ncols).
+void orgqr_cols(Ctx& ctx, const QrWork& work, int64_t m, int64_t p, int64_t c0, const DMat& Qout);
+// diag(R) to host (n values).
+void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d);
+
+// ------------------------------------------------------------------ syevj.cu
+// Symmetric eigendecomposition of S (n x n, device).  Ascending values to host
+// `vals`, vectors into Vout (n x n).  Jacobi for small n, QDWH spectral
+// divide-and-conquer above the Jacobi cutoff.
+void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+
+// ------------------------------------------------------------------ krylov.cu
+double two_norm_estimate(Ctx& ctx, const DMat& A);
+double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps);
+
+}  // namespace qdwhg

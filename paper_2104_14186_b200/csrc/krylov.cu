@@ -1,0 +1,281 @@
+// HBM-bound Krylov scalars of the partial drivers:
+//   two_norm_estimate  — power iteration on A^T A (kernels.cpp:332-360), alpha for Alg. 2
+//   lanczos_min_bound  — 30-step Lanczos with two-pass full reorthogonalisation
+//                        (kernels.cpp:362-439), mu for Alg. 1
+// Start vectors are generated on the host with the reference's own counter
+// generator (bit-identical, see host_gaussian in qdwhg.cpp), so mu and alpha
+// differ from the reference only by summation order.  GEMVs stream A once per
+// product at full HBM bandwidth (column-dot form for A^T x, row-split form with
+// a deterministic two-stage reduction for A x).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace qdwhg {
+
+std::vector<double> host_gaussian(int64_t count, uint64_t seed);  // qdwhg.cpp
+void syev_jacobi(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+
+namespace {
+
+// z_j = sum_i A(i,j) x_i  (one warp per column; coalesced down the column)
+__global__ void gemv_t_kernel(const double* A, int64_t lda, int64_t m, int64_t n, const double* x,
+                              double* z) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += warps) {
+    const double* a = A + j * lda;
+    double s0 = 0.0, s1 = 0.0;
+    int64_t i = lane;
+    for (; i + 32 < m; i += 64) {
+      s0 += a[i] * x[i];
+      s1 += a[i + 32] * x[i + 32];
+    }
+    if (i < m) s0 += a[i] * x[i];
+    const double s = warp_sum(s0 + s1);
+    if (lane == 0) z[j] = s;
+  }
+}
+
+// partial[s][i] = sum_{j in split s} A(i,j) x_j
+__global__ void gemv_n_partial_kernel(const double* A, int64_t lda, int64_t m, int64_t n,
+                                      const double* x, int64_t cols_per_split, double* partial) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t j0 = blockIdx.y * cols_per_split;
+  const int64_t j1 = std::min<int64_t>(n, j0 + cols_per_split);
+  if (i >= m) return;
+  double s0 = 0.0, s1 = 0.0;
+  int64_t j = j0;
+  for (; j + 1 < j1; j += 2) {
+    s0 += A[i + j * lda] * x[j];
+    s1 += A[i + (j + 1) * lda] * x[j + 1];
+  }
+  if (j < j1) s0 += A[i + j * lda] * x[j];
+  partial[blockIdx.y * m + i] = s0 + s1;
+}
+
+__global__ void reduce_partial_kernel(const double* partial, int splits, int64_t m, double* y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += partial[k * m + i];
+    y[i] = s;
+  }
+}
+
+// out[slot] = x . y  (two-stage: per-block partials, then final by block 0 of a 2nd launch)
+__global__ void dot_partial_kernel(const double* x, const double* y, int64_t n, double* partial) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s += x[i] * y[i];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+__global__ void dot_final_kernel(const double* partial, int nblk, double* out) {
+  __shared__ double scratch[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) s += partial[i];
+  s = block_sum(s, scratch);
+  if (threadIdx.x == 0) *out = s;
+}
+
+// x = y / sqrt(*nrm2)
+__global__ void scale_by_invnorm_kernel(const double* y, const double* nrm2, int64_t n, double* x) {
+  const double inv = 1.0 / sqrt(*nrm2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = y[i] * inv;
+}
+
+// w_i -= sum_k Q(i,k) h_k   (k < kcount <= 64)
+__global__ void sub_qh_kernel(const double* Q, int64_t ldq, int64_t n, int kcount, const double* h,
+                              double* w) {
+  __shared__ double hs[64];
+  if (threadIdx.x < kcount) hs[threadIdx.x] = h[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < kcount; ++k) s += Q[i + k * ldq] * hs[k];
+    w[i] -= s;
+  }
+}
+
+struct Vec {
+  double* p;
+};
+
+class Krylov {
+ public:
+  explicit Krylov(Ctx& c) : ctx(c) {
+    nblk = 2 * ctx.num_sms;
+    partial = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nblk));
+  }
+  void gemv_t(const DMat& A, const double* x, double* z) {
+    const int blocks = (int)std::min<int64_t>((A.cols + 7) / 8, 16LL * ctx.num_sms);
+    gemv_t_kernel<<<blocks, 256, 0, ctx.stream>>>(A.ptr(), A.ld, A.rows, A.cols, x, z);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+  }
+  void gemv_n(const DMat& A, const double* x, double* y, double* part, int splits) {
+    const int64_t cps = (A.cols + splits - 1) / splits;
+    dim3 grid((unsigned)((A.rows + 255) / 256), (unsigned)splits);
+    gemv_n_partial_kernel<<<grid, 256, 0, ctx.stream>>>(A.ptr(), A.ld, A.rows, A.cols, x, cps, part);
+    reduce_partial_kernel<<<(int)std::min<int64_t>((A.rows + 255) / 256, 4LL * ctx.num_sms), 256, 0,
+                            ctx.stream>>>(part, splits, A.rows, y);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count(2);
+  }
+  void dot(const double* x, const double* y, int64_t n, double* out) {
+    const int b = (int)std::min<int64_t>(nblk, std::max<int64_t>(1, (n + 255) / 256));
+    dot_partial_kernel<<<b, 256, 0, ctx.stream>>>(x, y, n, partial);
+    dot_final_kernel<<<1, 256, 0, ctx.stream>>>(partial, b, out);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count(2);
+  }
+  Ctx& ctx;
+  int nblk;
+  double* partial;
+};
+
+}  // namespace
+
+double two_norm_estimate(Ctx& ctx, const DMat& A) {
+  const int64_t m = A.rows, n = A.cols;
+  const MatStats st = mat_stats(ctx, A, false);
+  if (st.fro2 == 0.0) throw InvalidArgument("two_norm_estimate: zero matrix");
+  const Arena::Mark mark = ctx.arena->mark();
+  Krylov K(ctx);
+  std::vector<double> v0 = host_gaussian(n, 0x6e6f726d32ull);  // kernels.cpp:336
+  {
+    double s = 0.0;
+    for (double x : v0) s += x * x;
+    const double nv = std::sqrt(s);
+    for (double& x : v0) x /= nv;
+  }
+  double* v = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
+  double* y = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * m));
+  double* z = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, (2LL * ctx.num_sms * 256) / std::max<int64_t>(m, 1)));
+  double* part = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * splits * m));
+  double* sc = ctx.dscratch;  // [0] = ||y||^2, [1] = ||z||^2
+  QDWHG_CUDA(cudaMemcpyAsync(v, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+  double est = 0.0;
+  for (int it = 0; it < 100; ++it) {
+    K.gemv_n(A, v, y, part, splits);
+    K.dot(y, y, m, sc + 0);
+    K.gemv_t(A, y, z);
+    K.dot(z, z, n, sc + 1);
+    QDWHG_CUDA(cudaMemcpyAsync(ctx.hscratch, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+    const double ny = std::sqrt(ctx.hscratch[0]);
+    if (ny == 0.0) {
+      // start vector in the null space: restart from an axis (kernels.cpp:345-350)
+      std::vector<double> e(n, 0.0);
+      e[it % n] = 1.0;
+      QDWHG_CUDA(cudaMemcpyAsync(v, e.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+      QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+      continue;
+    }
+    const double nz = std::sqrt(ctx.hscratch[1]);
+    const double prev = est;
+    est = ny;
+    if (nz == 0.0) break;
+    scale_by_invnorm_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4LL * ctx.num_sms), 256, 0,
+                              ctx.stream>>>(z, sc + 1, n, v);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+    if (it > 0 && std::abs(est - prev) < 1e-3 * est) break;
+  }
+  ctx.arena->release_to(mark);
+  return 1.05 * est;
+}
+
+double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps) {
+  const int64_t n = A.rows;
+  if (A.cols != n) throw InvalidArgument("lanczos_min_bound: matrix not square");
+  if (steps < 1) throw InvalidArgument("lanczos_min_bound: steps must be >= 1");
+  const MatStats st = mat_stats(ctx, A, true);
+  const double fro = std::sqrt(st.fro2);
+  const double eps = 2.220446049250313e-16;
+  if (st.asym > 1e3 * (double)n * eps * std::max(1.0, fro))
+    throw InvalidArgument("lanczos_min_bound: input not symmetric within tolerance");
+  const int m = (int)std::min<int64_t>(steps, n);
+  if (m > 63) throw InvalidArgument("lanczos_min_bound: at most 63 steps supported");
+  const Arena::Mark mark = ctx.arena->mark();
+  Krylov K(ctx);
+  DMat Q = ctx.arena->alloc(n, m + 1);
+  double* w = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
+  double* h = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 64));
+  double* ab = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * 64));  // alpha | beta^2
+  std::vector<double> q0 = host_gaussian(n, 0x6c616e637aull);  // kernels.cpp:379
+  {
+    double s = 0.0;
+    for (double x : q0) s += x * x;
+    const double nv = std::sqrt(s);
+    for (double& x : q0) x /= nv;
+  }
+  QDWHG_CUDA(cudaMemcpyAsync(Q.ptr(), q0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
+  const int gblocks = (int)std::min<int64_t>((n + 255) / 256, 4LL * ctx.num_sms);
+  // All steps are enqueued without host round trips; a breakdown (beta <= tol)
+  // is detected afterwards and the recurrence truncated there, exactly like the
+  // reference's early exit (later entries are never read).
+  for (int j = 0; j < m; ++j) {
+    const double* qj = Q.ptr() + j * Q.ld;
+    K.gemv_t(A, qj, w);                 // w = A q_j (A symmetric)
+    K.dot(qj, w, n, ab + j);            // alpha_j before reorthogonalisation (kernels.cpp:402-404)
+    for (int pass = 0; pass < 2; ++pass) {  // two-pass full reorthogonalisation (CGS2)
+      K.gemv_t(Q.sub(0, 0, n, j + 1), w, h);
+      sub_qh_kernel<<<gblocks, 256, 0, ctx.stream>>>(Q.ptr(), Q.ld, n, j + 1, h, w);
+      QDWHG_CUDA(cudaGetLastError());
+      ctx.count();
+    }
+    K.dot(w, w, n, ab + 64 + j);
+    if (j + 1 < m) {
+      scale_by_invnorm_kernel<<<gblocks, 256, 0, ctx.stream>>>(w, ab + 64 + j, n,
+                                                               Q.ptr() + (j + 1) * Q.ld);
+      QDWHG_CUDA(cudaGetLastError());
+      ctx.count();
+    }
+  }
+  std::vector<double> hab(128);
+  QDWHG_CUDA(cudaMemcpyAsync(hab.data(), ab, sizeof(double) * 128, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  const double breakdown_tol = (double)n * eps * std::max(1.0, fro);
+  std::vector<double> alpha, beta;
+  double beta_last = 0.0;
+  for (int j = 0; j < m; ++j) {
+    alpha.push_back(hab[j]);
+    const double bj = std::sqrt(hab[64 + j]);
+    beta_last = bj;
+    if (j + 1 == m || bj <= breakdown_tol) {
+      if (bj <= breakdown_tol) beta_last = 0.0;
+      break;
+    }
+    beta.push_back(bj);
+  }
+  const int k = (int)alpha.size();
+  // tridiagonal T on device, Jacobi eigensolver (kernels.cpp:426-433)
+  std::vector<double> th((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) th[i + (size_t)i * k] = alpha[i];
+  for (int i = 0; i + 1 < k; ++i) th[i + (size_t)(i + 1) * k] = th[(i + 1) + (size_t)i * k] = beta[i];
+  DMat T = ctx.arena->alloc(k, k);
+  DMat TV = ctx.arena->alloc(k, k);
+  copy_from_host(ctx, th.data(), k, T);
+  std::vector<double> tvals;
+  syev_jacobi(ctx, T, tvals, TV);
+  double s_last = 0.0;
+  QDWHG_CUDA(cudaMemcpyAsync(&s_last, TV.ptr() + (k - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  double mu = tvals[0] - beta_last * std::abs(s_last);
+  if (mu < 0.0) mu *= 1.1;
+  ctx.arena->release_to(mark);
+  return mu;
+}
+
+}  // namespace qdwhg

@@ -1,0 +1,189 @@
+"""GPU parity of the building blocks (libqdwhg.so through the C ABI) against the
+reference's golden vectors and the oracle.  Marked gpu."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import qdwh_oracle as O
+from paper_2104_14186_b200 import qdwh
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("m,n,k", [(64, 64, 64), (300, 257, 129), (1024, 512, 2048), (17, 900, 33)])
+def test_gemm_dmma(cuda, ta, tb, m, n, k):
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(m * 7 + n * 3 + k)
+    A = torch.randn((k, m) if ta else (m, k), generator=g, dtype=torch.float64).to(cuda)
+    B = torch.randn((n, k) if tb else (k, n), generator=g, dtype=torch.float64).to(cuda)
+    C0 = torch.randn((m, n), generator=g, dtype=torch.float64).to(cuda)
+    C = C0.t().contiguous().t()  # column-major
+    Ac = A.t().contiguous().t()
+    Bc = B.t().contiguous().t()
+    qdwh.gemm(Ac, Bc, C, alpha=1.5, beta=-0.5, trans_a=ta, trans_b=tb)
+    ref = 1.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 0.5 * C0
+    err = (C - ref).abs().max().item()
+    assert err <= 1e-13 * max(1.0, ref.abs().max().item()) * np.sqrt(k), err
+
+
+def test_qr_factor_matches_reference():
+    g = golden("kernels")
+    q, r = qdwh.qr_factor(g["a"])
+    assert np.abs(q - g["q"]).max() < 1e-13
+    assert np.abs(r - g["r"]).max() < 1e-13 * np.abs(g["r"]).max()
+    assert np.all(np.tril(r, -1) == 0.0)
+
+
+@pytest.mark.parametrize("m,n", [(200, 130), (513, 512), (1000, 64), (70, 70), (2048, 1000)])
+def test_qr_factor_identities(m, n):
+    a = O.gaussian_matrix(m, n, 7 + m + n)
+    q, r = qdwh.qr_factor(a)
+    md = max(m, n)
+    assert np.linalg.norm(q.T @ q - np.eye(m)) <= 50 * md * O.EPS
+    assert np.linalg.norm(q @ r - a) <= 50 * md * O.EPS * np.linalg.norm(a)
+    qn, rn = np.linalg.qr(a, mode="complete")
+    # same reflector convention as the reference / LAPACK: same diag(R) signs
+    np.testing.assert_allclose(np.diag(r), np.diag(rn), rtol=1e-10, atol=1e-12)
+
+
+def test_cholesky_matches_reference():
+    g = golden("kernels")
+    w = qdwh.cholesky(g["z"])
+    assert np.abs(w - g["w"]).max() < 1e-13 * np.abs(g["w"]).max()
+
+
+@pytest.mark.parametrize("n", [50, 200, 1000, 1300])
+def test_cholesky_random_spd(n):
+    x = O.gaussian_matrix(n + 10, n, 3 + n)
+    z = x.T @ x / n + np.eye(n)
+    w = qdwh.cholesky(z)
+    assert np.all(np.tril(w, -1) == 0.0) and np.all(np.diag(w) > 0)
+    assert np.linalg.norm(w.T @ w - z) <= 1e-13 * n * np.linalg.norm(z)
+
+
+def test_cholesky_indefinite_raises():
+    z = np.eye(8)
+    z[5, 5] = -1.0
+    with pytest.raises(qdwh.NotPositiveDefinite):
+        qdwh.cholesky(z)
+
+
+@pytest.mark.parametrize("n", [2, 5, 30, 96, 160])
+def test_sym_eig_jacobi(n):
+    a = O.gaussian_matrix(n, n, 100 + n)
+    s = 0.5 * (a + a.T)
+    vals, v = qdwh.sym_eig_dense(s)
+    ref = np.linalg.eigvalsh(s)
+    np.testing.assert_allclose(vals, ref, rtol=0, atol=1e-13 * np.abs(ref).max() * n)
+    assert np.linalg.norm(s @ v - v * vals) <= 1e-13 * np.linalg.norm(s) * n
+    assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n", [300, 700])
+def test_sym_eig_divide_and_conquer(n):
+    lam = np.linspace(-1.0, 2.0, n) + 0.001 * np.sin(np.arange(n))
+    q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 5))
+    s = (q * lam) @ q.T
+    s = 0.5 * (s + s.T)
+    vals, v = qdwh.sym_eig_dense(s)
+    np.testing.assert_allclose(vals, np.sort(lam), rtol=0, atol=1e-12)
+    assert np.linalg.norm(s @ v - v * vals) <= 1e-12 * np.linalg.norm(s) * np.sqrt(n)
+    assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-12 * np.sqrt(n)
+
+
+def test_sym_eig_rejects_nonsymmetric():
+    s = np.eye(4)
+    s[0, 3] = 1.0
+    with pytest.raises(ValueError):
+        qdwh.sym_eig_dense(s)
+
+
+@pytest.mark.parametrize("m,n", [(40, 30), (300, 200)])
+def test_svd_dense(m, n):
+    a = O.gaussian_matrix(m, n, 9)
+    u, s, v = qdwh.svd_dense(a)
+    ref = np.linalg.svd(a, compute_uv=False)
+    np.testing.assert_allclose(s, ref, rtol=1e-12)
+    assert np.linalg.norm(u * s @ v.T - a) <= 1e-13 * np.linalg.norm(a) * np.sqrt(n)
+
+
+def test_norm_and_lanczos_match_reference():
+    g = golden("kernels")
+    assert abs(qdwh.two_norm_estimate(g["a"]) - float(g["norm2"])) <= 1e-12 * float(g["norm2"])
+    assert abs(qdwh.lanczos_min_bound(g["lanczos_a"]) - float(g["lanczos"])) <= 1e-10
+
+
+def test_norm_estimate_brackets():
+    # test_kernels.cpp:210-244
+    for s in range(10):
+        a = O.gaussian_matrix(30 + s, 20, 700 + s)
+        est = qdwh.two_norm_estimate(a)
+        truth = np.linalg.norm(a, 2)
+        assert 0.99 * truth <= est <= 1.10 * truth
+    with pytest.raises(ValueError):
+        qdwh.two_norm_estimate(np.zeros((3, 3)))
+
+
+def test_lanczos_lower_bound():
+    for s in range(10):
+        d = np.diag(np.linspace(-1 - s, 4, 40))
+        assert qdwh.lanczos_min_bound(d) <= -1 - s + 1e-12
+    assert qdwh.lanczos_min_bound(np.diag(np.arange(1.0, 9.0))) >= 0.0
+    ns = np.eye(5)
+    ns[0, 1] = 1.0
+    with pytest.raises(ValueError):
+        qdwh.lanczos_min_bound(ns)
+
+
+def test_qdwh_steps_match_reference():
+    g = golden("steps")
+    np.testing.assert_allclose(qdwh.qdwh_chol_step(g["x"], 0.5), g["chol"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(qdwh.qdwh_qr_step(g["x"], 0.5), g["qr"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(qdwh.qdwh_chol_step(g["xt"], 0.3), g["chol_t"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(qdwh.qdwh_qr_step(g["xt"], 1e-4), g["qr_t"], rtol=0, atol=1e-12)
+
+
+def test_qdwh_steps_identity_and_diagonal():
+    # test_polar.cpp:94-112
+    i4 = np.eye(4)
+    assert np.linalg.norm(qdwh.qdwh_chol_step(i4, 1.0) - i4) <= 1e-14
+    assert np.linalg.norm(qdwh.qdwh_qr_step(i4, 1.0) - i4) <= 1e-14
+    w = qdwh.halley_weights(0.3)
+    d = np.array([0.3, 0.55, 0.8, 1.0])
+    yc = qdwh.qdwh_chol_step(np.diag(d), 0.3)
+    yq = qdwh.qdwh_qr_step(np.diag(d), 0.3)
+    r = d * (w.a + w.b * d * d) / (1 + w.c * d * d)
+    np.testing.assert_allclose(np.diag(yc), r, rtol=1e-12)
+    np.testing.assert_allclose(np.diag(yq), r, rtol=1e-12)
+
+
+def test_fixed_iterations_match_reference():
+    f = golden("fixed")
+    r = qdwh.run_fixed_iterations(f["x0"], 0.2, 3, "CholeskyOnly")
+    np.testing.assert_allclose(r.x, f["x"], rtol=0, atol=1e-12)
+    assert r.ell_trace == list(f["ell_trace"])
+    assert np.array_equal(r.x, r.x.T)  # symmetric input stays exactly symmetric
+
+
+@pytest.mark.parametrize("name", ["polar_illcond", "polar_tall"])
+def test_polar_matches_reference(name):
+    g = golden(name)
+    p = qdwh.polar_decompose(g["a"], qdwh.PolarConfig(ell0=float(g["ell0"])))
+    assert (p.iters_qr, p.iters_chol) == (int(g["iters_qr"]), int(g["iters_chol"]))
+    a = g["a"]
+    n = a.shape[1]
+    assert np.abs(p.h - g["h"]).max() < 1e-11 * np.abs(g["h"]).max()
+    assert np.linalg.norm(p.up @ p.h - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.linalg.norm(p.up.T @ p.up - np.eye(n)) / np.sqrt(n) <= 1e-13
+    assert np.array_equal(p.h, p.h.T)
+
+
+def test_polar_config_errors():
+    a = O.gaussian_matrix(4, 4, 51)
+    with pytest.raises(ValueError):
+        qdwh.polar_decompose(a, qdwh.PolarConfig(ell0=0.0))
+    with pytest.raises(qdwh.NotConverged):
+        qdwh.polar_decompose(a, qdwh.PolarConfig(ell0=1e-6, max_iters=1))
+    with pytest.raises(ValueError):
+        qdwh.polar_decompose(O.gaussian_matrix(3, 4, 1))
