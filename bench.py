@@ -1,0 +1,461 @@
+#!/usr/bin/env python
+"""bench.py — QDWHpartial time-to-solution and sustained FP64 TFLOP/s on B200.
+
+Default workload (BASELINE.json configs[1], "cfg2"): QDWHpartial-EIG, n=4096,
+A = Q diag(lambda) Q^T with Q from QR of a seeded Gaussian, |lambda| logspaced
+over [1e-8, 1] with random signs, largest 1% (41) eigenpairs.  One step = one
+full solve (Lanczos bound, 3 Cholesky-based QDWH steps, subspace QR + diag
+scan, Q2 formation, Rayleigh-Ritz, back-transform) through libqdwhg.
+
+  value : algorithmic FP64 TFLOP/s (SURVEY.md §8(d) count with the run's own
+          ell/iterations) with A resident in HBM, CUDA events on the library's
+          stream, L2 flushed (256 MiB write) before every timed step;
+  e2e   : same metric through the public API with HOST buffers (pinned A in,
+          eigenvalues + eigenvectors out), copies inside the timed region;
+  roofline: the dominant kernel (DMMA GEMM) — algorithmic flops of every GEMM
+          launch / its CUDA-event duration, live over the timed steps, against
+          the measured DMMA peak (profiles/r01_fp64_peak_probe.txt);
+  cpu_baseline: the reference itself (oracle/_ref) on a bounded sample.
+
+--impl reference runs the reference's own CPU implementation on the host
+cores (one single-threaded reference solve per core, concurrently).
+Multi-GPU (torchrun): the path does not shard in round 1 — replicas, weak
+scaling.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.15  # DMMA m8n8k4 issue-bound probe on this pool's B200 (profiles/)
+METRIC = "QDWHpartial time-to-solution (s) and sustained FP64 TFLOP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-profile", action="store_true", help="skip live GEMM event timing")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ inputs
+def config_desc(cfg):
+    from paper_2104_14186_b200 import matgen
+    c = dict(matgen.CONFIGS[cfg])
+    return c
+
+
+def make_input(cfg, dev, handle):
+    """Synthetic config input generated on the GPU (seeded Gaussian, our own QR)."""
+    import torch
+    from paper_2104_14186_b200 import matgen, qdwh
+    c = config_desc(cfg)
+    if c["kind"] == "eig":
+        n = c["n"]
+        if c["family"] == "wishart":
+            G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=handle)
+            A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+            qdwh.gemm(G, G, A, alpha=1.0 / n, trans_a=True, handle=handle)
+            A -= torch.eye(n, dtype=torch.float64, device=dev)
+            A = 0.5 * (A + A.t())
+            A = A.t().contiguous().t()
+            return dict(A=A, c=c["shift"], k=c["k"], truth=None, kind="eig")
+        lam = matgen.config_eigenvalues(c["family"], n, c["seed"])
+        G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=handle)
+        Q, _ = qdwh.qr_factor(G, handle=handle)
+        QL = (Q * torch.from_numpy(lam).to(dev)[None, :]).t().contiguous().t()
+        A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+        qdwh.gemm(QL, Q, A, trans_b=True, handle=handle)
+        A = (0.5 * (A + A.t())).t().contiguous().t()
+        k = c["k"]
+        cs = matgen.largest_k_shift(lam, k)
+        return dict(A=A, c=cs, k=k, truth=np.sort(lam)[::-1][:k], kind="eig")
+    m, n = c["m"], c["n"]
+    sig = matgen.config_singular_values(c["family"], n)
+    Gl = qdwh.gaussian_matrix_device(m, n, c["seed"] ^ matgen.LEFT_STREAM, device=dev, handle=handle)
+    U, _ = qdwh.qr_factor(Gl, handle=handle) if m == n else (None, None)
+    if m != n:
+        # thin Q of the tall Gaussian: first n columns of the QR's Q
+        U = thin_q(Gl, handle)
+    Gr = qdwh.gaussian_matrix_device(n, n, c["seed"] ^ matgen.RIGHT_STREAM, device=dev, handle=handle)
+    V, _ = qdwh.qr_factor(Gr, handle=handle)
+    US = (U[:, :n] * torch.from_numpy(sig).to(dev)[None, :]).t().contiguous().t()
+    A = torch.empty((n, m), dtype=torch.float64, device=dev).t()
+    qdwh.gemm(US, V, A, trans_b=True, handle=handle)
+    k = c["k"]
+    return dict(A=A, cut=matgen.sigma_cut(sig, k), k=k, truth=np.sort(sig)[::-1][:k], kind="svd")
+
+
+def thin_q(G, handle):
+    from paper_2104_14186_b200 import qdwh
+    Q, _ = qdwh.qr_factor(G, handle=handle)
+    return Q[:, :G.shape[1]]
+
+
+def solve(inp, handle, host=False):
+    from paper_2104_14186_b200 import qdwh
+    A = inp["A_host"] if host else inp["A"]
+    if inp["kind"] == "eig":
+        return qdwh.partial_eig_request(A, "largest", inp["c"], inp["k"], handle=handle)
+    return qdwh.partial_svd_request(A, cut=inp["cut"], k=inp["k"], handle=handle)
+
+
+# ------------------------------------------------------------------ CPU legs
+def ref_sample(cfg):
+    """Bounded sample of the workload for the CPU reference: same spectrum family,
+    n scaled so one single-threaded reference solve takes ~5-10 s."""
+    from oracle import qdwh_oracle as O
+    from paper_2104_14186_b200 import matgen
+    c = config_desc(cfg)
+    if c["kind"] == "eig":
+        n = 1024
+        frac = c["k"] / c["n"]
+        k = max(1, int(round(frac * n)))
+        if c["family"] == "wishart":
+            g = O.gaussian_matrix(n, n, c["seed"])
+            a = g.T @ g / n - np.eye(n)
+            a = 0.5 * (a + a.T)
+            w = np.linalg.eigvalsh(a)
+            cs = matgen.largest_k_shift(w, k)
+        else:
+            lam = matgen.config_eigenvalues(c["family"], n, c["seed"])
+            q, _ = np.linalg.qr(O.gaussian_matrix(n, n, c["seed"]))
+            a = (q * lam) @ q.T
+            a = 0.5 * (a + a.T)
+            cs = matgen.largest_k_shift(lam, k)
+        return dict(kind="eig", b=cs * np.eye(n) - a, n=n, k=k,
+                    desc=f"cfg{cfg} family ({c['family']} spectrum, largest {k}) at n={n}, "
+                         f"1 reference qdwh_partial_eig solve")
+    m, n = (1024, 1024) if c["m"] == c["n"] else (2048, 512)
+    sig = matgen.config_singular_values(c["family"], n)
+    ul, _ = np.linalg.qr(O.gaussian_matrix(m, n, c["seed"] ^ matgen.LEFT_STREAM))
+    vr, _ = np.linalg.qr(O.gaussian_matrix(n, n, c["seed"] ^ matgen.RIGHT_STREAM))
+    a = (ul * sig) @ vr.T
+    k = max(1, int(round(c["k"] / c["n"] * n)))
+    return dict(kind="svd", a=a, m=m, n=n, k=k, cut=matgen.sigma_cut(sig, k),
+                desc=f"cfg{cfg} family ({c['family']} spectrum, top {k}) at {m}x{n}, "
+                     f"1 reference qdwh_partial_svd solve")
+
+
+def ref_solve_flops(sample):
+    """Run one reference solve; return (seconds, algorithmic flops)."""
+    from oracle import qdwh_oracle as O
+    from oracle import ref as R
+    t0 = time.perf_counter()
+    if sample["kind"] == "eig":
+        lam, v, d = R.partial_eig(sample["b"], 3)
+        dt = time.perf_counter() - t0
+        fl = O.flops_partial_eig(sample["n"], d["subspace_size"], d["k"], d["iters_chol"], False)
+    else:
+        alpha = R.two_norm_estimate(sample["a"])
+        t0 = time.perf_counter()
+        s, u, v, d = R.partial_svd(sample["a"], sample["cut"] / alpha)
+        dt = time.perf_counter() - t0
+        fl = O.flops_partial_svd(sample["m"], sample["n"], d["subspace_size"], d["k"], d["iters_qr"],
+                                 d["iters_chol"], False)
+    return dt, fl
+
+
+def _ref_worker(args):
+    cfg = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    s = ref_sample(cfg)
+    return ref_solve_flops(s)
+
+
+def cpu_baseline(cfg):
+    from oracle import ref as R
+    if not R.available():
+        return None
+    s = ref_sample(cfg)
+    dt, fl = ref_solve_flops(s)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": 1, "kind": "reference",
+            "sample": s["desc"], "seconds": dt,
+            "host_cpu": cpu_model(), "host_cores": os.cpu_count()}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args, rank):
+    from oracle import ref as R
+    cfgd = config_desc(args.config)
+    base = {"metric": METRIC, "impl": "reference"}
+    if rank != 0:
+        return None
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libqdwhref.so not built"}))
+        return None
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    sample = ref_sample(args.config)
+    times, flops = [], []
+    with mp.get_context("fork").Pool(cores) as pool:
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, [args.config] * cores)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                flops.append(sum(r[1] for r in res))
+    value = sum(flops) / sum(times) / 1e12
+    line = dict(base, value=value, unit="TFLOP/s", n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * float(np.mean(times)),
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic", config=config_json(args.config, args.gpus),
+                cpu_baseline={"value": value, "unit": "TFLOP/s", "cores": cores,
+                              "kind": "reference",
+                              "sample": f"{cores} concurrent single-threaded reference solves per "
+                                        f"step, each: {sample['desc']}"},
+                e2e={"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0},
+                host_cpu=cpu_model())
+    print(json.dumps(line))
+    return line
+
+
+def config_json(cfg, gpus):
+    c = config_desc(cfg)
+    d = {"workload": f"cfg{cfg}: QDWHpartial-{c['kind'].upper()} "
+                     + (f"n={c['n']}" if c["kind"] == "eig" else f"{c['m']}x{c['n']}")
+                     + f" {c['family']} spectrum, top {c['k']}",
+         "k": c["k"], "parallelism": f"replicas{gpus}" if gpus > 1 else "single",
+         "l2": "flushed (256 MiB write) before every timed step"}
+    d.update({kk: v for kk, v in c.items() if kk in ("n", "m")})
+    return d
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2104_14186_b200 import qdwh
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    handle = qdwh.Handle(device=local)
+    handle.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+
+    inp = make_input(args.config, dev, handle)
+    n_rows = inp["A"].shape[0]
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 0)):
+        res = solve(inp, handle)
+    barrier()
+
+    # ---- timed: device-resident A (value)
+    if not args.no_profile:
+        handle.profile(True)
+        handle.kernel_stats()  # reset
+    launches0 = handle.launches()
+    sampler = ClockSampler(local)
+    sampler.start()
+    times, flops = [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for s in range(args.steps):
+        flush.fill_(float(s))
+        torch.cuda.synchronize(dev)
+        e0.record()
+        res = solve(inp, handle)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        times.append(e0.elapsed_time(e1) / 1e3)
+        flops.append(res.flops)
+    clocks = sampler.stop()
+    launches = (handle.launches() - launches0) // max(args.steps, 1)
+    kst = handle.kernel_stats() if not args.no_profile else None
+    handle.profile(False)
+
+    # ---- timed: host buffers (e2e)
+    e2e_steps = args.e2e_steps or args.steps
+    A_pin = torch.empty((n_rows, inp["A"].shape[1]), dtype=torch.float64).t().contiguous().t()
+    A_pin = A_pin.pin_memory() if torch.cuda.is_available() else A_pin
+    A_pin.copy_(inp["A"].cpu())
+    inp["A_host"] = A_pin.numpy()
+    res_h = solve(inp, handle, host=True)  # warm the host path once
+    e2e_t, e2e_f = [], []
+    for s in range(e2e_steps):
+        flush.fill_(float(s))
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        res_h = solve(inp, handle, host=True)
+        torch.cuda.synchronize(dev)
+        e2e_t.append(time.perf_counter() - t0)
+        e2e_f.append(res_h.flops)
+    k = res.count()
+    h2d = inp["A"].shape[0] * inp["A"].shape[1] * 8
+    if inp["kind"] == "eig":
+        d2h = k * 8 + n_rows * k * 8
+    else:
+        d2h = k * 8 + (inp["A"].shape[0] + inp["A"].shape[1]) * k * 8
+
+    # ---- correctness of what was timed (device residual / orthogonality, planted truth)
+    check = verify(inp, res)
+
+    # ---- aggregate over ranks (max time, summed work)
+    tot_t, tot_f = float(sum(times)), float(sum(flops))
+    e_t, e_f = float(sum(e2e_t)), float(sum(e2e_f))
+    if world > 1:
+        tt = torch.tensor([tot_t, tot_f, e_t, e_f], dtype=torch.float64, device=dev)
+        mx = tt.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        tot_t, e_t = float(mx[0]), float(mx[2])
+        tot_f, e_f = float(tt[1]), float(tt[3])
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    value = tot_f / tot_t / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian factors, planted spectrum, generated on device)",
+        "config": config_json(args.config, world),
+        "time_to_solution_s": tot_t / args.steps,
+        "e2e": {"value": e_f / e_t / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "time_to_solution_s": e_t / e2e_steps},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "result": {"k": k, "subspace_size": res.subspace_size, "iters_chol": res.iters_chol,
+                   "iters_qr": res.iters_qr, "algorithmic_flops": flops[-1],
+                   "stage_seconds": [round(x, 6) for x in res.stage_seconds], **check},
+    }
+    if kst and kst["gemm_seconds"] > 0:
+        ach = kst["gemm_flops"] / kst["gemm_seconds"] / 1e12
+        line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                            "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                            "kernel": "gemm_dmma_kernel (TMA + DMMA.8x8x4)",
+                            "peak_source": "measured DMMA m8n8k4 probe (MEASURED_PEAKS.json has no FP64 entry)",
+                            "launches_per_step": kst["gemm_timed_launches"] / args.steps,
+                            "share_of_step": kst["gemm_seconds"] / tot_t}
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_baseline(args.config)
+        if cb:
+            line["cpu_baseline"] = cb
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def verify(inp, res):
+    import torch
+    A = inp["A"]
+    out = {}
+    k = res.count()
+    if k == 0:
+        return {"k": 0}
+    if inp["kind"] == "eig":
+        V = res.v
+        lam = torch.from_numpy(np.array(res.lambda_minus)).to(A.device)
+        R = A @ V - V * lam[None, :]
+        out["resid"] = float(torch.linalg.norm(R) / torch.linalg.norm(A))
+        out["orth"] = float(torch.linalg.norm(V.T @ V - torch.eye(k, dtype=A.dtype, device=A.device)))
+        vals = np.array(res.lambda_minus)
+    else:
+        U, V = res.u1, res.v1
+        s = torch.from_numpy(np.array(res.sigma1)).to(A.device)
+        out["resid"] = float(torch.linalg.norm(A @ V - U * s[None, :]) / torch.linalg.norm(A))
+        out["orth"] = float(torch.linalg.norm(V.T @ V - torch.eye(k, dtype=A.dtype, device=A.device)))
+        vals = np.array(res.sigma1)
+    n = A.shape[1]
+    out["gate_sqrt_n"] = 1e-12 * float(np.sqrt(n))
+    if inp.get("truth") is not None and len(inp["truth"]) == k:
+        out["max_rel_err_vs_planted"] = float(np.max(np.abs(vals - inp["truth"]) / np.abs(inp["truth"])))
+    return out
+
+
+if __name__ == "__main__":
+    main()

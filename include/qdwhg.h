@@ -152,6 +152,22 @@ qdwhg_status qdwhg_destroy(qdwhg_handle* h);
 const char* qdwhg_last_error(const qdwhg_handle* h);
 qdwhg_status qdwhg_get_launch_count(const qdwhg_handle* h, uint64_t* launches);
 qdwhg_status qdwhg_synchronize(qdwhg_handle* h);
+/* Run on a caller stream (cudaStream_t, e.g. torch's current stream); NULL
+ * restores the handle's own stream.  Calls stay synchronous. */
+qdwhg_status qdwhg_set_stream(qdwhg_handle* h, void* stream);
+
+/* Live kernel accounting: with profiling enabled every DMMA GEMM launch is
+ * bracketed by CUDA events on its stream; get_kernel_stats returns and resets
+ * the event-timed totals (launch counters are cumulative). */
+typedef struct qdwhg_kernel_stats {
+  uint64_t gemm_launches;       /* cumulative */
+  uint64_t other_launches;      /* cumulative, all other libqdwhg kernels */
+  uint64_t gemm_timed_launches; /* since the last get_kernel_stats */
+  double gemm_seconds;          /* sum of event-timed GEMM durations */
+  double gemm_flops;            /* sum of algorithmic flops of those launches */
+} qdwhg_kernel_stats;
+qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable);
+qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out);
 
 /* ---- drivers ------------------------------------------------------------ */
 qdwhg_status qdwhg_partial_eig(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,

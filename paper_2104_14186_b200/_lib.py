@@ -55,6 +55,11 @@ class PolarInfo(ctypes.Structure):
                 ("n_trace", _I32), ("ell_trace", _D * MAX_TRACE), ("seconds", _D), ("flops", _D)]
 
 
+class KernelStats(ctypes.Structure):
+    _fields_ = [("gemm_launches", _U64), ("other_launches", _U64), ("gemm_timed_launches", _U64),
+                ("gemm_seconds", _D), ("gemm_flops", _D)]
+
+
 class EigRequest(ctypes.Structure):
     _fields_ = [("which", _I32), ("iters", _I32), ("c", _D), ("k", _I64), ("tol", _D),
                 ("randomize", _I32), ("reserved", _I32), ("seed", _U64)]
@@ -72,6 +77,9 @@ SIGNATURES = {
     "qdwhg_last_error": [_P],
     "qdwhg_get_launch_count": [_P, _P],
     "qdwhg_synchronize": [_P],
+    "qdwhg_set_stream": [_P, _P],
+    "qdwhg_profile": [_P, _I32],
+    "qdwhg_get_kernel_stats": [_P, _P],
     "qdwhg_partial_eig": [_P, _I64, _P, _I64, _I64, _I32, _D, _U64, _P, _P, _I64, _I64, _P],
     "qdwhg_partial_eig_request": [_P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P],
     "qdwhg_partial_svd": [_P, _I64, _I64, _P, _I64, _D, _D, _I32, _U64, _P, _P, _I64, _P, _I64,

@@ -68,6 +68,36 @@ DMat Arena::alloc(int64_t rows, int64_t cols) {
   return m;
 }
 
+void Ctx::prof_begin(double flops) {
+  if (ev_pool.size() < 2 * (ev_used + 1)) {
+    for (int i = 0; i < 512; ++i) {
+      cudaEvent_t e;
+      QDWHG_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+  }
+  ev_flops.resize(ev_used + 1);
+  ev_flops[ev_used] = flops;
+  QDWHG_CUDA(cudaEventRecord(ev_pool[2 * ev_used], stream));
+}
+void Ctx::prof_end() {
+  QDWHG_CUDA(cudaEventRecord(ev_pool[2 * ev_used + 1], stream));
+  ++ev_used;
+  if (ev_used >= 4096) prof_collect();  // bound the number of pending events
+}
+void Ctx::prof_collect() {
+  if (ev_used == 0) return;
+  QDWHG_CUDA(cudaEventSynchronize(ev_pool[2 * ev_used - 1]));
+  for (size_t i = 0; i < ev_used; ++i) {
+    float ms = 0.f;
+    QDWHG_CUDA(cudaEventElapsedTime(&ms, ev_pool[2 * i], ev_pool[2 * i + 1]));
+    gemm_ms += ms;
+    gemm_flops += ev_flops[i];
+  }
+  gemm_timed += ev_used;
+  ev_used = 0;
+}
+
 std::vector<double> host_gaussian(int64_t count, uint64_t seed) {
   // kernels.cpp:16-32 restated (splitmix64 + Box-Muller on counters 2i, 2i+1);
   // glibc log/cos, so bit-identical to the reference's gaussian_matrix.
@@ -236,7 +266,7 @@ qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
 qdwhg_status qdwhg_destroy(qdwhg_handle* h) {
   if (!h) return QDWHG_OK;
   cudaSetDevice(h->device);
-  cudaStreamSynchronize(h->stream);
+  cudaStreamSynchronize(h->ctx.stream);
   cudaFree(h->ctx.dscratch);
   cudaFreeHost(h->ctx.hscratch);
   cudaFree(h->ctx.dflag);
@@ -254,7 +284,38 @@ qdwhg_status qdwhg_get_launch_count(const qdwhg_handle* h, uint64_t* launches) {
 }
 
 qdwhg_status qdwhg_synchronize(qdwhg_handle* h) {
-  return guard(h, [&] { QDWHG_CUDA(cudaStreamSynchronize(h->stream)); });
+  return guard(h, [&] { QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream)); });
+}
+
+qdwhg_status qdwhg_set_stream(qdwhg_handle* h, void* stream) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream));
+    h->ctx.stream = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+  });
+}
+
+qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    h->ctx.prof_collect();
+    h->ctx.profile = enable != 0;
+  });
+}
+
+qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out) {
+  if (!h || !out) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    h->ctx.prof_collect();
+    out->gemm_launches = h->ctx.gemm_launches;
+    out->other_launches = h->ctx.other_launches;
+    out->gemm_timed_launches = h->ctx.gemm_timed;
+    out->gemm_seconds = h->ctx.gemm_ms * 1e-3;
+    out->gemm_flops = h->ctx.gemm_flops;
+    h->ctx.gemm_timed = 0;
+    h->ctx.gemm_ms = 0.0;
+    h->ctx.gemm_flops = 0.0;
+  });
 }
 
 // ---------------------------------------------------------------- drivers
@@ -654,8 +715,21 @@ qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64
     Cd.cols = n;
     if (!is_device_ptr(A) || !is_device_ptr(B) || !is_device_ptr(C))
       throw InvalidArgument("qdwhg_gemm: operands must be device pointers");
-    gemm(h->ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cd);
-    QDWHG_CUDA(cudaStreamSynchronize(h->stream));
+    // TMA needs 16-byte aligned bases and even leading dimensions: stage others
+    auto aligned = [](const DMat& d) {
+      return (d.ld % 2 == 0) && (reinterpret_cast<uintptr_t>(d.base) % 16 == 0);
+    };
+    Ctx& ctx = h->ctx;
+    if (!aligned(Ad)) Ad = stage_in(ctx, A, Ad.rows, Ad.cols, lda, nullptr);
+    if (!aligned(Bd)) Bd = stage_in(ctx, B, Bd.rows, Bd.cols, ldb, nullptr);
+    if (!aligned(Cd)) {
+      DMat Cs = stage_in(ctx, C, m, n, ldc, nullptr);
+      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cs);
+      stage_out(ctx, Cs, C, ldc);
+    } else {
+      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cd);
+    }
+    QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream));
   });
 }
 
@@ -670,7 +744,7 @@ qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64
     Ad.rows = m;
     Ad.cols = n;
     gaussian_fill(h->ctx, Ad, seed);
-    QDWHG_CUDA(cudaStreamSynchronize(h->stream));
+    QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream));
   });
 }
 

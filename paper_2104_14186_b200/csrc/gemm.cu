@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <mutex>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -316,6 +318,25 @@ CUtensorMap make_desc(const DMat& v, int box0, int box1) {
   return tm;
 }
 
+// Useful FP64 flops of one launch (zeros of triangular operands and the
+// mirrored half of a symmetric output are not counted).
+double algorithmic_flops(const GemmParams& p) {
+  const double M = p.M, N = p.N, K = p.K;
+  auto tri = [](double rows, double len, double kmax) {
+    // sum_{j<len} min(kmax, j+1)
+    const double full = std::min(len, kmax);
+    return full * (full + 1) / 2 + std::max(0.0, len - kmax) * kmax;
+  };
+  if (p.omode == (int)OutMode::LowerMirror) return K * N * (N + 1);
+  switch ((KRange)p.kmode) {
+    case KRange::BUpper: return 2 * M * tri(M, N, K);
+    case KRange::BLower: return 2 * M * tri(M, std::min(N, K), K);  // sum_j (K - j)
+    case KRange::AUpper: return 2 * N * tri(N, std::min(M, K), K);
+    case KRange::ALower: return 2 * N * tri(N, M, K);
+    default: return 2 * M * N * K;
+  }
+}
+
 template <int BM, int BN, int WM, int WN, int STAGES, bool AK, bool BK_>
 void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
   constexpr int threads = WM * WN * 32;
@@ -334,8 +355,19 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
   else
     ntiles = p.tiles_m * p.tiles_n;
   dim3 grid(ntiles, 1, p.splits);
+  static const bool debug = getenv("QDWHG_DEBUG") != nullptr;
+  if (debug)
+    fprintf(stderr,
+            "gemm BM=%d AK=%d BK=%d M=%d N=%d K=%d kmode=%d omode=%d splits=%d tiles=%dx%d "
+            "A(r0=%ld c0=%ld %ldx%ld ld=%ld) B(r0=%ld c0=%ld %ldx%ld ld=%ld)\n",
+            BM, (int)AK, (int)BK_, p.M, p.N, p.K, p.kmode, p.omode, p.splits, p.tiles_m, p.tiles_n,
+            (long)A.r0, (long)A.c0, (long)A.rows, (long)A.cols, (long)A.ld, (long)B.r0,
+            (long)B.c0, (long)B.rows, (long)B.cols, (long)B.ld);
+  if (ctx.profile) ctx.prof_begin(algorithmic_flops(p));
   kern<<<grid, threads, smem, ctx.stream>>>(ta, tb, p);
   QDWHG_CUDA(cudaGetLastError());
+  if (ctx.profile) ctx.prof_end();
+  if (debug) QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
   ctx.gemm_launches++;
 }
 
@@ -362,6 +394,24 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   if ((A.ld % 2) || (B.ld % 2) || (reinterpret_cast<uintptr_t>(A.base) % 16) ||
       (reinterpret_cast<uintptr_t>(B.base) % 16))
     throw InvalidArgument("gemm: operands must be 16-byte aligned with even leading dimension");
+  // TMA box starts must be 16-byte aligned in the contiguous dimension: an odd
+  // row offset (e.g. Q2 = Q(m:m+n, :) with odd m in the QR step) is staged
+  // into an aligned copy first.
+  if ((A.r0 & 1) || (B.r0 & 1)) {
+    const Arena::Mark m0 = ctx.arena->mark();
+    DMat A2 = A, B2 = B;
+    if (A.r0 & 1) {
+      A2 = ctx.arena->alloc(A.rows, A.cols);
+      copy(ctx, A, A2);
+    }
+    if (B.r0 & 1) {
+      B2 = ctx.arena->alloc(B.rows, B.cols);
+      copy(ctx, B, B2);
+    }
+    gemm(ctx, ta, tb, alpha, A2, B2, beta, C, ex);
+    ctx.arena->release_to(m0);
+    return;
+  }
 
   GemmParams p{};
   p.M = (int)M;

@@ -209,11 +209,11 @@ void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
   int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
   int rpc = (mp + nblk - 1) / nblk;
   const size_t smem = ((size_t)kBW * (rpc | 1) + (kPanelThreads / kBW) * kBW + kBW) * 8;
-  if (smem > 227 * 1024) throw InvalidArgument("geqrf: panel too tall for shared memory");
+  if (smem > 220 * 1024) throw InvalidArgument("geqrf: panel too tall for shared memory");
   static bool set = false;
   if (!set) {
     QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     set = true;
   }
   QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));

@@ -105,6 +105,17 @@ struct Ctx {
   uint64_t gemm_launches = 0;   // our kernels launched (for bench accounting)
   uint64_t other_launches = 0;
   void count(int n = 1) { other_launches += n; }
+  // Live GEMM profiling: CUDA events around every DMMA GEMM launch on the
+  // launching stream (qdwhg_profile / qdwhg_get_kernel_stats).
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<double> ev_flops;  // algorithmic flops of launch i (events 2i, 2i+1)
+  size_t ev_used = 0;
+  double gemm_ms = 0.0, gemm_flops = 0.0;
+  uint64_t gemm_timed = 0;
+  void prof_begin(double flops);
+  void prof_end();
+  void prof_collect();
 };
 
 // ------------------------------------------------------------------ gemm.cu

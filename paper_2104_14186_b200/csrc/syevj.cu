@@ -170,7 +170,9 @@ void syev_jacobi(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat&
   static bool set = false;
   if (!set) {
     QDWHG_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    227 * 1024));
+                                    (int)(((size_t)kJacobiMax * (kJacobiMax + 1) +
+                                           2 * (kJacobiMax / 2 + 1)) * 8 +
+                                          2 * (kJacobiMax / 2 + 1) * 4)));
     set = true;
   }
   const Arena::Mark mark = ctx.arena->mark();

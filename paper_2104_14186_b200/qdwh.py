@@ -69,6 +69,21 @@ class Handle:
         self.check(self.lib.qdwhg_get_launch_count(self.h, ctypes.byref(v)))
         return v.value
 
+    def set_stream(self, stream_ptr: int = 0):
+        """Run on a caller CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
+        self.check(self.lib.qdwhg_set_stream(self.h, ctypes.c_void_p(stream_ptr or None)))
+
+    def profile(self, enable: bool = True):
+        """Bracket every DMMA GEMM launch with CUDA events (live kernel timing)."""
+        self.check(self.lib.qdwhg_profile(self.h, int(bool(enable))))
+
+    def kernel_stats(self) -> dict:
+        st = _lib.KernelStats()
+        self.check(self.lib.qdwhg_get_kernel_stats(self.h, ctypes.byref(st)))
+        return dict(gemm_launches=st.gemm_launches, other_launches=st.other_launches,
+                    gemm_timed_launches=st.gemm_timed_launches, gemm_seconds=st.gemm_seconds,
+                    gemm_flops=st.gemm_flops)
+
     def close(self):
         if self.h:
             self.lib.qdwhg_destroy(self.h)
