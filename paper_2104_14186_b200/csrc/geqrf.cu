@@ -43,12 +43,12 @@ QDWHG_DEV void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
   __syncthreads();
   ++epoch;
   if (threadIdx.x == 0) {
-    __threadfence();
+    // bar.sync orders the CTA's prior writes/atomics before thread 0's
+    // gpu-scope release (cumulativity); acquire on the poll orders what follows.
     red_release_add(bar, 1u);
     const unsigned target = epoch * nblocks;
     while (ld_acquire(bar) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -170,25 +170,43 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     }
 }
 
-// T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise):
-// T(i,i) = tau_i, T(0:i, i) = -tau_i * T(0:i, 0:i) * G(0:i, i).
+// T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise),
+// by recursive doubling instead of the column recurrence:
+//   T = [T11, -T11 (V1^T V2) T22; 0, T22],  V1^T V2 = G12,
+// block size s = 1, 2, 4, ... — 2 barriers per level, log2(b) levels.
 __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, double* T,
                              int64_t ldt, int b) {
-  __shared__ double Ts[kBW][kBW + 1];
-  __shared__ double g[kBW];
+  extern __shared__ double larft_sm[];
+  double(*Ts)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm);
+  double(*M)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm + kBW * (kBW + 1));
   const int t = threadIdx.x;
-  for (int i = t; i < kBW * kBW; i += blockDim.x) Ts[i % kBW][i / kBW] = 0.0;
+  for (int i = t; i < kBW * kBW; i += blockDim.x) {
+    const int r = i % kBW, c = i / kBW;
+    Ts[r][c] = (r == c && r < b) ? tau[r] : 0.0;
+  }
   __syncthreads();
-  for (int i = 0; i < b; ++i) {
-    const double ti = tau[i];
-    if (t < i) g[t] = G[t + (int64_t)i * ldg];
-    __syncthreads();
-    if (t < i) {
-      double s = 0.0;
-      for (int k = t; k < i; ++k) s += Ts[t][k] * g[k];
-      Ts[t][i] = -ti * s;
+  for (int s = 1; s < b; s *= 2) {
+    // M(a+r, a+s+c) = sum_{k=r}^{s-1} T11(r, k) G(a+k, a+s+c)
+    for (int i = t; i < b * s; i += blockDim.x) {
+      const int r = i % s, rest = i / s;          // rest = a/(2s) * s + c  over all pairs
+      const int pair = rest / s, c = rest % s;
+      const int a = pair * 2 * s;
+      if (a + s + c >= b) continue;
+      double acc = 0.0;
+      for (int k = r; k < s; ++k) acc += Ts[a + r][a + k] * G[(a + k) + (int64_t)(a + s + c) * ldg];
+      M[a + r][a + s + c] = acc;
     }
-    if (t == i) Ts[i][i] = ti;
+    __syncthreads();
+    // T12(r, c) = -sum_{k=0}^{c} M(a+r, a+s+k) T22(k, c)
+    for (int i = t; i < b * s; i += blockDim.x) {
+      const int r = i % s, rest = i / s;
+      const int pair = rest / s, c = rest % s;
+      const int a = pair * 2 * s;
+      if (a + s + c >= b) continue;
+      double acc = 0.0;
+      for (int k = 0; k <= c; ++k) acc += M[a + r][a + s + k] * Ts[a + s + k][a + s + c];
+      Ts[a + r][a + s + c] = -acc;
+    }
     __syncthreads();
   }
   for (int i = t; i < b * b; i += blockDim.x) {
@@ -255,7 +273,13 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     const DMat Gp = G.sub(0, 0, b, b);
     gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
     const DMat Tp = w.T.sub(0, p * nb, b, b);
-    larft_kernel<<<1, 64, 0, ctx.stream>>>(Gp.ptr(), Gp.ld, tau_dev + j0, Tp.ptr(), Tp.ld, (int)b);
+    static bool larft_attr = false;
+    if (!larft_attr) {
+      QDWHG_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      2 * kBW * (kBW + 1) * 8));
+      larft_attr = true;
+    }
+    larft_kernel<<<1, 256, 2 * kBW * (kBW + 1) * 8, ctx.stream>>>(Gp.ptr(), Gp.ld, tau_dev + j0, Tp.ptr(), Tp.ld, (int)b);
     QDWHG_CUDA(cudaGetLastError());
     ctx.count();
     // trailing update C = (I - V T V^T)^T C = C - V T^T (V^T C)

@@ -19,93 +19,243 @@ namespace qdwhg {
 
 namespace {
 
-constexpr int kDiagThreads = 512;
+constexpr int kDiagThreads = 256;
 
-// Factor the nb x nb block Zkk (symmetric; reads the lower triangle) -> W_kk
-// (upper, written to W) and W_kk^{-1} (upper, written to Winv).
-template <int NB>
+// 1/sqrt(d) without the libdevice slow-path call (which forces the unrolled
+// register row to the stack): float seed + 3 Newton steps, exponent-scaled so
+// any positive double works.  Non-positive d returns NaN (the caller flags it).
+QDWHG_DEV double rsqrt_newton(double d) {
+  if (!(d > 0.0)) return __longlong_as_double(0x7ff8000000000000ll);
+  const int e = ((__double2hiint(d) >> 20) & 0x7ff) - 1023;  // d = m * 2^e, m in [1, 2)
+  const int h = e >> 1;                                       // floor(e/2)
+  const double m = __hiloint2double(__double2hiint(d) - (h << 21), __double2loint(d));  // d / 4^h
+  double y = (double)rsqrtf((float)m);
+#pragma unroll
+  for (int it = 0; it < 3; ++it) y = y * (1.5 - 0.5 * m * y * y);
+  return __hiloint2double(__double2hiint(y) - (h << 20), __double2loint(y));  // y / 2^h
+}
+constexpr int kSB = 32;          // sub-block handled by one warp
+constexpr int kLDA = 129;        // padded smem leading dimension (odd -> conflict free)
+
+// One right-looking Cholesky column step of a 32x32 block held as one row per
+// lane; template recursion guarantees compile-time register indices.
+template <int J>
+struct CholStep {
+  static QDWHG_DEV void run(double (&row)[kSB], int lane, bool& bad, double& my_inv) {
+    const double djj = __shfl_sync(0xffffffffu, row[J], J);
+    if (!(djj > 0.0)) bad = true;
+    const double inv = rsqrt_newton(djj);
+    if (lane > J) row[J] *= inv;
+    if (lane == J) {
+      row[J] = djj * inv;
+      my_inv = inv;
+    }
+#pragma unroll
+    for (int c = J + 1; c < kSB; ++c) {
+      const double lcj = __shfl_sync(0xffffffffu, row[J], c);
+      if (lane >= c) row[c] -= row[J] * lcj;
+    }
+    CholStep<J + 1>::run(row, lane, bad, my_inv);
+  }
+};
+template <>
+struct CholStep<kSB> {
+  static QDWHG_DEV void run(double (&)[kSB], int, bool&, double&) {}
+};
+
+// Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
+// -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
+// all in shared memory, blocked by 32:
+//   per 32-column step: warp 0 factors + inverts the 32x32 diagonal block in
+//   registers (shuffles, no CTA barrier), the panel below is L_p = Z_p D^{-T},
+//   the trailing lower triangle gets a rank-32 update with 4x4 register tiles;
+//   then L^{-1} column block by column block: Linv_ij = -D_i^{-1} sum_k L_ik Linv_kj.
+// The block is padded to a multiple of 32 with an identity (chol([Z 0;0 I]) = [L 0;0 I]).
 __global__ void __launch_bounds__(kDiagThreads, 1)
     potrf_diag_kernel(const double* Z, int64_t ldz, double* W, int64_t ldw, double* Winv,
                       int64_t ldwi, int nb, int* flag) {
   extern __shared__ double sm[];
-  constexpr int LDS = NB + 1;
-  double* L = sm;                  // column-major L[c*LDS + r], lower
-  double* X = sm + NB * LDS;       // inverse scratch: 64 columns X[g*LDS + r]
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  constexpr int NW = kDiagThreads / 32;
+  double* A = sm;                          // 128 x kLDA, column-major, lower = L
+  double* Dinv = A + 128 * kLDA;           // 4 blocks of 32 x 33 (column-major, lower)
+  double* T = Dinv + 4 * kSB * 33;         // 32 columns x kLDA: panel temp / Linv column block
+  double* S = T + kSB * kLDA;              // 32 x 33 scratch
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nbp = ((nb + kSB - 1) / kSB) * kSB;
+  const int nsb = nbp / kSB;
+  if (tid == 0) bad_s = 0;
 
-  // load lower triangle (column-major, coalesced down columns)
-  for (int c = warp; c < nb; c += NW)
-    for (int r = lane; r < nb; r += 32) L[c * LDS + r] = (r >= c) ? Z[r + (int64_t)c * ldz] : 0.0;
+  for (int idx = tid; idx < nbp * nbp; idx += kDiagThreads) {
+    const int r = idx % nbp, c = idx / nbp;
+    double v = 0.0;
+    if (r >= c) v = (r < nb && c < nb) ? Z[r + (int64_t)c * ldz] : (r == c ? 1.0 : 0.0);
+    A[c * kLDA + r] = v;
+  }
   __syncthreads();
 
-  // right-looking, one barrier per column: the trailing update of step j uses
-  // the unscaled column j and the pivot d_j; column j-1 is scaled during step j.
-  bool bad = false;
-  for (int j = 0; j < nb; ++j) {
-    const double d = L[j * LDS + j];
-    if (!(d > 0.0)) bad = true;
-    const double inv_d = 1.0 / d;
-    if (j > 0) {
-      const double sp = sqrt(L[(j - 1) * LDS + (j - 1)]);
-      // scale column j-1 below the diagonal (not read in this step)
-      for (int r = j + tid; r < nb; r += kDiagThreads) L[(j - 1) * LDS + r] /= sp;
-    }
-    for (int c = j + 1 + warp; c < nb; c += NW) {
-      const double f = L[j * LDS + c] * inv_d;
-      for (int r = c + lane; r < nb; r += 32) L[c * LDS + r] -= L[j * LDS + r] * f;
+  for (int kb = 0; kb < nsb; ++kb) {
+    const int b0 = kb * kSB;
+    double* D = Dinv + kb * kSB * 33;
+    if (warp == 0) {
+      // ---- factor the 32x32 diagonal block in registers: lane i owns row i.
+      // No division/sqrt library calls in here (their slow-path CALL would push
+      // the unrolled register rows to the stack): pivots use rsqrt_newton.
+      double row[kSB];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) row[c] = (c <= lane) ? A[(b0 + c) * kLDA + b0 + lane] : 0.0;
+      bool bad = false;
+      double my_inv = 0.0;
+      CholStep<0>::run(row, lane, bad, my_inv);  // fully unrolled: registers stay registers
+#pragma unroll
+      for (int c = 0; c < kSB; ++c)
+        if (c <= lane) A[(b0 + c) * kLDA + b0 + lane] = row[c];
+      if (bad && lane == 0) bad_s = 1;
+      S[lane] = my_inv;  // 1 / L_ii
+      __syncwarp();
+      // ---- D^{-1}: lane j computes column j by forward substitution (registers)
+      double x[kSB];
+#pragma unroll
+      for (int i = 0; i < kSB; ++i) {
+        double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k)
+          if (k >= lane) s -= A[(b0 + k) * kLDA + b0 + i] * x[k];
+        x[i] = (i >= lane) ? s * S[i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kSB; ++i) D[lane * 33 + i] = x[i];
     }
     __syncthreads();
-  }
-  // last column has no sub-diagonal; now take sqrt of every pivot
-  __syncthreads();
-  for (int j = tid; j < nb; j += kDiagThreads) L[j * LDS + j] = sqrt(L[j * LDS + j]);
-  __syncthreads();
-  if (bad && lane == 0) atomicExch(flag, 1);
-
-  // W_kk = L^T: W(r, c) = L(c, r) for r <= c
-  for (int c = warp; c < nb; c += NW)
-    for (int r = lane; r < nb; r += 32) W[r + (int64_t)c * ldw] = (r <= c) ? L[r * LDS + c] : 0.0;
-
-  // Linv by forward substitution, 8 lanes per column of Linv (column j solves
-  // L x = e_j); X holds the partial results.  Winv_kk = Linv^T.
-  constexpr int G = 8;
-  const int grp = tid / G, sub = tid % G;
-  constexpr int NGRP = kDiagThreads / G;
-  for (int j0 = 0; j0 < nb; j0 += NGRP) {
-    const int j = j0 + grp;
-    const bool live = j < nb;
-    double* x = X + grp * LDS;
-    // all groups of a warp walk the same i range so the warp stays converged
-    for (int i = j0; i < nb; ++i) {
-      const bool act = live && i >= j;
-      double s = 0.0;
-      if (act)
-        for (int k = j + sub; k < i; k += G) s += L[k * LDS + i] * x[k];
+    const int p0 = b0 + kSB, R = nbp - p0;
+    if (R > 0) {
+      // ---- panel: L(i, b0+c) = sum_{k<=c} Z(i, b0+k) * Dinv(c, k); 12 rows per thread
+      {
+        const int c = tid & 31, i0 = tid >> 5;
+        double acc[12];
 #pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-      if (act && sub == 0) x[i] = ((i == j ? 1.0 : 0.0) - s) / L[i * LDS + i];
-      __syncwarp();
+        for (int q = 0; q < 12; ++q) acc[q] = 0.0;
+        for (int k = 0; k <= c; ++k) {
+          const double dk = D[k * 33 + c];
+          const double* col = A + (b0 + k) * kLDA + p0 + i0;
+#pragma unroll
+          for (int q = 0; q < 12; ++q)
+            if (i0 + 8 * q < R) acc[q] += col[8 * q] * dk;
+        }
+#pragma unroll
+        for (int q = 0; q < 12; ++q)
+          if (i0 + 8 * q < R) T[c * kLDA + i0 + 8 * q] = acc[q];
+      }
+      __syncthreads();
+      for (int idx = tid; idx < R * kSB; idx += kDiagThreads) {
+        const int i = idx % R, c = idx / R;
+        A[(b0 + c) * kLDA + p0 + i] = T[c * kLDA + i];
+      }
+      __syncthreads();
+      // ---- trailing rank-32 update of the lower triangle, 4x4 register tiles
+      const int tr = R / 4;
+      const int ntiles = tr * (tr + 1) / 2;
+      for (int t = tid; t < ntiles; t += kDiagThreads) {
+        int tj = 0, rem = t;
+        while (rem >= tr - tj) {
+          rem -= tr - tj;
+          ++tj;
+        }
+        const int ti = tj + rem;
+        const int i0 = p0 + 4 * ti, j0 = p0 + 4 * tj;
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int c = 0; c < kSB; ++c) {
+          const double* col = A + (b0 + c) * kLDA;
+          double li[4], lj[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            li[a] = col[i0 + a];
+            lj[a] = col[j0 + a];
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] += li[a] * lj[b];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (i0 + a >= j0 + b) A[(j0 + b) * kLDA + i0 + a] -= acc[a][b];
+      }
+      __syncthreads();
     }
-    // Winv(j, i) = Linv(i, j) for i >= j  -> row j of Winv
-    if (live)
-      for (int i = sub; i < nb; i += G) Winv[j + (int64_t)i * ldwi] = (i >= j) ? x[i] : 0.0;
+  }
+  if (tid == 0 && bad_s) atomicExch(flag, 1);
+
+  // ---- W = L^T (upper) with explicit zeros below
+  for (int idx = tid; idx < nb * nb; idx += kDiagThreads) {
+    const int r = idx % nb, c = idx / nb;
+    W[r + (int64_t)c * ldw] = (r <= c) ? A[r * kLDA + c] : 0.0;
+  }
+
+  // ---- L^{-1} by 32-column blocks; Winv = L^{-T}
+  for (int jb = 0; jb < nsb; ++jb) {
+    const int c0 = jb * kSB;
+    for (int idx = tid; idx < kSB * nbp; idx += kDiagThreads) {
+      const int r = idx % nbp, c = idx / nbp;
+      double v = 0.0;
+      if (r >= c0 && r < c0 + kSB) v = Dinv[jb * kSB * 33 + c * 33 + (r - c0)];
+      T[c * kLDA + r] = v;
+    }
+    __syncthreads();
+    for (int ib = jb + 1; ib < nsb; ++ib) {
+      const int r0 = ib * kSB;
+      // S = sum_{k in [c0, r0)} L(r0 + r, k) * Linv(k, c0 + c)
+      {
+        const int r = tid & 31, cb = tid >> 5;  // columns cb + 8q
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k = c0; k < r0; ++k) {
+          const double a = A[k * kLDA + r0 + r];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += a * T[(cb + 8 * q) * kLDA + k];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S[(cb + 8 * q) * 33 + r] = acc[q];
+      }
+      __syncthreads();
+      const double* Di = Dinv + ib * kSB * 33;
+      {
+        const int r = tid & 31, cb = tid >> 5;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = 0; t <= r; ++t) {
+          const double d = Di[t * 33 + r];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += d * S[(cb + 8 * q) * 33 + t];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) T[(cb + 8 * q) * kLDA + r0 + r] = -acc[q];
+      }
+      __syncthreads();
+    }
+    // Winv(c0 + c, row) = Linv(row, c0 + c)
+    for (int idx = tid; idx < kSB * nb; idx += kDiagThreads) {
+      const int c = idx & 31, row = idx >> 5;
+      if (c0 + c < nb) Winv[(c0 + c) + (int64_t)row * ldwi] = (row >= c0 + c) ? T[c * kLDA + row] : 0.0;
+    }
     __syncthreads();
   }
 }
 
-template <int NB>
 void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk) {
-  const size_t smem = (size_t)(NB + kDiagThreads / 8) * (NB + 1) * 8;
+  const size_t smem = (size_t)(128 * kLDA + 4 * kSB * 33 + kSB * kLDA + kSB * 33) * 8;
   static bool set = false;
   if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel<NB>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    QDWHG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
     set = true;
   }
-  potrf_diag_kernel<NB><<<1, kDiagThreads, smem, ctx.stream>>>(
-      Zkk.ptr(), Zkk.ld, Wkk.ptr(), Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag);
+  potrf_diag_kernel<<<1, kDiagThreads, smem, ctx.stream>>>(Zkk.ptr(), Zkk.ld, Wkk.ptr(), Wkk.ld,
+                                                           Wikk.ptr(), Wikk.ld, (int)Zkk.rows,
+                                                           ctx.dflag);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count();
 }
@@ -135,7 +285,7 @@ void trtri_rec(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv) {
   const int64_t n = Z.rows;
   if (Z.cols != n) throw InvalidArgument("cholesky: matrix not square");
-  const int nb = n >= 1024 ? 128 : 64;
+  const int nb = 128;
   QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);
@@ -144,10 +294,7 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv) {
   for (int64_t k = 0; k < n; k += nb) {
     const int64_t b = std::min<int64_t>(nb, n - k);
     const int64_t rest = n - k - b;
-    if (nb == 128)
-      launch_diag<128>(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
-    else
-      launch_diag<64>(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
+    launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
     if (rest > 0) {
       // W_k,rest = W_kk^{-T} Z_k,rest   (op(A) = Winv_kk^T is lower -> ALower)
       GemmExtra e1;

@@ -165,5 +165,7 @@ def test_device_pointer_path_matches_host(cuda):
     ad = torch.from_numpy(np.asfortranarray(g["a"])).to(cuda)
     r_dev = qdwh.qdwh_partial_eig(ad, qdwh.choose_shift(3))
     assert torch.is_tensor(r_dev.v) and r_dev.v.is_cuda
-    np.testing.assert_array_equal(r_dev.lambda_minus, r_host.lambda_minus)
-    np.testing.assert_array_equal(r_dev.v.cpu().numpy(), r_host.v)
+    # the panel QR reduces with FP64 atomics: run-to-run differences are at rounding level
+    np.testing.assert_allclose(r_dev.lambda_minus, r_host.lambda_minus, rtol=1e-13)
+    vd, vh = r_dev.v.cpu().numpy(), r_host.v
+    assert np.linalg.norm(vd @ (vd.T @ vh) - vh) < 1e-12
