@@ -56,9 +56,9 @@ QDWHG_DEV void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
 // Partial sums for pivot column `col` over this CTA's rows:
 //   top[c]  = A(col, c)                       (row owner only)
 //   dbel[c] = sum_{r > col} A(r, col) A(r, c) (dbel[col] = sigma^2 below the pivot)
-// for c >= col, accumulated into buf = [top(BW) | dbel(BW)].
+// for c >= col, written to this CTA's out = [top(BW) | dbel(BW)] (zeros elsewhere).
 QDWHG_DEV void panel_partials(const double* S, int RP, int nr, int rbeg, int b, int col, double* red,
-                              double* buf) {
+                              double* out) {
   const int c = threadIdx.x % kBW, rg = threadIdx.x / kBW;
   double d = 0.0;
   if (c < b && c >= col) {
@@ -69,46 +69,91 @@ QDWHG_DEV void panel_partials(const double* S, int RP, int nr, int rbeg, int b, 
   }
   red[rg * kBW + c] = d;
   __syncthreads();
-  if (rg == 0 && c < b && c >= col) {
-    double s = 0.0;
+  if (rg == 0) {
+    double s = 0.0, top = 0.0;
+    if (c < b && c >= col) {
 #pragma unroll
-    for (int q = 0; q < kPanelThreads / kBW; ++q) s += red[q * kBW + c];
-    if (s != 0.0) atomicAdd(&buf[kBW + c], s);
-    const int rl = col - rbeg;
-    if (rl >= 0 && rl < nr) atomicAdd(&buf[c], S[c * RP + rl]);
+      for (int q = 0; q < kPanelThreads / kBW; ++q) s += red[q * kBW + c];
+      const int rl = col - rbeg;
+      if (rl >= 0 && rl < nr) top = S[c * RP + rl];
+    }
+    out[c] = top;
+    out[kBW + c] = s;
   }
   __syncthreads();
 }
 
+// Unblocked Householder QR of an mp x b panel (b <= 64) whose rows are spread
+// over the CTAs of the launch, each CTA keeping its rows in shared memory.
+// Per column ONE cross-CTA reduction of [x0, sigma^2, a_jj,c, x^T a_c] gives the
+// pivot, tau and all v^T a_c at once.
+//   CLUSTER = true : one thread-block cluster (<= 16 CTAs): partial vectors are
+//                    read from the peers' shared memory (DSMEM) in fixed order
+//                    (deterministic) behind one hardware cluster barrier;
+//   CLUSTER = false: any number of co-resident CTAs (cooperative launch): FP64
+//                    atomics into a rotating global buffer + a grid barrier.
+template <bool CLUSTER>
 __global__ void __launch_bounds__(kPanelThreads, 1)
     geqr2_panel_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
                        int b, int rpc, double* acc, unsigned* bar) {
   extern __shared__ double smem[];
   const int RP = rpc | 1;
-  double* S = smem;               // [b][RP] column-major panel rows of this CTA
-  double* red = S + kBW * RP;     // [4][kBW]
+  double* S = smem;                                  // [b][RP] panel rows of this CTA
+  double* red = S + kBW * RP;                        // [4][kBW]
   double* coef = red + (kPanelThreads / kBW) * kBW;  // [kBW] w_c
+  double* part = coef + kBW;                         // [2][2*kBW] this CTA's partials (by parity)
+  double* tot = part + 4 * kBW;                      // [2*kBW] reduced vector
   const int rbeg = blockIdx.x * rpc;
   const int nr = max(0, min(rpc, mp - rbeg));
   const int c = threadIdx.x % kBW, rg = threadIdx.x / kBW;
   constexpr int NRG = kPanelThreads / kBW;
   unsigned epoch = 0;
+  namespace cg = cooperative_groups;
 
   for (int cc = 0; cc < b; ++cc)
     for (int r = threadIdx.x; r < nr; r += kPanelThreads) S[cc * RP + r] = A[(rbeg + r) + cc * lda];
   __syncthreads();
 
-  panel_partials(S, RP, nr, rbeg, b, 0, red, acc);
-  grid_barrier(bar, gridDim.x, epoch);
-
-  for (int jj = 0; jj < b; ++jj) {
-    const double* buf = acc + (jj % 3) * (2 * kBW);
-    if (blockIdx.x == 0) {
-      double* z = acc + ((jj + 2) % 3) * (2 * kBW);
-      for (int i = threadIdx.x; i < 2 * kBW; i += kPanelThreads) z[i] = 0.0;
+  // publish this CTA's partials for column `col` and make the reduced vector
+  // visible in `tot`
+  auto reduce = [&](int col) {
+    double* mine = part + (col & 1) * (2 * kBW);
+    panel_partials(S, RP, nr, rbeg, b, col, red, mine);
+    if (CLUSTER) {
+      cg::cluster_group cluster = cg::this_cluster();
+      cluster.sync();
+      if (threadIdx.x < 2 * kBW) {
+        const int nb_ = (int)cluster.num_blocks();
+        double v[16];
+#pragma unroll
+        for (int p = 0; p < 16; ++p)  // all remote loads in flight before the sum
+          v[p] = (p < nb_) ? cluster.map_shared_rank(mine, p)[threadIdx.x] : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) s += v[p];
+        tot[threadIdx.x] = s;
+      }
+      __syncthreads();
+    } else {
+      double* buf = acc + (col % 3) * (2 * kBW);
+      if (threadIdx.x < 2 * kBW) {
+        const int cc = threadIdx.x % kBW;
+        if (cc < b && cc >= col && mine[threadIdx.x] != 0.0) atomicAdd(&buf[threadIdx.x], mine[threadIdx.x]);
+      }
+      grid_barrier(bar, gridDim.x, epoch);
+      if (threadIdx.x < 2 * kBW) tot[threadIdx.x] = __ldcg(&buf[threadIdx.x]);
+      if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
+        double* z = acc + ((col + 2) % 3) * (2 * kBW);
+        if (threadIdx.x < 2 * kBW) z[threadIdx.x] = 0.0;
+      }
+      __syncthreads();
     }
-    const double x0 = __ldcg(&buf[jj]);
-    const double sig2 = __ldcg(&buf[kBW + jj]);
+  };
+
+  reduce(0);
+  for (int jj = 0; jj < b; ++jj) {
+    const double x0 = tot[jj];
+    const double sig2 = tot[kBW + jj];
     const double normx = sqrt(x0 * x0 + sig2);
     const bool reflect = (jj < mp - 1) && normx > 0.0;
     double beta = x0, v0 = 1.0, taup = 0.0;
@@ -121,7 +166,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     if (threadIdx.x < kBW) {
       const int cc = threadIdx.x;
       double w = 0.0;
-      if (reflect && cc > jj && cc < b) w = taup * (__ldcg(&buf[cc]) + __ldcg(&buf[kBW + cc]) / v0);
+      if (reflect && cc > jj && cc < b) w = taup * (tot[cc] + tot[kBW + cc] / v0);
       coef[cc] = w;
     }
     __syncthreads();
@@ -156,13 +201,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       if (rl >= 0 && rl < nr) S[jj * RP + rl] = beta;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) tau_out[jj] = taup;
-    if (jj + 1 < b) {
-      panel_partials(S, RP, nr, rbeg, b, jj + 1, red, acc + ((jj + 1) % 3) * (2 * kBW));
-      grid_barrier(bar, gridDim.x, epoch);
-    }
+    if (jj + 1 < b) reduce(jj + 1);
   }
+  if (CLUSTER) cg::this_cluster().sync();  // peers may still read our partials
   __syncthreads();
-  // write back R (upper part) with explicit zeros below the diagonal; V above diag = 0
+  // write back R (upper part) with explicit zeros below the diagonal
   for (int cc = 0; cc < b; ++cc)
     for (int r = threadIdx.x; r < nr; r += kPanelThreads) {
       const int rgl = rbeg + r;
@@ -221,28 +264,87 @@ __global__ void diag_kernel(const double* R, int64_t ld, int64_t n, double* out)
     out[i] = R[i + i * ld];
 }
 
+size_t panel_smem(int rpc) {
+  return ((size_t)kBW * (rpc | 1) + (kPanelThreads / kBW) * kBW + kBW + 4 * kBW + 2 * kBW) * 8;
+}
+
+constexpr size_t kPanelSmemMax = 220 * 1024;
+
+// Largest cluster the device allows for the panel (16 non-portable, else 8).
+int cluster_size_limit() {
+  static int cs = -1;
+  if (cs < 0) {
+    cs = 8;
+    if (cudaFuncSetAttribute(geqr2_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(kPanelThreads);
+      cfg.dynamicSmemBytes = kPanelSmemMax;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 16;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, geqr2_panel_kernel<true>, &cfg) == cudaSuccess && n > 0)
+        cs = 16;
+    }
+    cudaGetLastError();
+  }
+  return cs;
+}
+
 void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
                   unsigned* bar) {
-  const int mp = (int)P.rows, b = (int)P.cols;
-  int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
-  int rpc = (mp + nblk - 1) / nblk;
-  const size_t smem = ((size_t)kBW * (rpc | 1) + (kPanelThreads / kBW) * kBW + kBW) * 8;
-  if (smem > 220 * 1024) throw InvalidArgument("geqrf: panel too tall for shared memory");
+  int mp = (int)P.rows, b = (int)P.cols;
   static bool set = false;
   if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel<false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax));
+    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax));
     set = true;
   }
-  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
-  QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
   double* Ap = P.ptr();
   int64_t lda = P.ld;
   double* Vptr = Vp.ptr();
   int64_t ldv = Vp.ld;
-  void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, (void*)&mp, (void*)&b, &rpc, &acc, &bar};
-  QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)geqr2_panel_kernel, dim3(nblk),
-                                         dim3(kPanelThreads), args, smem, ctx.stream));
+  const int csmax = cluster_size_limit();
+  // cluster path when <= 64 rows per CTA fit in one cluster (deterministic,
+  // cheapest barrier); taller panels spread over more SMs with the grid path,
+  // whose per-column work shrinks with the CTA count (measured faster at n=4096).
+  int cs = std::max(1, (mp + 63) / 64);
+  int rpc = (mp + cs - 1) / cs;
+  if (cs <= csmax) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kPanelThreads);
+    cfg.dynamicSmemBytes = panel_smem(rpc);
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = cs;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    QDWHG_CUDA(cudaLaunchKernelEx(&cfg, geqr2_panel_kernel<true>, Ap, lda, Vptr, ldv, tau_dev, mp, b,
+                                  rpc, acc, bar));
+    ctx.count();
+    return;
+  }
+  // grid path (tall panels): cooperative launch over up to all SMs
+  const int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
+  rpc = (mp + nblk - 1) / nblk;
+  if (panel_smem(rpc) > kPanelSmemMax) throw InvalidArgument("geqrf: panel too tall for shared memory");
+  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+  void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, &mp, &b, &rpc, &acc, &bar};
+  QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)geqr2_panel_kernel<false>, dim3(nblk),
+                                         dim3(kPanelThreads), args, panel_smem(rpc), ctx.stream));
   ctx.count();
 }
 
