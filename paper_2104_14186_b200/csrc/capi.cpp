@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -68,7 +70,9 @@ DMat Arena::alloc(int64_t rows, int64_t cols) {
   return m;
 }
 
-void Ctx::prof_begin(double flops) {
+void Ctx::prof_begin(double flops, const std::string& tag) {
+  ev_tag.resize(ev_used + 1);
+  ev_tag[ev_used] = tag;
   if (ev_pool.size() < 2 * (ev_used + 1)) {
     for (int i = 0; i < 512; ++i) {
       cudaEvent_t e;
@@ -88,12 +92,18 @@ void Ctx::prof_end() {
 void Ctx::prof_collect() {
   if (ev_used == 0) return;
   QDWHG_CUDA(cudaEventSynchronize(ev_pool[2 * ev_used - 1]));
+  static const char* log_path = getenv("QDWHG_PROFILE_LOG");
+  FILE* log = log_path ? fopen(log_path, "a") : nullptr;
   for (size_t i = 0; i < ev_used; ++i) {
     float ms = 0.f;
     QDWHG_CUDA(cudaEventElapsedTime(&ms, ev_pool[2 * i], ev_pool[2 * i + 1]));
     gemm_ms += ms;
     gemm_flops += ev_flops[i];
+    if (log)
+      fprintf(log, "%s ms=%.4f gflop=%.4f tf=%.2f\n", ev_tag[i].c_str(), ms, ev_flops[i] * 1e-9,
+              ms > 0 ? ev_flops[i] / ms * 1e-9 : 0.0);
   }
+  if (log) fclose(log);
   gemm_timed += ev_used;
   ev_used = 0;
 }
@@ -624,7 +634,7 @@ qdwhg_status qdwhg_cholesky(qdwhg_handle* h, int64_t n, const double* Z, int64_t
     DMat Zd = stage_in(ctx, Z, n, n, ldz, nullptr);
     if (mat_stats(ctx, Zd, false).nonfinite > 0) throw InvalidArgument("cholesky: non-finite entry");
     DMat Wi = ctx.arena->alloc(n, n);
-    potrf_upper_and_inverse(ctx, Zd, Wi);
+    potrf_upper_and_inverse(ctx, Zd, Wi, true);
     stage_out(ctx, Zd, W, ldw);
     QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
   });

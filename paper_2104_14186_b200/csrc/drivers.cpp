@@ -90,7 +90,7 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   DMat Z = ctx.arena->alloc(n, n);
   DMat Winv = ctx.arena->alloc(n, n);
   GemmExtra syrk;
-  syrk.out = OutMode::LowerMirror;  // symmetric by construction (one dot product per pair)
+  syrk.out = OutMode::Lower;  // POTRF reads the lower triangle only
   syrk.diag_add = 1.0;
   gemm(ctx, Op::T, Op::N, w.c, X, X, 0.0, Z, syrk);
   try {

@@ -43,6 +43,10 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int splits;       // split-K factor (1 = fused epilogue)
   double* partial;  // splits x (M x N) raw partials (ld = M) when splits > 1
+  // batch item b (blockIdx.y): TMA coordinates += b * (x_bs0, x_bs1), D/Cin += b * stride
+  int a_bs0, a_bs1, b_bs0, b_bs1;
+  int64_t d_bs, cin_bs;
+  int nbatch;
 };
 
 template <bool KMAJ>
@@ -82,7 +86,7 @@ QDWHG_DEV int frag_at(const FragBase& b, int x) {
 
 // blockIdx -> (tm, tn); heaviest tiles first for triangular K ranges.
 QDWHG_DEV void tile_coords(const GemmParams& p, int bid, int& tm, int& tn) {
-  if (p.omode == (int)OutMode::LowerMirror) {
+  if (p.omode != (int)OutMode::Full) {
     // enumerate lower tiles column by column: column tn holds tiles tm = tn..tiles_m-1
     int c = 0, rem = bid;
     while (rem >= p.tiles_m - c) {
@@ -150,6 +154,12 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     kt0 = min(s0, kt1);
   }
   const int nkt = max(kt1 - kt0, 0);
+  // batched launches (blockIdx.y): per-item coordinate / pointer offsets
+  const int bi = blockIdx.y;
+  const int ac0 = p.a_c0 + bi * p.a_bs0, ac1 = p.a_c1 + bi * p.a_bs1;
+  const int bc0 = p.b_c0 + bi * p.b_bs0, bc1 = p.b_c1 + bi * p.b_bs1;
+  double* const Dp = p.D + (int64_t)bi * p.d_bs;
+  const double* const Cinp = p.Cin + (int64_t)bi * p.cin_bs;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -170,18 +180,18 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     double* a_dst = sA + s * A_ELEMS;
     double* b_dst = sB + s * B_ELEMS;
     if (A_KMAJ) {
-      tma_load_2d(a_dst, &tmA, &full[s], p.a_c0 + k0, p.a_c1 + m0);
+      tma_load_2d(a_dst, &tmA, &full[s], ac0 + k0, ac1 + m0);
     } else {
 #pragma unroll
       for (int b = 0; b < BM / 16; ++b)
-        tma_load_2d(a_dst + b * 256, &tmA, &full[s], p.a_c0 + m0 + 16 * b, p.a_c1 + k0);
+        tma_load_2d(a_dst + b * 256, &tmA, &full[s], ac0 + m0 + 16 * b, ac1 + k0);
     }
     if (B_KMAJ) {
-      tma_load_2d(b_dst, &tmB, &full[s], p.b_c0 + k0, p.b_c1 + n0);
+      tma_load_2d(b_dst, &tmB, &full[s], bc0 + k0, bc1 + n0);
     } else {
 #pragma unroll
       for (int b = 0; b < BN / 16; ++b)
-        tma_load_2d(b_dst + b * 256, &tmB, &full[s], p.b_c0 + n0 + 16 * b, p.b_c1 + k0);
+        tma_load_2d(b_dst + b * 256, &tmB, &full[s], bc0 + n0 + 16 * b, bc1 + k0);
     }
   };
   const bool producer = (threadIdx.x == 0);
@@ -233,45 +243,76 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
   }
 
-  // ---------------- epilogue
-  if (p.splits > 1) {
-    double* P = p.partial + (size_t)blockIdx.z * p.M * p.N;
-#pragma unroll
-    for (int x = 0; x < TM; ++x)
-#pragma unroll
-      for (int y = 0; y < TN; ++y)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = m0 + wm * WTM + 8 * x + g;
-          const int j = n0 + wn * WTN + 8 * y + 2 * t + e;
-          if (i < p.M && j < p.N) P[i + (size_t)j * p.M] = acc[x][y][e];
-        }
-    return;
-  }
-  const bool lower = p.omode == (int)OutMode::LowerMirror;
+  // ---------------- epilogue: accumulators -> smem tile -> coalesced column writes
+  __syncthreads();  // every warp is past the mainloop: the stage buffers are free
+  constexpr int LDC = BM + 2;  // conflict-free 8-byte writes per half-warp
+  double* Cs = sA;
 #pragma unroll
   for (int x = 0; x < TM; ++x)
 #pragma unroll
     for (int y = 0; y < TN; ++y)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = m0 + wm * WTM + 8 * x + g;
-        const int j = n0 + wn * WTN + 8 * y + 2 * t + e;
-        if (i >= p.M || j >= p.N) continue;
-        if (lower && i < j) continue;
-        double v = p.alpha * acc[x][y][e];
-        if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
-        if (i == j) v += p.diag_add;
-        p.D[i + (size_t)j * p.ldd] = v;
-        if (lower && i != j) p.D[j + (size_t)i * p.ldd] = v;
+      for (int e = 0; e < 2; ++e)
+        Cs[(wn * WTN + 8 * y + 2 * t + e) * LDC + wm * WTM + 8 * x + g] = acc[x][y][e];
+  __syncthreads();
+  constexpr int NW = WM * WN;
+  const bool split = p.splits > 1;
+  double* D = split ? p.partial + (size_t)blockIdx.z * p.M * p.N : Dp;
+  const int64_t ldd = split ? p.M : p.ldd;
+  const bool lower = !split && p.omode != (int)OutMode::Full;
+  const bool mirror = !split && p.omode == (int)OutMode::LowerMirror;
+  const bool vec = ((reinterpret_cast<uintptr_t>(D) & 15) == 0) && ((ldd & 1) == 0) &&
+                   (split || p.beta == 0.0 ||
+                    (((reinterpret_cast<uintptr_t>(Cinp) & 15) == 0) && ((p.ldcin & 1) == 0)));
+  for (int cl = warp; cl < BN; cl += NW) {
+    const int j = n0 + cl;
+    if (j >= p.N) break;
+    const double* col = Cs + cl * LDC;
+#pragma unroll
+    for (int rl0 = 0; rl0 < BM; rl0 += 64) {
+      const int rl = rl0 + 2 * lane;
+      const int i = m0 + rl;
+      if (i >= p.M) continue;
+      double v0 = col[rl], v1 = col[rl + 1];
+      if (!split) {
+        v0 *= p.alpha;
+        v1 *= p.alpha;
+        if (p.beta != 0.0) {
+          const double* cin = Cinp + i + (size_t)j * p.ldcin;
+          if (vec && i + 1 < p.M) {
+            const double2 c2 = *reinterpret_cast<const double2*>(cin);
+            v0 += p.beta * c2.x;
+            v1 += p.beta * c2.y;
+          } else {
+            v0 += p.beta * cin[0];
+            if (i + 1 < p.M) v1 += p.beta * cin[1];
+          }
+        }
+        if (i == j) v0 += p.diag_add;
+        if (i + 1 == j) v1 += p.diag_add;
       }
+      double* dst = D + i + (size_t)j * ldd;
+      const bool w0 = !lower || i >= j, w1 = (i + 1 < p.M) && (!lower || i + 1 >= j);
+      if (vec && w0 && w1) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        if (w0) dst[0] = v0;
+        if (w1) dst[1] = v1;
+      }
+      if (mirror) {
+        if (w0 && i > j) D[j + (size_t)i * ldd] = v0;
+        if (w1 && i + 1 > j) D[j + (size_t)(i + 1) * ldd] = v1;
+      }
+    }
+  }
 }
 
 // Split-K reduction + epilogue: D = alpha * sum_z P_z + beta * Cin (+diag), with
 // the same LowerMirror semantics.
 __global__ void splitk_reduce_kernel(const GemmParams p) {
   const int64_t total = (int64_t)p.M * p.N;
-  const bool lower = p.omode == (int)OutMode::LowerMirror;
+  const bool lower = p.omode != (int)OutMode::Full;
+  const bool mirror = p.omode == (int)OutMode::LowerMirror;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(idx % p.M), j = (int)(idx / p.M);
@@ -282,7 +323,7 @@ __global__ void splitk_reduce_kernel(const GemmParams p) {
     if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
     if (i == j) v += p.diag_add;
     p.D[i + (size_t)j * p.ldd] = v;
-    if (lower && i != j) p.D[j + (size_t)i * p.ldd] = v;
+    if (mirror && i != j) p.D[j + (size_t)i * p.ldd] = v;
   }
 }
 
@@ -327,7 +368,7 @@ double algorithmic_flops(const GemmParams& p) {
     const double full = std::min(len, kmax);
     return full * (full + 1) / 2 + std::max(0.0, len - kmax) * kmax;
   };
-  if (p.omode == (int)OutMode::LowerMirror) return K * N * (N + 1);
+  if (p.omode != (int)OutMode::Full) return K * N * (N + 1);
   switch ((KRange)p.kmode) {
     case KRange::BUpper: return 2 * M * tri(M, N, K);
     case KRange::BLower: return 2 * M * tri(M, std::min(N, K), K);  // sum_j (K - j)
@@ -350,11 +391,11 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
   const CUtensorMap ta = AK ? make_desc(A, 16, BM) : make_desc(A, 16, 16);
   const CUtensorMap tb = BK_ ? make_desc(B, 16, BN) : make_desc(B, 16, 16);
   int ntiles;
-  if (p.omode == (int)OutMode::LowerMirror)
+  if (p.omode != (int)OutMode::Full)
     ntiles = p.tiles_n * (p.tiles_n + 1) / 2;
   else
     ntiles = p.tiles_m * p.tiles_n;
-  dim3 grid(ntiles, 1, p.splits);
+  dim3 grid(ntiles, p.nbatch, p.splits);
   static const bool debug = getenv("QDWHG_DEBUG") != nullptr;
   if (debug)
     fprintf(stderr,
@@ -363,7 +404,12 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
             BM, (int)AK, (int)BK_, p.M, p.N, p.K, p.kmode, p.omode, p.splits, p.tiles_m, p.tiles_n,
             (long)A.r0, (long)A.c0, (long)A.rows, (long)A.cols, (long)A.ld, (long)B.r0,
             (long)B.c0, (long)B.rows, (long)B.cols, (long)B.ld);
-  if (ctx.profile) ctx.prof_begin(algorithmic_flops(p));
+  if (ctx.profile) {
+    char tag[160];
+    snprintf(tag, sizeof(tag), "BM=%d AK=%d BK=%d M=%d N=%d K=%d kmode=%d omode=%d splits=%d grid=%d",
+             BM, (int)AK, (int)BK_, p.M, p.N, p.K, p.kmode, p.omode, p.splits, ntiles * p.splits);
+    ctx.prof_begin(algorithmic_flops(p), tag);
+  }
   kern<<<grid, threads, smem, ctx.stream>>>(ta, tb, p);
   QDWHG_CUDA(cudaGetLastError());
   if (ctx.profile) ctx.prof_end();
@@ -390,7 +436,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   const int64_t bn = (tb == Op::N) ? B.cols : B.rows;
   if (am != M || bn != N || bk != K) throw InvalidArgument("gemm: shape mismatch");
   if (M == 0 || N == 0) return;
-  if (ex.out == OutMode::LowerMirror && M != N) throw InvalidArgument("gemm: LowerMirror needs square C");
+  if (ex.out != OutMode::Full && M != N) throw InvalidArgument("gemm: lower output needs square C");
   if ((A.ld % 2) || (B.ld % 2) || (reinterpret_cast<uintptr_t>(A.base) % 16) ||
       (reinterpret_cast<uintptr_t>(B.base) % 16))
     throw InvalidArgument("gemm: operands must be 16-byte aligned with even leading dimension");
@@ -434,30 +480,50 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   p.omode = (int)ex.out;
   const bool ak = (ta == Op::T);  // op(A) K-contiguous
   const bool bkm = (tb == Op::N); // op(B) K-contiguous
+  const int nb_ = std::max(1, ex.batch);
+  p.nbatch = nb_;
+  p.a_bs0 = (int)ex.a_step_r;
+  p.a_bs1 = (int)ex.a_step_c;
+  p.b_bs0 = (int)ex.b_step_r;
+  p.b_bs1 = (int)ex.b_step_c;
+  p.d_bs = ex.c_step_r + ex.c_step_c * C.ld;
+  p.cin_bs = ex.c_step_r + ex.c_step_c * cin.ld;
+  // descriptors must cover every batch item (items tile exactly: no zero-fill reliance)
+  DMat Ae = A, Be = B;
+  Ae.rows += (nb_ - 1) * ex.a_step_r;
+  Ae.cols += (nb_ - 1) * ex.a_step_c;
+  Be.rows += (nb_ - 1) * ex.b_step_r;
+  Be.cols += (nb_ - 1) * ex.b_step_c;
 
   // Tile choice: 128x128 when the grid fills the machine, else 64x64.
-  const bool big = ((M + 127) / 128) * ((N + 127) / 128) >= ctx.num_sms;
+  const bool big = ((M + 127) / 128) * ((N + 127) / 128) * nb_ >= ctx.num_sms;
   const int BMt = big ? 128 : 64;
   p.tiles_m = (int)((M + BMt - 1) / BMt);
   p.tiles_n = (int)((N + BMt - 1) / BMt);
-  int ntiles = (ex.out == OutMode::LowerMirror) ? p.tiles_n * (p.tiles_n + 1) / 2
+  int ntiles = (ex.out != OutMode::Full) ? p.tiles_n * (p.tiles_n + 1) / 2
                                                  : p.tiles_m * p.tiles_n;
   // split-K when the output grid leaves SMs idle and K is long
   int splits = ex.split_k;
   if (splits <= 0) {
     splits = 1;
     const int64_t ktiles = (K + BK - 1) / BK;
-    while (ntiles * splits * 2 <= 2 * ctx.num_sms && ktiles / (splits * 2) >= 16 && splits < 32)
+    while (ntiles * nb_ * splits * 2 <= 2 * ctx.num_sms && ktiles / (splits * 2) >= 16 &&
+           splits < 32)
       splits *= 2;
+  }
+  if (nb_ > 1) {
+    splits = 1;
+    if (M % BMt || N % BMt || K % BK)
+      throw InvalidArgument("gemm: batched items must tile exactly");
   }
   p.splits = splits;
   const Arena::Mark mark = ctx.arena->mark();
   if (splits > 1) p.partial = static_cast<double*>(ctx.arena->alloc_bytes((size_t)splits * M * N * 8));
 
   if (big)
-    dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, A, B, p);
+    dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, Ae, Be, p);
   else
-    dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, A, B, p);
+    dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, Ae, Be, p);
 
   if (splits > 1) {
     const int64_t total = M * N;

@@ -93,7 +93,8 @@ enum class Op { N, T };
 // Which part of the K range can contribute for an output tile (triangular
 // operands store explicit zeros; skipping them is the TRMM saving).
 enum class KRange { Full, BUpper, BLower, AUpper, ALower };
-enum class OutMode { Full, LowerMirror };
+// Lower: only the lower triangle of a square C is written; LowerMirror also mirrors it.
+enum class OutMode { Full, LowerMirror, Lower };
 
 struct Ctx {
   cudaStream_t stream = nullptr;
@@ -110,10 +111,11 @@ struct Ctx {
   bool profile = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<double> ev_flops;  // algorithmic flops of launch i (events 2i, 2i+1)
+  std::vector<std::string> ev_tag;  // per-launch shape tag (QDWHG_PROFILE_LOG)
   size_t ev_used = 0;
   double gemm_ms = 0.0, gemm_flops = 0.0;
   uint64_t gemm_timed = 0;
-  void prof_begin(double flops);
+  void prof_begin(double flops, const std::string& tag = std::string());
   void prof_end();
   void prof_collect();
 };
@@ -127,6 +129,10 @@ struct GemmExtra {
   const DMat* cin = nullptr;
   double diag_add = 0.0;
   int split_k = 0;  // 0 = automatic
+  // Batched launch: item b uses A/B/C shifted by b * (step_r rows, step_c cols)
+  // of their stored matrices (items must tile exactly; no split-K).
+  int batch = 1;
+  int64_t a_step_r = 0, a_step_c = 0, b_step_r = 0, b_step_c = 0, c_step_r = 0, c_step_c = 0;
 };
 void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, double beta,
           const DMat& C, const GemmExtra& ex = {});
@@ -151,9 +157,10 @@ void mirror_lower_to_upper(Ctx& ctx, const DMat& X);
 void zero_strict_lower(Ctx& ctx, const DMat& X);
 
 // ------------------------------------------------------------------ potrf.cu
-// In place: upper triangle of Z becomes W with Z = W^T W (strict lower zeroed).
-// Throws NotPositiveDefinite.  Winv (n x n) receives W^{-1} (upper, zeros below).
-void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv);
+// Z = W^T W with W upper; only the lower triangle of Z is read (it is used as
+// workspace).  Winv (n x n) receives W^{-1} (upper, explicit zeros below); with
+// want_w, Z is overwritten by W (upper, zeros below).  Throws NotPositiveDefinite.
+void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false);
 
 // ------------------------------------------------------------------ geqrf.cu
 struct QrWork {

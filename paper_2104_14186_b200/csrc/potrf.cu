@@ -280,9 +280,35 @@ void trtri_rec(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
   ctx.arena->release_to(mark);
 }
 
+// Same recursion, level by level for n = nb * 2^L: all merges of one level are
+// independent, so each level is two batched GEMM launches instead of 2 * pairs.
+void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb) {
+  for (int64_t h = nb; h < n; h *= 2) {
+    const int64_t pairs = n / (2 * h);
+    const Arena::Mark mark = ctx.arena->mark();
+    DMat T = ctx.arena->alloc(h, h * pairs);  // T_p = T(:, p*h : (p+1)*h)
+    GemmExtra e1;
+    e1.krange = KRange::BUpper;  // W22^-1 upper
+    e1.batch = (int)pairs;
+    e1.a_step_r = e1.a_step_c = 2 * h;
+    e1.b_step_r = e1.b_step_c = 2 * h;
+    e1.c_step_c = h;
+    gemm(ctx, Op::N, Op::N, 1.0, W.sub(0, h, h, h), Winv.sub(h, h, h, h), 0.0, T.sub(0, 0, h, h), e1);
+    GemmExtra e2;
+    e2.krange = KRange::AUpper;  // W11^-1 upper
+    e2.batch = (int)pairs;
+    e2.a_step_r = e2.a_step_c = 2 * h;
+    e2.b_step_c = h;
+    e2.c_step_r = e2.c_step_c = 2 * h;
+    gemm(ctx, Op::N, Op::N, -1.0, Winv.sub(0, 0, h, h), T.sub(0, 0, h, h), 0.0,
+         Winv.sub(0, h, h, h), e2);
+    ctx.arena->release_to(mark);
+  }
+}
+
 }  // namespace
 
-void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv) {
+void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w) {
   const int64_t n = Z.rows;
   if (Z.cols != n) throw InvalidArgument("cholesky: matrix not square");
   const int nb = 128;
@@ -296,14 +322,15 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv) {
     const int64_t rest = n - k - b;
     launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
     if (rest > 0) {
-      // W_k,rest = W_kk^{-T} Z_k,rest   (op(A) = Winv_kk^T is lower -> ALower)
+      // W_k,rest = W_kk^{-T} Z_k,rest = W_kk^{-T} (Z_rest,k)^T   (only the lower
+      // triangle of Z is ever read or updated; op(A) = Winv_kk^T is lower -> ALower)
       GemmExtra e1;
       e1.krange = KRange::ALower;
-      gemm(ctx, Op::T, Op::N, 1.0, Winv.sub(k, k, b, b), Z.sub(k, k + b, b, rest), 0.0,
+      gemm(ctx, Op::T, Op::T, 1.0, Winv.sub(k, k, b, b), Z.sub(k + b, k, rest, b), 0.0,
            W.sub(k, k + b, b, rest), e1);
-      // Z_rest -= W_k,rest^T W_k,rest   (symmetric, lower tiles mirrored)
+      // Z_rest -= W_k,rest^T W_k,rest   (lower triangle only)
       GemmExtra e2;
-      e2.out = OutMode::LowerMirror;
+      e2.out = OutMode::Lower;
       const DMat Wp = W.sub(k, k + b, b, rest);
       gemm(ctx, Op::T, Op::N, -1.0, Wp, Wp, 1.0, Z.sub(k + b, k + b, rest, rest), e2);
     }
@@ -316,9 +343,12 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv) {
     ctx.arena->release_to(mark);
     throw NotPositiveDefinite("cholesky: pivot is not positive");
   }
-  trtri_rec(ctx, W, Winv, 0, n, nb);
-  // hand W back in Z's upper triangle (zero strict lower) for callers that want it
-  copy(ctx, W, Z);
+  const int64_t nblk = n / nb;
+  if (n % nb == 0 && (nblk & (nblk - 1)) == 0)
+    trtri_levels(ctx, W, Winv, n, nb);
+  else
+    trtri_rec(ctx, W, Winv, 0, n, nb);
+  if (want_w) copy(ctx, W, Z);  // W (upper, zero strict lower) back in Z for qdwhg_cholesky
   ctx.arena->release_to(mark);
 }
 
