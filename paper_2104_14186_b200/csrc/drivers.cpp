@@ -305,9 +305,65 @@ void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) 
   syev_dc(ctx, S, vals, Vout, 0);
 }
 
+// Tall-skinny QR A = Q R by CholeskyQR2 (two Gram/POTRF/TRMM passes, all GEMM
+// work) when A is well enough conditioned (diag ratio of the first Cholesky
+// factor <= 1e5, i.e. u*kappa^2 << 1); returns false (caller falls back to
+// Householder) otherwise or on a Cholesky breakdown.
+static bool cholesky_qr2(Ctx& ctx, const DMat& A, const DMat& Q, const DMat& R) {
+  const int64_t n = A.cols;
+  DMat G = ctx.arena->alloc(n, n), Gi = ctx.arena->alloc(n, n);
+  DMat G2 = ctx.arena->alloc(n, n), G2i = ctx.arena->alloc(n, n);
+  GemmExtra syrk;
+  syrk.out = OutMode::Lower;
+  GemmExtra trmm;
+  trmm.krange = KRange::BUpper;
+  try {
+    gemm(ctx, Op::T, Op::N, 1.0, A, A, 0.0, G, syrk);
+    potrf_upper_and_inverse(ctx, G, Gi, true);  // G <- W1
+    std::vector<double> d;
+    diag_to_host(ctx, G, d);
+    double dmax = 0.0, dmin = 1e308;
+    for (double x : d) {
+      dmax = std::max(dmax, std::abs(x));
+      dmin = std::min(dmin, std::abs(x));
+    }
+    if (!(dmin > 0.0) || dmax / dmin > 1e5) return false;
+    DMat Q1 = ctx.arena->alloc(A.rows, n);
+    gemm(ctx, Op::N, Op::N, 1.0, A, Gi, 0.0, Q1, trmm);  // Q1 = A W1^-1
+    gemm(ctx, Op::T, Op::N, 1.0, Q1, Q1, 0.0, G2, syrk);
+    potrf_upper_and_inverse(ctx, G2, G2i, true);           // G2 <- W2
+    gemm(ctx, Op::N, Op::N, 1.0, Q1, G2i, 0.0, Q, trmm);  // Q = Q1 W2^-1
+  } catch (const NotPositiveDefinite&) {
+    return false;
+  }
+  GemmExtra up;
+  up.krange = KRange::AUpper;
+  gemm(ctx, Op::N, Op::N, 1.0, G2, G, 0.0, R, up);  // R = W2 W1
+  return true;
+}
+
 void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V) {
-  // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order
+  // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order.
+  // Tall A (m > n) is first reduced to its n x n triangular factor (A = Q R), so
+  // every QDWH iteration runs on n x n instead of m x n; U = Q U_R.
   const int64_t m = A.rows, n = A.cols;
+  if (m > n) {
+    const Arena::Mark mark = ctx.arena->mark();
+    DMat Q = ctx.arena->alloc(m, n), R = ctx.arena->alloc(n, n);
+    if (!cholesky_qr2(ctx, A, Q, R)) {
+      DMat Aw = ctx.arena->alloc(m, n);
+      copy(ctx, A, Aw);
+      QrWork qw;
+      geqrf(ctx, Aw, qw);
+      orgqr_cols(ctx, qw, m, n, 0, Q);
+      copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
+    }
+    DMat UR = ctx.arena->alloc(n, n);
+    svd_polar(ctx, R, UR, sigma, V);
+    gemm(ctx, Op::N, Op::N, 1.0, Q, UR, 0.0, U);
+    ctx.arena->release_to(mark);
+    return;
+  }
   const Arena::Mark mark = ctx.arena->mark();
   DMat Up = ctx.arena->alloc(m, n);
   DMat H = ctx.arena->alloc(n, n);
