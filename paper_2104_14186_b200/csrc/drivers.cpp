@@ -7,6 +7,7 @@
 #include <cmath>
 #include <numeric>
 #include <sstream>
+#include <cstdlib>
 
 namespace qdwhg {
 
@@ -301,7 +302,15 @@ static void syev_dc(Ctx& ctx, const DMat& A, std::vector<double>& vals, const DM
   ctx.arena->release_to(mark);
 }
 
+bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+
 void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
+  // Jacobi (n <= 160) / tridiagonal + bisection + inverse iteration; the QDWH
+  // spectral divide-and-conquer remains the fallback for tight clusters.
+  static const bool force_dc = getenv("QDWHG_SYEV_DC") != nullptr;
+  if (S.rows > kJacobiMaxN && !force_dc) {
+    if (syev_tridiag(ctx, S, vals, Vout)) return;
+  }
   syev_dc(ctx, S, vals, Vout, 0);
 }
 

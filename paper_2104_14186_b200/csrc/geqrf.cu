@@ -350,6 +350,20 @@ void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
 
 }  // namespace
 
+// T (b x b, b <= 64) of a compact-WY block from its Gram G = V^T V and taus.
+void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T) {
+  static bool larft_attr = false;
+  if (!larft_attr) {
+    QDWHG_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * kBW * (kBW + 1) * 8));
+    larft_attr = true;
+  }
+  larft_kernel<<<1, 256, 2 * kBW * (kBW + 1) * 8, ctx.stream>>>(G.ptr(), G.ld, tau_dev, T.ptr(),
+                                                               T.ld, (int)G.rows);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+}
+
 void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   const int64_t m = A.rows, n = A.cols;
   if (m < n) throw InvalidArgument("geqrf: requires rows >= cols");
@@ -375,15 +389,7 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     const DMat Gp = G.sub(0, 0, b, b);
     gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
     const DMat Tp = w.T.sub(0, p * nb, b, b);
-    static bool larft_attr = false;
-    if (!larft_attr) {
-      QDWHG_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      2 * kBW * (kBW + 1) * 8));
-      larft_attr = true;
-    }
-    larft_kernel<<<1, 256, 2 * kBW * (kBW + 1) * 8, ctx.stream>>>(Gp.ptr(), Gp.ld, tau_dev + j0, Tp.ptr(), Tp.ld, (int)b);
-    QDWHG_CUDA(cudaGetLastError());
-    ctx.count();
+    larft_launch(ctx, Gp, tau_dev + j0, Tp);
     // trailing update C = (I - V T V^T)^T C = C - V T^T (V^T C)
     const int64_t nc = n - j0 - b;
     if (nc > 0) {

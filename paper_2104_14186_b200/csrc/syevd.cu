@@ -1,0 +1,451 @@
+// Symmetric eigensolver for the large Rayleigh-Ritz blocks (ell in the
+// thousands: partial.cpp:80-81 sym_eig_dense of Q2^T A Q2, and eig(H) of the
+// polar-based SVD, fullsolve.cpp:82-103).  The reference uses cyclic Jacobi
+// (kernels.cpp:148-215), which is hours at ell ~ 5000; the values/vectors are
+// the same mathematical objects, computed here by
+//   1. SYTRD  A = Q T Q^T, Householder, blocked (LAPACK dsytrd/dlatrd shape):
+//      a cooperative panel kernel does the per-column work (column update with
+//      the panel's V/W, reflector, SYMV of the stale trailing matrix + panel
+//      corrections, w) with 4 grid barriers per column; the trailing update
+//      A -= V W^T + W V^T is two DMMA GEMMs;
+//   2. bisection (Sturm counts), one thread per eigenvalue -> ascending values
+//      to ~u*||T||;
+//   3. inverse iteration with partial pivoting (LAPACK dlagtf/dlagts shape),
+//      one thread per eigenvector, vectors stored transposed for coalescing;
+//   4. Lowdin orthogonalisation Z <- Z (I - E/2 + 3E^2/8), E = Z^T Z - I, for
+//      the O(u*||T||/gap) inner-product defects of inverse iteration
+//      (falls back to the QDWH divide-and-conquer if E is not small);
+//   5. back-transform Z_A = Q Z with the compact-WY blocks (Gram + larft + GEMMs).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.hpp"
+
+namespace qdwhg {
+
+void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T);  // geqrf.cu
+
+namespace {
+
+constexpr int kTrdThreads = 256;
+constexpr int kTrdNB = 32;
+
+QDWHG_DEV unsigned ld_acquire_u(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+QDWHG_DEV void red_release_add_u(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+QDWHG_DEV void gbar(unsigned* bar, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0) {
+    red_release_add_u(bar, 1u);
+    const unsigned target = epoch * gridDim.x;
+    while (ld_acquire_u(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
+// Block-wide sum into one atomic on `dst` (skip zeros).
+QDWHG_DEV void block_atomic_sum(double v, double* dst, double* scratch) {
+  v = block_sum(v, scratch);
+  if (threadIdx.x == 0 && v != 0.0) atomicAdd(dst, v);
+  __syncthreads();
+}
+
+struct TrdArgs {
+  double* A;  // n x n full symmetric (lower triangle used), ld
+  int64_t lda;
+  double* V;  // n x nb panel reflectors (unit at row c+1, zeros above)
+  double* W;  // n x nb
+  int64_t ldp;
+  double* d;    // diag (n)
+  double* e;    // sub-diagonal (n-1)
+  double* tau;  // n
+  double* y;    // n scratch (SYMV result, with 2*nb extra slots for t1/t2)
+  double* red;  // 4 x 8 rotating reduction slots
+  unsigned* bar;
+  int n, j0, nb;
+};
+
+// One panel of dlatrd (lower).  Columns c = j0 .. j0+nb-1.
+__global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) {
+  __shared__ double scratch[32];
+  __shared__ double vw[2 * kTrdNB];  // V(c, 0:i), W(c, 0:i)  /  t1, t2
+  const int n = a.n;
+  const int tid = threadIdx.x;
+  const int gtid = blockIdx.x * kTrdThreads + tid;
+  const int gsz = gridDim.x * kTrdThreads;
+  const int warps_total = gsz / 32;
+  const int gwarp = gtid / 32, lane = tid & 31;
+  unsigned epoch = 0;
+  for (int i = 0; i < a.nb; ++i) {
+    const int c = a.j0 + i;
+    double* red = a.red + (i % 4) * 8;
+    // zero the slot used two columns ahead (last read before the barrier below)
+    if (blockIdx.x == 0 && tid < 8) a.red[((i + 2) % 4) * 8 + tid] = 0.0;
+    // ---- A: a_c(r) -= sum_t V(r,t) W(c,t) + W(r,t) V(c,t), r >= c
+    if (tid < i) {
+      vw[tid] = a.V[c + (int64_t)tid * a.ldp];
+      vw[kTrdNB + tid] = a.W[c + (int64_t)tid * a.ldp];
+    }
+    __syncthreads();
+    double xs = 0.0, alpha_part = 0.0;
+    for (int r = c + gtid; r < n; r += gsz) {
+      double v = a.A[r + (int64_t)c * a.lda];
+      for (int t = 0; t < i; ++t)
+        v -= a.V[r + (int64_t)t * a.ldp] * vw[kTrdNB + t] + a.W[r + (int64_t)t * a.ldp] * vw[t];
+      a.A[r + (int64_t)c * a.lda] = v;
+      if (r >= c + 2) xs += v * v;
+      if (r == c + 1) alpha_part = v;
+      if (r == c) a.d[c] = v;
+    }
+    block_atomic_sum(xs, &red[0], scratch);
+    block_atomic_sum(alpha_part, &red[1], scratch);
+    gbar(a.bar, epoch);
+    // ---- B: reflector for a_c(c+1 : n)
+    const double alpha = __ldcg(&red[1]);
+    const double xnorm = sqrt(__ldcg(&red[0]));
+    double beta = alpha, taui = 0.0, scal = 0.0;
+    if (c + 1 < n && xnorm > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xnorm * xnorm), alpha);
+      taui = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int r = gtid; r < n; r += gsz) {
+      double v = 0.0;
+      if (r == c + 1) v = 1.0;
+      else if (r > c + 1) v = a.A[r + (int64_t)c * a.lda] * scal;
+      a.V[r + (int64_t)i * a.ldp] = v;
+    }
+    if (gtid == 0) {
+      if (c + 1 < n) a.e[c] = beta;
+      a.tau[c] = taui;
+    }
+    gbar(a.bar, epoch);
+    // ---- C: y = A(c+1:n, c+1:n) v  (column dots) and t1 = W^T v, t2 = V^T v
+    const int m = n - c - 1;
+    const int nvirt = m + 2 * i;
+    for (int jv = gwarp; jv < nvirt; jv += warps_total) {
+      const double* col;
+      if (jv < m) col = a.A + (int64_t)(c + 1 + jv) * a.lda;
+      else if (jv < m + i) col = a.W + (int64_t)(jv - m) * a.ldp;
+      else col = a.V + (int64_t)(jv - m - i) * a.ldp;
+      double s = 0.0;
+      for (int r = c + 1 + lane; r < n; r += 32) s += col[r] * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
+      s = warp_sum(s);
+      if (lane == 0) a.y[jv] = s;
+    }
+    gbar(a.bar, epoch);
+    // ---- D: w = tau (y - V t1 - W t2); alpha2 = w . v; w -= tau/2 alpha2 v
+    if (tid < 2 * i) vw[tid] = __ldcg(&a.y[m + tid]);  // t1 = vw[0:i], t2 = vw[i:2i]
+    __syncthreads();
+    double dotp = 0.0;
+    for (int r = c + 1 + gtid; r < n; r += gsz) {
+      double w = __ldcg(&a.y[r - c - 1]);
+      for (int t = 0; t < i; ++t)
+        w -= a.V[r + (int64_t)t * a.ldp] * vw[t] + a.W[r + (int64_t)t * a.ldp] * vw[i + t];
+      w *= taui;
+      a.W[r + (int64_t)i * a.ldp] = w;
+      dotp += w * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
+    }
+    block_atomic_sum(dotp, &red[2], scratch);
+    gbar(a.bar, epoch);
+    const double a2 = -0.5 * taui * __ldcg(&red[2]);
+    for (int r = gtid; r < n; r += gsz) {
+      double* wp = &a.W[r + (int64_t)i * a.ldp];
+      if (r <= c) *wp = 0.0;
+      else *wp += a2 * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
+    }
+    gbar(a.bar, epoch);
+  }
+}
+
+// Sturm count: number of eigenvalues of T (d, e) strictly below x.
+QDWHG_DEV int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (q < 0.0) ++cnt;
+  for (int i = 1; i < n; ++i) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = d[i] - x - e2[i - 1] / q;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+// Eigenvalue k (ascending) by multisection on [lo, hi]: one warp per
+// eigenvalue, the 32 lanes evaluate 32 Sturm counts at once, so every round
+// shrinks the bracket 33x (~11 rounds to full precision instead of ~55).
+__global__ void bisect_kernel(const double* d, const double* e2, int n, double lo0, double hi0,
+                              double pivmin, double abstol, double* w) {
+  const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= n) return;
+  double lo = lo0, hi = hi0;
+  for (int it = 0; it < 40; ++it) {
+    if (hi - lo <= abstol + 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const bool above = sturm_count(d, e2, n, x, pivmin) > k;  // lambda_k < x
+    const unsigned m = __ballot_sync(0xffffffffu, above);
+    // first lane whose point lies above lambda_k
+    const int f = m ? (__ffs(m) - 1) : 32;
+    const double nlo = (f == 0) ? lo : lo + (hi - lo) * (double)f / 33.0;
+    const double nhi = (f == 32) ? hi : lo + (hi - lo) * (double)(f + 1) / 33.0;
+    if (nlo == lo && nhi == hi) break;
+    lo = nlo;
+    hi = nhi;
+  }
+  if (lane == 0) w[k] = 0.5 * (lo + hi);
+}
+
+// Inverse iteration for eigenvalue w[k]: (T - w I) z = b with partial pivoting,
+// 3 solves, normalised.  Z is stored transposed: Zt[k + i*n] = z_k(i).
+// Factor storage (per thread, transposed likewise): u1 diag, u2 super, u3 super2, l, piv.
+__global__ void inviter_kernel(const double* d, const double* e, int n, const double* w,
+                               double tnorm, double* Zt, double* U1, double* U2, double* U3,
+                               double* L, unsigned char* P) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double lam = w[k];
+  const double eps = 2.220446049250313e-16;
+  const double tiny = eps * tnorm;
+  // ---- LU with partial pivoting of the tridiagonal (dlagtf shape)
+  double a = d[0] - lam;                  // current diagonal
+  double b = (n > 1) ? e[0] : 0.0;        // current super
+  for (int i = 0; i < n - 1; ++i) {
+    const double cc = e[i];              // sub-diagonal below row i
+    const double dn = d[i + 1] - lam;
+    const double bn = (i + 2 < n) ? e[i + 1] : 0.0;
+    const size_t o = (size_t)k + (size_t)i * n;
+    if (fabs(a) >= fabs(cc)) {
+      // no swap: row i stays; multiplier l = cc / a
+      const double piv = (a == 0.0) ? tiny : a;
+      const double l = cc / piv;
+      U1[o] = piv;
+      U2[o] = b;
+      U3[o] = 0.0;
+      L[o] = l;
+      P[o] = 0;
+      a = dn - l * b;
+      b = bn;
+    } else {
+      // swap rows i and i+1
+      const double l = a / cc;
+      U1[o] = cc;
+      U2[o] = dn;
+      U3[o] = bn;
+      L[o] = l;
+      P[o] = 1;
+      a = b - l * dn;
+      b = -l * bn;
+    }
+  }
+  {
+    const size_t o = (size_t)k + (size_t)(n - 1) * n;
+    U1[o] = (a == 0.0) ? tiny : a;
+    U2[o] = 0.0;
+    U3[o] = 0.0;
+  }
+  // ---- iterations: forward apply L (with pivots), back-solve U
+  // start vector: ones (dstein uses random; ones is adequate after 3 solves)
+  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] = 1.0;
+  for (int it = 0; it < 3; ++it) {
+    if (it > 0) {
+      // forward: apply the row swaps/multipliers to the rhs
+      for (int i = 0; i < n - 1; ++i) {
+        const size_t o = (size_t)k + (size_t)i * n;
+        double zi = Zt[o], zn = Zt[o + n];
+        if (P[o]) {
+          const double t = zi;
+          zi = zn;
+          zn = t;
+        }
+        zn -= L[o] * zi;
+        Zt[o] = zi;
+        Zt[o + n] = zn;
+      }
+    }
+    // back substitution U z = rhs, with scaling against overflow
+    double z2 = 0.0, z1 = 0.0, nrm = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+      const size_t o = (size_t)k + (size_t)i * n;
+      double v = Zt[o] - U2[o] * z1 - U3[o] * z2;
+      v /= U1[o];
+      Zt[o] = v;
+      z2 = z1;
+      z1 = v;
+      nrm = fmax(nrm, fabs(v));
+    }
+    // normalise (inf-norm first, then 2-norm at the end)
+    const double s = (nrm > 0.0) ? 1.0 / nrm : 1.0;
+    for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] *= s;
+  }
+  double s2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = Zt[(size_t)k + (size_t)i * n];
+    s2 += v * v;
+  }
+  const double inv = 1.0 / sqrt(s2);
+  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] *= inv;
+}
+
+// Z(i, k) = Zt[k + i*n]
+__global__ void transpose_kernel(const double* Zt, int n, double* Z, int64_t ldz) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = by + r, k = bx + threadIdx.x;
+    tile[r][threadIdx.x] = (i < n && k < n) ? Zt[(size_t)k + (size_t)i * n] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int k = bx + r, i = by + threadIdx.x;
+    if (i < n && k < n) Z[i + (int64_t)k * ldz] = tile[threadIdx.x][r];
+  }
+}
+
+__global__ void square_kernel(const double* e, int n, double* e2) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n - 1; i += gridDim.x * blockDim.x)
+    e2[i] = e[i] * e[i];
+}
+
+}  // namespace
+
+void syev_dc_fallback(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+
+// Returns false if the eigenvectors could not be orthogonalised cheaply (caller falls back).
+bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
+  const int n = (int)S.rows;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat A = ctx.arena->alloc(n, n);
+  copy(ctx, S, A);
+  const int nb = kTrdNB;
+  const int npan = (n - 1 + nb - 1) / nb;  // columns 0 .. n-2 carry reflectors
+  DMat Vfull = ctx.arena->alloc(n, std::max(npan * nb, 1));
+  DMat Vp = ctx.arena->alloc(n, nb), Wp = ctx.arena->alloc(n, nb);
+  double* dd = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
+  double* ee = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
+  double* tau = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (npan * nb + 8)));
+  double* y = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 2 * nb + 8)));
+  double* red = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 64));
+  unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
+  QDWHG_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (npan * nb + 8), ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(ee, 0, sizeof(double) * (n + 8), ctx.stream));
+  fill(ctx, Vfull, 0.0, 0.0);
+  // all SMs: the per-column SYMV streams the trailing matrix (HBM/L2 bound)
+  const int grid = std::max(1, std::min(ctx.num_sms, (n + 31) / 32));
+  for (int p = 0; p < npan; ++p) {
+    const int j0 = p * nb;
+    const int b = std::min(nb, n - 1 - j0);
+    QDWHG_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * 64, ctx.stream));
+    QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+    TrdArgs args{A.ptr(), A.ld, Vp.ptr(), Wp.ptr(), Vp.ld, dd, ee, tau, y, red, bar, n, j0, b};
+    void* kargs[] = {&args};
+    QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, dim3(grid), dim3(kTrdThreads),
+                                           kargs, 0, ctx.stream));
+    ctx.count();
+    copy(ctx, Vp.sub(0, 0, n, b), Vfull.sub(0, j0, n, b));
+    const int r0 = j0 + b;
+    const int rest = n - r0;
+    if (rest > 0) {
+      const DMat Vr = Vp.sub(r0, 0, rest, b), Wr = Wp.sub(r0, 0, rest, b);
+      const DMat At = A.sub(r0, r0, rest, rest);
+      gemm(ctx, Op::N, Op::T, -1.0, Vr, Wr, 1.0, At);
+      gemm(ctx, Op::N, Op::T, -1.0, Wr, Vr, 1.0, At);
+    }
+  }
+  // last diagonal entry (and the one before if the last panel ended early)
+  {
+    // d[n-1] = A(n-1, n-1) after all updates (no reflector column touches it again)
+    QDWHG_CUDA(cudaMemcpyAsync(dd + (n - 1), A.ptr() + (n - 1) + (int64_t)(n - 1) * A.ld,
+                               sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+  }
+  // ---- tridiagonal eigenvalues (bisection) and vectors (inverse iteration)
+  std::vector<double> hd(n), he(n);
+  QDWHG_CUDA(cudaMemcpyAsync(hd.data(), dd, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaMemcpyAsync(he.data(), ee, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  double lo = 1e308, hi = -1e308, tnorm = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? std::abs(he[i - 1]) : 0.0) + (i + 1 < n ? std::abs(he[i]) : 0.0);
+    lo = std::min(lo, hd[i] - r);
+    hi = std::max(hi, hd[i] + r);
+    tnorm = std::max(tnorm, std::abs(hd[i]) + r);
+  }
+  if (!(tnorm > 0.0)) tnorm = 1.0;
+  const double eps = 2.220446049250313e-16;
+  lo -= 2 * eps * tnorm + 1e-300;
+  hi += 2 * eps * tnorm + 1e-300;
+  double* e2 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
+  double* wv = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
+  square_kernel<<<std::max(1, std::min(148, (n + 255) / 256)), 256, 0, ctx.stream>>>(ee, n, e2);
+  const double pivmin = std::max(1e-300, eps * eps * tnorm * tnorm * 1e-10);
+  bisect_kernel<<<(32 * n + 127) / 128, 128, 0, ctx.stream>>>(dd, e2, n, lo, hi, pivmin, 2 * eps * tnorm * 1e-3,
+                                                     wv);
+  const size_t nn = (size_t)n * n;
+  double* Zt = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
+  double* U1 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
+  double* U2 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
+  double* U3 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
+  double* Lm = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
+  unsigned char* Pv = static_cast<unsigned char*>(ctx.arena->alloc_bytes(nn));
+  inviter_kernel<<<(n + 63) / 64, 64, 0, ctx.stream>>>(dd, ee, n, wv, tnorm, Zt, U1, U2, U3, Lm, Pv);
+  DMat Z = ctx.arena->alloc(n, n);
+  transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx.stream>>>(Zt, n, Z.ptr(),
+                                                                                     Z.ld);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count(4);
+  // ---- Lowdin: E = Z^T Z - I;  Z <- Z (I - E/2 + 3/8 E^2)
+  DMat E = ctx.arena->alloc(n, n);
+  GemmExtra gr;
+  gr.out = OutMode::LowerMirror;
+  gr.diag_add = -1.0;
+  gemm(ctx, Op::T, Op::N, 1.0, Z, Z, 0.0, E, gr);
+  const MatStats es = mat_stats(ctx, E, false);
+  if (!(es.maxabs < 1e-4)) {
+    ctx.arena->release_to(mark);
+    return false;
+  }
+  DMat F = ctx.arena->alloc(n, n);
+  GemmExtra f2;
+  f2.cin = &E;  // F = 3/8 E^2 - 1/2 E + I
+  f2.diag_add = 1.0;
+  gemm(ctx, Op::N, Op::N, 0.375, E, E, -0.5, F, f2);
+  DMat Z2 = ctx.arena->alloc(n, n);
+  gemm(ctx, Op::N, Op::N, 1.0, Z, F, 0.0, Z2);
+  // ---- back-transform: Vout = Q Z2, Q = H_0 ... H_{n-2}, blocks applied last to first
+  copy(ctx, Z2, Vout);
+  DMat G = ctx.arena->alloc(nb, nb), Tb = ctx.arena->alloc(nb, nb);
+  for (int p = npan - 1; p >= 0; --p) {
+    const int j0 = p * nb;
+    const int b = std::min(nb, n - 1 - j0);
+    const int r0 = j0 + 1;  // reflectors of this panel act on rows >= j0+1
+    const int mp = n - r0;
+    const DMat Vb = Vfull.sub(r0, j0, mp, b);
+    gemm(ctx, Op::T, Op::N, 1.0, Vb, Vb, 0.0, G.sub(0, 0, b, b));
+    larft_launch(ctx, G.sub(0, 0, b, b), tau + j0, Tb.sub(0, 0, b, b));
+    const Arena::Mark m2 = ctx.arena->mark();
+    DMat W1 = ctx.arena->alloc(b, n), W2 = ctx.arena->alloc(b, n);
+    const DMat C = Vout.sub(r0, 0, mp, n);
+    gemm(ctx, Op::T, Op::N, 1.0, Vb, C, 0.0, W1);
+    GemmExtra eu;
+    eu.krange = KRange::AUpper;
+    gemm(ctx, Op::N, Op::N, 1.0, Tb.sub(0, 0, b, b), W1, 0.0, W2, eu);
+    gemm(ctx, Op::N, Op::N, -1.0, Vb, W2, 1.0, C);
+    ctx.arena->release_to(m2);
+  }
+  vals.resize(n);
+  QDWHG_CUDA(cudaMemcpyAsync(vals.data(), wv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  ctx.arena->release_to(mark);
+  return true;
+}
+
+}  // namespace qdwhg
