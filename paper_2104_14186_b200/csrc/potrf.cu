@@ -306,6 +306,43 @@ void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb) 
   }
 }
 
+// Recursive Cholesky-and-inverse on the diagonal block [r0, r0+n):
+//   (W11, W11^-1) = rec(Z11);  W12 = W11^-T Z12;  Z22 -= W12^T W12;
+//   (W22, W22^-1) = rec(Z22);  W^-1_12 = -W11^-1 W12 W22^-1.
+// The trailing SYRK of the top level has K = n/2 (vs 128 for a right-looking
+// sweep), so almost all flops run at full DMMA rate; leaves are the 128-block
+// diag kernel.  Only the lower triangle of Z is read/updated.
+void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
+                  int nb) {
+  if (n <= nb) {
+    launch_diag(ctx, Z.sub(r0, r0, n, n), W.sub(r0, r0, n, n), Winv.sub(r0, r0, n, n));
+    return;
+  }
+  int64_t n1 = ((n / 2 + nb - 1) / nb) * nb;
+  if (n1 >= n) n1 = n - nb;
+  const int64_t n2 = n - n1;
+  chol_inv_rec(ctx, Z, W, Winv, r0, n1, nb);
+  const int64_t r1 = r0 + n1;
+  GemmExtra e1;
+  e1.krange = KRange::ALower;  // op(A) = W11^-T lower
+  gemm(ctx, Op::T, Op::T, 1.0, Winv.sub(r0, r0, n1, n1), Z.sub(r1, r0, n2, n1), 0.0,
+       W.sub(r0, r1, n1, n2), e1);
+  GemmExtra e2;
+  e2.out = OutMode::Lower;
+  const DMat W12 = W.sub(r0, r1, n1, n2);
+  gemm(ctx, Op::T, Op::N, -1.0, W12, W12, 1.0, Z.sub(r1, r1, n2, n2), e2);
+  chol_inv_rec(ctx, Z, W, Winv, r1, n2, nb);
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat T = ctx.arena->alloc(n1, n2);
+  GemmExtra e3;
+  e3.krange = KRange::BUpper;  // W22^-1 upper
+  gemm(ctx, Op::N, Op::N, 1.0, W12, Winv.sub(r1, r1, n2, n2), 0.0, T, e3);
+  GemmExtra e4;
+  e4.krange = KRange::AUpper;  // W11^-1 upper
+  gemm(ctx, Op::N, Op::N, -1.0, Winv.sub(r0, r0, n1, n1), T, 0.0, Winv.sub(r0, r1, n1, n2), e4);
+  ctx.arena->release_to(mark);
+}
+
 }  // namespace
 
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w) {
@@ -317,25 +354,9 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   DMat W = ctx.arena->alloc(n, n);
   fill(ctx, W, 0.0, 0.0);
   fill(ctx, Winv, 0.0, 0.0);
-  for (int64_t k = 0; k < n; k += nb) {
-    const int64_t b = std::min<int64_t>(nb, n - k);
-    const int64_t rest = n - k - b;
-    launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
-    if (rest > 0) {
-      // W_k,rest = W_kk^{-T} Z_k,rest = W_kk^{-T} (Z_rest,k)^T   (only the lower
-      // triangle of Z is ever read or updated; op(A) = Winv_kk^T is lower -> ALower)
-      GemmExtra e1;
-      e1.krange = KRange::ALower;
-      gemm(ctx, Op::T, Op::T, 1.0, Winv.sub(k, k, b, b), Z.sub(k + b, k, rest, b), 0.0,
-           W.sub(k, k + b, b, rest), e1);
-      // Z_rest -= W_k,rest^T W_k,rest   (lower triangle only)
-      GemmExtra e2;
-      e2.out = OutMode::Lower;
-      const DMat Wp = W.sub(k, k + b, b, rest);
-      gemm(ctx, Op::T, Op::N, -1.0, Wp, Wp, 1.0, Z.sub(k + b, k + b, rest, rest), e2);
-    }
-  }
-  // pivot check before the inverse is trusted
+  chol_inv_rec(ctx, Z, W, Winv, 0, n, nb);
+  // one pivot check for the whole factorisation (a failed pivot poisons what
+  // follows with NaN, which is discarded: the call throws)
   int hflag = 0;
   QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -343,11 +364,6 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
     ctx.arena->release_to(mark);
     throw NotPositiveDefinite("cholesky: pivot is not positive");
   }
-  const int64_t nblk = n / nb;
-  if (n % nb == 0 && (nblk & (nblk - 1)) == 0)
-    trtri_levels(ctx, W, Winv, n, nb);
-  else
-    trtri_rec(ctx, W, Winv, 0, n, nb);
   if (want_w) copy(ctx, W, Z);  // W (upper, zero strict lower) back in Z for qdwhg_cholesky
   ctx.arena->release_to(mark);
 }
