@@ -367,47 +367,91 @@ void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T)
 void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   const int64_t m = A.rows, n = A.cols;
   if (m < n) throw InvalidArgument("geqrf: requires rows >= cols");
-  const int nb = w.nb = kBW;
-  const int64_t npan = (n + nb - 1) / nb;
+  // Two-level blocking: 64-column panels (one cooperative/cluster kernel each)
+  // inside 256-column outer blocks.  Inner updates touch only the outer block;
+  // the outer T (256 x 256) is assembled by merging the panel T's
+  // (T = [T1, -T1 (V1^T V2) T2; 0, T2]) so the trailing update of the rest of
+  // the matrix — the O(n^3) part — runs as GEMMs with K = 256.
+  const int nbi = kBW;
+  const int nbo = 4 * kBW;
+  w.nb = nbo;
+  const int64_t nout = (n + nbo - 1) / nbo;
   w.V = ctx.arena->alloc(m, n);
-  w.T = ctx.arena->alloc(nb, npan * nb);
+  w.T = ctx.arena->alloc(nbo, nout * nbo);
+  fill(ctx, w.T, 0.0, 0.0);
   double* tau_dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 64)));
   double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW));
   unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
-  DMat G = ctx.arena->alloc(nb, nb);
+  DMat G = ctx.arena->alloc(nbo, nbo);
   const Arena::Mark mark = ctx.arena->mark();
-  for (int64_t p = 0; p < npan; ++p) {
-    const int64_t j0 = p * nb;
-    const int64_t b = std::min<int64_t>(nb, n - j0);
-    const int64_t mp = m - j0;
-    const DMat Pn = A.sub(j0, j0, mp, b);
-    const DMat Vp = w.V.sub(j0, j0, mp, b);
-    panel_factor(ctx, Pn, Vp, tau_dev + j0, acc, bar);
-    // V above the panel block is zero (rows < j0 of these columns)
-    if (j0 > 0) fill(ctx, w.V.sub(0, j0, j0, b), 0.0, 0.0);
-    // T_p from Gram V^T V
-    const DMat Gp = G.sub(0, 0, b, b);
-    gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
-    const DMat Tp = w.T.sub(0, p * nb, b, b);
-    larft_launch(ctx, Gp, tau_dev + j0, Tp);
-    // trailing update C = (I - V T V^T)^T C = C - V T^T (V^T C)
-    const int64_t nc = n - j0 - b;
+  for (int64_t po = 0; po < nout; ++po) {
+    const int64_t jo = po * nbo;
+    const int64_t bo = std::min<int64_t>(nbo, n - jo);
+    const int64_t mo = m - jo;
+    const DMat To = w.T.sub(0, po * nbo, bo, bo);
+    std::vector<std::pair<int64_t, int64_t>> blocks;  // (offset in outer block, width)
+    for (int64_t ji = 0; ji < bo; ji += nbi) {
+      const int64_t bi = std::min<int64_t>(nbi, bo - ji);
+      const int64_t j0 = jo + ji;
+      const int64_t mp = m - j0;
+      const DMat Vp = w.V.sub(j0, j0, mp, bi);
+      panel_factor(ctx, A.sub(j0, j0, mp, bi), Vp, tau_dev + j0, acc, bar);
+      if (j0 > 0) fill(ctx, w.V.sub(0, j0, j0, bi), 0.0, 0.0);  // V above the panel is zero
+      const DMat Gp = G.sub(0, 0, bi, bi);
+      gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
+      const DMat Ti = To.sub(ji, ji, bi, bi);
+      larft_launch(ctx, Gp, tau_dev + j0, Ti);
+      blocks.push_back({ji, bi});
+      const int64_t nc = bo - ji - bi;  // rest of the outer block
+      if (nc > 0) {
+        const DMat C = A.sub(j0, j0 + bi, mp, nc);
+        DMat W1 = ctx.arena->alloc(bi, nc), W2 = ctx.arena->alloc(bi, nc);
+        gemm(ctx, Op::T, Op::N, 1.0, Vp, C, 0.0, W1);
+        GemmExtra e;
+        e.krange = KRange::ALower;  // op(A) = T^T lower
+        gemm(ctx, Op::T, Op::N, 1.0, Ti, W1, 0.0, W2, e);
+        gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, C);
+        ctx.arena->release_to(mark);
+      }
+    }
+    const int64_t nc = n - jo - bo;
+    // ---- outer T (also needed by ORGQR for the last block) by pairwise merges of the panel T's
+    if (blocks.size() > 1) {
+      const DMat Vo = w.V.sub(jo, jo, mo, bo);
+      const DMat Go = G.sub(0, 0, bo, bo);
+      gemm(ctx, Op::T, Op::N, 1.0, Vo, Vo, 0.0, Go);
+      while (blocks.size() > 1) {
+        std::vector<std::pair<int64_t, int64_t>> next;
+        for (size_t q = 0; q + 1 < blocks.size(); q += 2) {
+          const auto [o1, s1] = blocks[q];
+          const auto [o2, s2] = blocks[q + 1];
+          DMat M1 = ctx.arena->alloc(s1, s2);
+          GemmExtra a1;
+          a1.krange = KRange::AUpper;  // T11 upper
+          gemm(ctx, Op::N, Op::N, 1.0, To.sub(o1, o1, s1, s1), Go.sub(o1, o2, s1, s2), 0.0, M1, a1);
+          GemmExtra a2;
+          a2.krange = KRange::BUpper;  // T22 upper
+          gemm(ctx, Op::N, Op::N, -1.0, M1, To.sub(o2, o2, s2, s2), 0.0, To.sub(o1, o2, s1, s2), a2);
+          ctx.arena->release_to(mark);
+          next.push_back({o1, s1 + s2});
+        }
+        if (blocks.size() % 2) next.push_back(blocks.back());
+        blocks.swap(next);
+      }
+    }
+    // ---- trailing update of the rest: C = C - V T^T (V^T C), K = bo
     if (nc > 0) {
-      const DMat C = A.sub(j0, j0 + b, mp, nc);
-      DMat W1 = ctx.arena->alloc(b, nc);
-      DMat W2 = ctx.arena->alloc(b, nc);
-      gemm(ctx, Op::T, Op::N, 1.0, Vp, C, 0.0, W1);
+      const DMat Vo = w.V.sub(jo, jo, mo, bo);
+      const DMat C = A.sub(jo, jo + bo, mo, nc);
+      DMat W1 = ctx.arena->alloc(bo, nc), W2 = ctx.arena->alloc(bo, nc);
+      gemm(ctx, Op::T, Op::N, 1.0, Vo, C, 0.0, W1);
       GemmExtra e;
-      e.krange = KRange::ALower;  // op(A) = T^T lower
-      gemm(ctx, Op::T, Op::N, 1.0, Tp, W1, 0.0, W2, e);
-      gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, C);
+      e.krange = KRange::ALower;
+      gemm(ctx, Op::T, Op::N, 1.0, To, W1, 0.0, W2, e);
+      gemm(ctx, Op::N, Op::N, -1.0, Vo, W2, 1.0, C);
       ctx.arena->release_to(mark);
     }
   }
-  w.taus.assign(n, 0.0);
-  QDWHG_CUDA(cudaMemcpyAsync(w.taus.data(), tau_dev, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                             ctx.stream));
-  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, const DMat& Q) {
