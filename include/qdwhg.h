@@ -216,6 +216,21 @@ qdwhg_status qdwhg_lanczos_min_bound(qdwhg_handle* h, int64_t n, const double* A
 qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
                         int64_t k, double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double beta, double* C, int64_t ldc);
+/* The same engine with the structure flags the QDWH steps use (DEVICE pointers):
+ *   krange: 0 full, 1 op(B) upper, 2 op(B) lower, 3 op(A) upper, 4 op(A) lower
+ *           (triangular operands store explicit zeros; their zero tiles are skipped)
+ *   out:    0 full C, 1 lower triangle mirrored to the upper, 2 lower triangle only
+ *   diag_add is added to the diagonal of C (e.g. Z = I + c X^T X in one launch). */
+qdwhg_status qdwhg_gemm_ex(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+                           int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double beta, double* C, int64_t ldc, int32_t krange,
+                           int32_t out, double diag_add);
+/* Upper Cholesky factor and its inverse: Z = W^T W; on return Z holds W and
+ * Winv = W^{-1} (both upper, explicit zeros below).  Reads the lower triangle
+ * of Z.  NOT_POSITIVE_DEFINITE on a non-positive pivot (kernels.cpp:136-138).
+ * Host or device pointers. */
+qdwhg_status qdwhg_cholesky_inverse(qdwhg_handle* h, int64_t n, double* Z, int64_t ldz,
+                                    double* Winv, int64_t ldwi);
 /* Counter-based N(0,1) matrix on the device (kernels.cpp:441-447 scheme, device libm). */
 qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64_t seed, double* A,
                                    int64_t lda);

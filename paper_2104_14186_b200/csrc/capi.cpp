@@ -708,8 +708,36 @@ qdwhg_status qdwhg_lanczos_min_bound(qdwhg_handle* h, int64_t n, const double* A
 qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
                         int64_t k, double alpha, const double* A, int64_t lda, const double* B,
                         int64_t ldb, double beta, double* C, int64_t ldc) {
+  return qdwhg_gemm_ex(h, trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, 0, 0, 0.0);
+}
+
+qdwhg_status qdwhg_cholesky_inverse(qdwhg_handle* h, int64_t n, double* Z, int64_t ldz,
+                                    double* Winv, int64_t ldwi) {
   if (!h) return QDWHG_INVALID_ARGUMENT;
   return guard(h, [&] {
+    if (n < 1 || !Z || !Winv) throw InvalidArgument("cholesky_inverse: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Zd = stage_in(ctx, Z, n, n, ldz, nullptr);
+    DMat Wi = ctx.arena->alloc(n, n);
+    potrf_upper_and_inverse(ctx, Zd, Wi, true);
+    stage_out(ctx, Wi, Winv, ldwi);
+    stage_out(ctx, Zd, Z, ldz);  // Z <- W (upper, zeros below)
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_gemm_ex(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+                           int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double beta, double* C, int64_t ldc, int32_t krange,
+                           int32_t out, double diag_add) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (krange < 0 || krange > 4 || out < 0 || out > 2)
+      throw InvalidArgument("qdwhg_gemm_ex: bad krange/out flags");
+    GemmExtra ex;
+    ex.krange = static_cast<KRange>(krange);
+    ex.out = out == 1 ? OutMode::LowerMirror : out == 2 ? OutMode::Lower : OutMode::Full;
+    ex.diag_add = diag_add;
     DMat Ad, Bd, Cd;
     Ad.base = const_cast<double*>(A);
     Ad.ld = lda;
@@ -734,10 +762,10 @@ qdwhg_status qdwhg_gemm(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64
     if (!aligned(Bd)) Bd = stage_in(ctx, B, Bd.rows, Bd.cols, ldb, nullptr);
     if (!aligned(Cd)) {
       DMat Cs = stage_in(ctx, C, m, n, ldc, nullptr);
-      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cs);
+      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cs, ex);
       stage_out(ctx, Cs, C, ldc);
     } else {
-      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cd);
+      gemm(ctx, trans_a ? Op::T : Op::N, trans_b ? Op::T : Op::N, alpha, Ad, Bd, beta, Cd, ex);
     }
     QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream));
   });

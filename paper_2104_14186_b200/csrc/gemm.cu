@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstdlib>
 
@@ -343,10 +344,38 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // Descriptor over the stored matrix of view `v`, extent clipped at the end of
 // the view so reads past the view are zero-filled by TMA.
+// Encoded descriptors are cached by (base, ld, extent, box): the arena hands
+// out the same addresses every QDWH iteration, so steady-state launches skip
+// the driver call.
+struct DescKey {
+  uintptr_t base;
+  int64_t ld;
+  uint64_t d0, d1;
+  int box0, box1;
+  bool operator==(const DescKey& o) const {
+    return base == o.base && ld == o.ld && d0 == o.d0 && d1 == o.d1 && box0 == o.box0 &&
+           box1 == o.box1;
+  }
+};
+struct DescKeyHash {
+  size_t operator()(const DescKey& k) const {
+    size_t h = std::hash<uintptr_t>()(k.base);
+    h ^= std::hash<int64_t>()(k.ld) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= std::hash<uint64_t>()(k.d0 * 1000003ull + k.d1) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= (size_t)(k.box0 * 131 + k.box1);
+    return h;
+  }
+};
+
 CUtensorMap make_desc(const DMat& v, int box0, int box1) {
+  static thread_local std::unordered_map<DescKey, CUtensorMap, DescKeyHash> cache;
   CUtensorMap tm;
   const uint64_t d0 = (uint64_t)std::max<int64_t>(v.r0 + v.rows, 1);
   const uint64_t d1 = (uint64_t)std::max<int64_t>(v.c0 + v.cols, 1);
+  const DescKey key{reinterpret_cast<uintptr_t>(v.base), v.ld, d0, d1, box0, box1};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 8192) cache.clear();
   cuuint64_t dims[2] = {d0, d1};
   cuuint64_t strides[1] = {(cuuint64_t)v.ld * 8};
   cuuint32_t box[2] = {(cuuint32_t)box0, (cuuint32_t)box1};
@@ -356,6 +385,7 @@ CUtensorMap make_desc(const DMat& v, int box0, int box1) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  cache.emplace(key, tm);
   return tm;
 }
 

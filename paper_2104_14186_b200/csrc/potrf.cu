@@ -12,6 +12,8 @@
 //     become two TRMMs with W^-1 (same 2mn^2 flops, fully parallel).
 // A non-positive pivot raises the device flag; the host turns it into
 // NotPositiveDefinite, matching kernels.cpp:136-138.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.hpp"
 
@@ -348,7 +350,8 @@ void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int6
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w) {
   const int64_t n = Z.rows;
   if (Z.cols != n) throw InvalidArgument("cholesky: matrix not square");
-  const int nb = 128;
+  static const int nb_env = getenv("QDWHG_POTRF_NB") ? atoi(getenv("QDWHG_POTRF_NB")) : 0;
+  const int nb = (nb_env == 32 || nb_env == 64 || nb_env == 96 || nb_env == 128) ? nb_env : 128;
   QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);

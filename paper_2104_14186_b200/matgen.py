@@ -47,6 +47,18 @@ def to_unit_np(h: np.ndarray) -> np.ndarray:
     return ((h >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
 
 
+def gaussian_host(count: int, seed: int) -> np.ndarray:
+    """N(0,1) draws 0..count-1 of the reference's counter generator
+    (kernels.cpp:28-32): exact u64 hashing, then glibc log/cos via `math`,
+    so the values are bit-identical to qdwh::gaussian_matrix(count, 1, seed)."""
+    import math
+    i = np.arange(count, dtype=np.uint64)
+    u1 = to_unit_np(hash64_np(seed, 2 * i))
+    u2 = to_unit_np(hash64_np(seed, 2 * i + 1))
+    return np.array([math.sqrt(-2.0 * math.log(a)) * math.cos(2.0 * math.pi * b)
+                     for a, b in zip(u1.tolist(), u2.tolist())])
+
+
 def config_eigenvalues(family: str, n: int, seed: int = 42) -> np.ndarray:
     """Planted eigenvalues, index order (not sorted)."""
     i = np.arange(n)

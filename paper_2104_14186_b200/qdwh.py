@@ -566,9 +566,14 @@ def lanczos_min_bound(a, steps: int = 30, *, handle: Optional[Handle] = None) ->
     return out.value
 
 
-def gemm(a, b, c, alpha=1.0, beta=0.0, trans_a=False, trans_b=False, *,
-         handle: Optional[Handle] = None):
-    """C = alpha op(A) op(B) + beta C on torch CUDA tensors (column-major views)."""
+KRANGE = {"full": 0, "b_upper": 1, "b_lower": 2, "a_upper": 3, "a_lower": 4}
+OUTMODE = {"full": 0, "lower_mirror": 1, "lower": 2}
+
+
+def gemm(a, b, c, alpha=1.0, beta=0.0, trans_a=False, trans_b=False, *, krange="full",
+         out="full", diag_add=0.0, handle: Optional[Handle] = None):
+    """C = alpha op(A) op(B) + beta C (+ diag_add I) on torch CUDA tensors (column-major
+    views), with the triangular K-range / lower-output structure flags of qdwhg_gemm_ex."""
     h = handle or default_handle()
     A, B, C = _Mat(a), _Mat(b), _Mat(c)
     if not (A.device and B.device and C.device):
@@ -577,9 +582,29 @@ def gemm(a, b, c, alpha=1.0, beta=0.0, trans_a=False, trans_b=False, *,
         raise ValueError("gemm: C must be a column-major view")
     m, n = C.shape
     k = A.shape[0] if trans_a else A.shape[1]
-    h.check(h.lib.qdwhg_gemm(h.h, int(trans_a), int(trans_b), m, n, k, float(alpha), A.ptr, A.ld,
-                             B.ptr, B.ld, float(beta), C.ptr, C.ld))
+    h.check(h.lib.qdwhg_gemm_ex(h.h, int(trans_a), int(trans_b), m, n, k, float(alpha), A.ptr,
+                                A.ld, B.ptr, B.ld, float(beta), C.ptr, C.ld, KRANGE[krange],
+                                OUTMODE[out], float(diag_add)))
     return c
+
+
+def cholesky_factor_inverse(z, *, handle: Optional[Handle] = None):
+    """(W, W^{-1}), both upper, of Z = W^T W; reads the lower triangle of z
+    (kernels.cpp:124-146).  Raises NotPositiveDefinite."""
+    h = handle or default_handle()
+    Z = _Mat(z)
+    n = Z.shape[0]
+    zc = Z.obj.clone() if Z.device else np.array(Z.obj, order="F", copy=True)
+    Wi = _empty_like_kind(Z, n, n)
+    zp, ldz = _ptr_ld(zc)
+    wp, ldw = _ptr_ld(Wi)
+    h.check(h.lib.qdwhg_cholesky_inverse(h.h, n, zp, ldz, wp, ldw))
+    return zc, Wi
+
+
+def cholesky_inverse(z, *, handle: Optional[Handle] = None):
+    """W^{-1} (upper) of Z = W^T W."""
+    return cholesky_factor_inverse(z, handle=handle)[1]
 
 
 def gaussian_matrix_device(m: int, n: int, seed: int, *, device=None,
