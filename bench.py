@@ -49,7 +49,81 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip live GEMM event timing")
+    p.add_argument("--dist", action="store_true",
+                   help="one solve split over the ranks (1D row blocks, strong scaling) "
+                        "instead of one replica per rank")
     return p.parse_args()
+
+
+def run_dist(args, world, rank, dev, handle, dist):
+    """Strong scaling: ONE config solve over all ranks (paper_2104_14186_b200/dist.py).
+    A is generated on rank 0 and broadcast; rank r keeps its row block."""
+    import torch
+    from paper_2104_14186_b200 import dist as D
+    comm = D.Comm(dist) if world > 1 else None
+    if comm is None:
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                                world_size=1)
+        comm = D.Comm(dist)
+    inp = make_input(args.config, dev, handle) if rank == 0 else None
+    c = config_desc(args.config)
+    m = c["n"] if c["kind"] == "eig" else c["m"]
+    n = c["n"]
+    A = inp["A"] if rank == 0 else torch.empty((n, m), dtype=torch.float64, device=dev).t()
+    comm.broadcast(A)
+    meta = torch.tensor([inp["c"] if (rank == 0 and c["kind"] == "eig") else
+                         (inp["cut"] if rank == 0 else 0.0)], dtype=torch.float64, device=dev)
+    comm.broadcast(meta)
+    r0, r1 = D.row_range(m, rank, world)
+    A_r = A[r0:r1].t().contiguous().t()
+    be = D.GpuBackend(handle)
+
+    def one():
+        if c["kind"] == "eig":
+            B_r = -A_r.clone()
+            idx = torch.arange(r1 - r0, device=dev)
+            B_r[idx, r0 + idx] += float(meta.item())        # rows of cI - A (LARGEST)
+            return D.dist_partial_eig(be, comm, B_r.t().contiguous().t(), m)
+        return D.dist_partial_svd(be, comm, A_r, m, n, cut=float(meta.item()))
+
+    for _ in range(max(args.warmup, 0)):
+        res = one()
+    times, flops = [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(int(str(dev).split(":")[-1]) if ":" in str(dev) else 0)
+    sampler.start()
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0.record()
+        res = one()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        times.append(e0.elapsed_time(e1) / 1e3)
+        flops.append(res.flops)
+    clocks = sampler.stop()
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_t = float(t.item())
+    if rank == 0:
+        kk = len(res.values)
+        line = {"metric": METRIC, "value": sum(flops) / tot_t / 1e12, "unit": "TFLOP/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Gaussian factors, planted spectrum, generated on device)",
+                "config": dict(config_json(args.config, world), parallelism=f"rows{world}"),
+                "time_to_solution_s": tot_t / args.steps, "clocks": clocks,
+                "gpu_launches": int(handle.launches()),
+                "result": {"k": kk, "subspace_size": res.subspace_size,
+                           "iters_chol": res.iters_chol, "iters_qr": res.iters_qr}}
+        print(json.dumps(line))
+    dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ clocks
@@ -320,6 +394,9 @@ def main():
     handle = qdwh.Handle(device=local)
     handle.set_stream(torch.cuda.current_stream(dev).cuda_stream)
 
+    if args.dist:
+        run_dist(args, world, rank, dev, handle, dist)
+        return
     inp = make_input(args.config, dev, handle)
     n_rows = inp["A"].shape[0]
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > L2

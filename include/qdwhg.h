@@ -153,7 +153,8 @@ const char* qdwhg_last_error(const qdwhg_handle* h);
 qdwhg_status qdwhg_get_launch_count(const qdwhg_handle* h, uint64_t* launches);
 qdwhg_status qdwhg_synchronize(qdwhg_handle* h);
 /* Run on a caller stream (cudaStream_t, e.g. torch's current stream); NULL
- * restores the handle's own stream.  Calls stay synchronous. */
+ * restores the handle's own (non-blocking) stream, cudaStreamLegacy ((void*)1)
+ * selects the legacy default stream.  Calls stay synchronous. */
 qdwhg_status qdwhg_set_stream(qdwhg_handle* h, void* stream);
 
 /* Live kernel accounting: with profiling enabled every DMMA GEMM launch is

@@ -95,7 +95,8 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   syrk.diag_add = 1.0;
   gemm(ctx, Op::T, Op::N, w.c, X, X, 0.0, Z, syrk);
   try {
-    potrf_upper_and_inverse(ctx, Z, Winv);
+    // kappa(Z) <= 1 + c: the fast recursive Cholesky-and-inverse is accurate here
+    potrf_upper_and_inverse(ctx, Z, Winv, false, false);
   } catch (...) {
     ctx.arena->release_to(mark);
     throw;
@@ -314,43 +315,6 @@ void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) 
   syev_dc(ctx, S, vals, Vout, 0);
 }
 
-// Tall-skinny QR A = Q R by CholeskyQR2 (two Gram/POTRF/TRMM passes, all GEMM
-// work) when A is well enough conditioned (diag ratio of the first Cholesky
-// factor <= 1e5, i.e. u*kappa^2 << 1); returns false (caller falls back to
-// Householder) otherwise or on a Cholesky breakdown.
-static bool cholesky_qr2(Ctx& ctx, const DMat& A, const DMat& Q, const DMat& R) {
-  const int64_t n = A.cols;
-  DMat G = ctx.arena->alloc(n, n), Gi = ctx.arena->alloc(n, n);
-  DMat G2 = ctx.arena->alloc(n, n), G2i = ctx.arena->alloc(n, n);
-  GemmExtra syrk;
-  syrk.out = OutMode::Lower;
-  GemmExtra trmm;
-  trmm.krange = KRange::BUpper;
-  try {
-    gemm(ctx, Op::T, Op::N, 1.0, A, A, 0.0, G, syrk);
-    potrf_upper_and_inverse(ctx, G, Gi, true);  // G <- W1
-    std::vector<double> d;
-    diag_to_host(ctx, G, d);
-    double dmax = 0.0, dmin = 1e308;
-    for (double x : d) {
-      dmax = std::max(dmax, std::abs(x));
-      dmin = std::min(dmin, std::abs(x));
-    }
-    if (!(dmin > 0.0) || dmax / dmin > 1e5) return false;
-    DMat Q1 = ctx.arena->alloc(A.rows, n);
-    gemm(ctx, Op::N, Op::N, 1.0, A, Gi, 0.0, Q1, trmm);  // Q1 = A W1^-1
-    gemm(ctx, Op::T, Op::N, 1.0, Q1, Q1, 0.0, G2, syrk);
-    potrf_upper_and_inverse(ctx, G2, G2i, true);           // G2 <- W2
-    gemm(ctx, Op::N, Op::N, 1.0, Q1, G2i, 0.0, Q, trmm);  // Q = Q1 W2^-1
-  } catch (const NotPositiveDefinite&) {
-    return false;
-  }
-  GemmExtra up;
-  up.krange = KRange::AUpper;
-  gemm(ctx, Op::N, Op::N, 1.0, G2, G, 0.0, R, up);  // R = W2 W1
-  return true;
-}
-
 void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V) {
   // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order.
   // Tall A (m > n) is first reduced to its n x n triangular factor (A = Q R), so
@@ -358,8 +322,10 @@ void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigm
   const int64_t m = A.rows, n = A.cols;
   if (m > n) {
     const Arena::Mark mark = ctx.arena->mark();
+    // Householder (not CholeskyQR2: A Q2 can be ill-conditioned and R's accuracy
+    // sets the small singular values' relative accuracy)
     DMat Q = ctx.arena->alloc(m, n), R = ctx.arena->alloc(n, n);
-    if (!cholesky_qr2(ctx, A, Q, R)) {
+    {
       DMat Aw = ctx.arena->alloc(m, n);
       copy(ctx, A, Aw);
       QrWork qw;

@@ -160,7 +160,12 @@ void zero_strict_lower(Ctx& ctx, const DMat& X);
 // Z = W^T W with W upper; only the lower triangle of Z is read (it is used as
 // workspace).  Winv (n x n) receives W^{-1} (upper, explicit zeros below); with
 // want_w, Z is overwritten by W (upper, zeros below).  Throws NotPositiveDefinite.
-void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false);
+// stable = true: right-looking factorisation with triangular-solve panels
+// (backward stable for any SPD input); stable = false: recursive variant that
+// multiplies by explicit inverses of half blocks (errors ~ u*kappa(W)^2, used
+// only for the QDWH Cholesky steps where kappa(Z) <= 1 + c).
+void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false,
+                             bool stable = true);
 
 // ------------------------------------------------------------------ geqrf.cu
 struct QrWork {

@@ -130,27 +130,16 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
     __syncthreads();
     const int p0 = b0 + kSB, R = nbp - p0;
     if (R > 0) {
-      // ---- panel: L(i, b0+c) = sum_{k<=c} Z(i, b0+k) * Dinv(c, k); 12 rows per thread
-      {
-        const int c = tid & 31, i0 = tid >> 5;
-        double acc[12];
-#pragma unroll
-        for (int q = 0; q < 12; ++q) acc[q] = 0.0;
-        for (int k = 0; k <= c; ++k) {
-          const double dk = D[k * 33 + c];
-          const double* col = A + (b0 + k) * kLDA + p0 + i0;
-#pragma unroll
-          for (int q = 0; q < 12; ++q)
-            if (i0 + 8 * q < R) acc[q] += col[8 * q] * dk;
+      // ---- panel rows below the block by forward substitution (one thread per
+      // row; no multiplication by the explicit inverse, which would cost
+      // u*kappa(D)^2 accuracy on ill-conditioned blocks):
+      // L(i, b0+c) = (Z(i, b0+c) - sum_{t<c} L(i, b0+t) L(b0+c, b0+t)) / L(b0+c, b0+c)
+      for (int i = tid; i < R; i += kDiagThreads) {
+        for (int c = 0; c < kSB; ++c) {
+          double s = A[(b0 + c) * kLDA + p0 + i];
+          for (int t = 0; t < c; ++t) s -= A[(b0 + t) * kLDA + p0 + i] * A[(b0 + t) * kLDA + b0 + c];
+          A[(b0 + c) * kLDA + p0 + i] = s * S[c];
         }
-#pragma unroll
-        for (int q = 0; q < 12; ++q)
-          if (i0 + 8 * q < R) T[c * kLDA + i0 + 8 * q] = acc[q];
-      }
-      __syncthreads();
-      for (int idx = tid; idx < R * kSB; idx += kDiagThreads) {
-        const int i = idx % R, c = idx / R;
-        A[(b0 + c) * kLDA + p0 + i] = T[c * kLDA + i];
       }
       __syncthreads();
       // ---- trailing rank-32 update of the lower triangle, 4x4 register tiles
@@ -308,6 +297,55 @@ void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb) 
   }
 }
 
+// Panel of the stable POTRF: X = W_kk^{-T} Z_k,rest with Z_k,rest read as the
+// transpose of the lower block Zr = Z(rest, k) (b x ncols result into X).
+// W_kk^T is lower: forward substitution per column, 64 columns per CTA,
+// W_kk and the solution tile in shared memory.
+__global__ void __launch_bounds__(64) panel_trsm_kernel(const double* Wkk, int64_t ldw,
+                                                         const double* Zr, int64_t ldz, double* X,
+                                                         int64_t ldx, int b, int ncols) {
+  extern __shared__ double smt[];
+  double* Ws = smt;              // b x (b+1), Ws[c*(b+1) + r] = W_kk(r, c)
+  double* Xs = Ws + b * (b + 1);  // b x 65, Xs[i*65 + col]
+  const int tid = threadIdx.x;
+  const int j = blockIdx.x * 64 + tid;
+  for (int idx = tid; idx < b * b; idx += 64) {
+    const int r = idx % b, c = idx / b;
+    Ws[c * (b + 1) + r] = Wkk[r + (int64_t)c * ldw];
+  }
+  __syncthreads();
+  if (j < ncols) {
+    for (int i = 0; i < b; ++i) {
+      double s = Zr[j + (int64_t)i * ldz];  // Z(k+b+j, k+i) = Z_k,rest(i, j)
+      const double* wc = Ws + i * (b + 1);  // column i of W_kk: W_kk(t, i)
+      for (int t = 0; t < i; ++t) s -= wc[t] * Xs[t * 65 + tid];
+      Xs[i * 65 + tid] = s / wc[i];
+    }
+  }
+  __syncthreads();
+  // X(i, j): rows i of W's panel block, coalesced along j
+  for (int idx = tid; idx < b * 64; idx += 64) {
+    const int i = idx / 64, col = idx % 64;
+    const int jj = blockIdx.x * 64 + col;
+    if (jj < ncols) X[i + (int64_t)jj * ldx] = Xs[i * 65 + col];
+  }
+}
+
+void launch_panel_trsm(Ctx& ctx, const DMat& Wkk, const DMat& Zr, const DMat& X) {
+  const int b = (int)Wkk.rows, ncols = (int)Zr.rows;
+  const size_t smem = ((size_t)b * (b + 1) + (size_t)b * 65) * 8;
+  static bool set = false;
+  if (!set) {
+    QDWHG_CUDA(cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)((128 * 129 + 128 * 65) * 8)));
+    set = true;
+  }
+  panel_trsm_kernel<<<(ncols + 63) / 64, 64, smem, ctx.stream>>>(Wkk.ptr(), Wkk.ld, Zr.ptr(), Zr.ld,
+                                                                X.ptr(), X.ld, b, ncols);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+}
+
 // Recursive Cholesky-and-inverse on the diagonal block [r0, r0+n):
 //   (W11, W11^-1) = rec(Z11);  W12 = W11^-T Z12;  Z22 -= W12^T W12;
 //   (W22, W22^-1) = rec(Z22);  W^-1_12 = -W11^-1 W12 W22^-1.
@@ -347,7 +385,7 @@ void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int6
 
 }  // namespace
 
-void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w) {
+void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w, bool stable) {
   const int64_t n = Z.rows;
   if (Z.cols != n) throw InvalidArgument("cholesky: matrix not square");
   static const int nb_env = getenv("QDWHG_POTRF_NB") ? atoi(getenv("QDWHG_POTRF_NB")) : 0;
@@ -357,7 +395,29 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   DMat W = ctx.arena->alloc(n, n);
   fill(ctx, W, 0.0, 0.0);
   fill(ctx, Winv, 0.0, 0.0);
-  chol_inv_rec(ctx, Z, W, Winv, 0, n, nb);
+  if (!stable) {
+    chol_inv_rec(ctx, Z, W, Winv, 0, n, nb);
+  } else {
+    // right-looking, panel by forward substitution (no explicit inverse in the
+    // factorisation: backward stable like the reference's dot-product Cholesky)
+    for (int64_t k = 0; k < n; k += nb) {
+      const int64_t b = std::min<int64_t>(nb, n - k);
+      const int64_t rest = n - k - b;
+      launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
+      if (rest > 0) {
+        launch_panel_trsm(ctx, W.sub(k, k, b, b), Z.sub(k + b, k, rest, b), W.sub(k, k + b, b, rest));
+        GemmExtra e2;
+        e2.out = OutMode::Lower;
+        const DMat Wp = W.sub(k, k + b, b, rest);
+        gemm(ctx, Op::T, Op::N, -1.0, Wp, Wp, 1.0, Z.sub(k + b, k + b, rest, rest), e2);
+      }
+    }
+    const int64_t nblk = n / nb;
+    if (n % nb == 0 && (nblk & (nblk - 1)) == 0)
+      trtri_levels(ctx, W, Winv, n, nb);
+    else
+      trtri_rec(ctx, W, Winv, 0, n, nb);
+  }
   // one pivot check for the whole factorisation (a failed pivot poisons what
   // follows with NaN, which is discarded: the call throws)
   int hflag = 0;

@@ -257,22 +257,48 @@ def dist_partial_svd(be, comm, A_r, m: int, n: int, s: float = None, cut: float 
         Q2 = be.empty(n, ellw, like=A_r)
     comm.broadcast(Q2)
     Y_r = be.matmul(A_r, Q2)                                 # rows of A Q2 (unscaled A)
-    # tall-skinny CholeskyQR2 with all-reduced Grams: Y = Q R
-    G1 = comm.allreduce(be.gram(Y_r))
-    W1, W1inv = be.chol_factor_inv(G1)
-    Q1_r = be.matmul(Y_r, W1inv)
-    G2 = comm.allreduce(be.gram(Q1_r))
-    W2, W2inv = be.chol_factor_inv(G2)
-    Q_r = be.matmul(Q1_r, W2inv)
-    if comm.rank == 0:
+    # tall-skinny CholeskyQR2 with all-reduced Grams: Y = Q R.  Every rank holds
+    # the same reduced Grams, so the success test is taken identically everywhere.
+    from .qdwh import NotPositiveDefinite
+    ok = True
+    try:
+        G1 = comm.allreduce(be.gram(Y_r))
+        W1, W1inv = be.chol_factor_inv(G1)
+        d = np.abs(np.diagonal(be.to_numpy(W1)))
+        # R from the Grams perturbs sigma_i^2 by ~u*sigma_max^2: keep the Gram route
+        # only while that stays far inside the 1e-10 relative gate (kappa <~ 1e2)
+        ok = bool(d.min() > 0.0 and d.max() / d.min() <= 1e2)
+        if ok:
+            Q1_r = be.matmul(Y_r, W1inv)
+            G2 = comm.allreduce(be.gram(Q1_r))
+            W2, W2inv = be.chol_factor_inv(G2)
+            Q_r = be.matmul(Q1_r, W2inv)
+    except RuntimeError as e:  # qdwh.NotPositiveDefinite (GPU) / oracle's (CPU stand-in)
+        if type(e).__name__ != NotPositiveDefinite.__name__:
+            raise
+        ok = False
+    if not ok:
+        # ill-conditioned A Q2: Householder SVD of the gathered Y on rank 0
+        Y = comm.allgather_rows(Y_r, m)
+        if comm.rank == 0:
+            U, sig, VR = be.svd(Y)
+            sig_t = be.from_numpy(sig, like=A_r)
+        else:
+            U, VR = be.empty(m, ellw, like=A_r), be.empty(ellw, ellw, like=A_r)
+            sig_t = be.empty_vec(ellw, like=A_r)
+        for t in (U, sig_t, VR):
+            comm.broadcast(t)
+        Q_r, UR = U[r0:r1], None
+    if ok and comm.rank == 0:
         R = be.matmul(W2, W1)                                # R = W2 W1 (upper)
         UR, sig, VR = be.svd(R)
         sig_t = be.from_numpy(sig, like=A_r)
-    else:
+    elif ok:
         UR, VR = be.empty(ellw, ellw, like=A_r), be.empty(ellw, ellw, like=A_r)
         sig_t = be.empty_vec(ellw, like=A_r)
-    for t in (UR, sig_t, VR):
-        comm.broadcast(t)
+    if ok:
+        for t in (UR, sig_t, VR):
+            comm.broadcast(t)
     sig = be.to_numpy(sig_t)
     cutoff = s * alpha
     k = 0
@@ -280,7 +306,7 @@ def dist_partial_svd(be, comm, A_r, m: int, n: int, s: float = None, cut: float 
         k += 1
     res.values = sig[:k]
     if k:
-        res.u_rows = be.matmul(Q_r, UR[:, :k])
+        res.u_rows = be.matmul(Q_r, UR[:, :k]) if ok else Q_r[:, :k]
         res.v = be.matmul(Q2, VR[:, :k])
     md, nd, l = float(m), float(n), float(ellw)
     res.flops = (res.iters_qr * (6 * md * nd * nd + 8.0 / 3.0 * nd ** 3)

@@ -70,8 +70,16 @@ class Handle:
         return v.value
 
     def set_stream(self, stream_ptr: int = 0):
-        """Run on a caller CUDA stream (e.g. torch.cuda.current_stream().cuda_stream)."""
-        self.check(self.lib.qdwhg_set_stream(self.h, ctypes.c_void_p(stream_ptr or None)))
+        """Run on a caller CUDA stream (e.g. torch.cuda.current_stream().cuda_stream).
+
+        torch reports its legacy default stream as 0; that is passed as
+        cudaStreamLegacy (0x1) so the library orders itself after torch's
+        work instead of falling back to its own non-blocking stream."""
+        self.check(self.lib.qdwhg_set_stream(self.h, ctypes.c_void_p(stream_ptr or 0x1)))
+
+    def own_stream(self):
+        """Back to the handle's own (non-blocking) stream."""
+        self.check(self.lib.qdwhg_set_stream(self.h, None))
 
     def profile(self, enable: bool = True):
         """Bracket every DMMA GEMM launch with CUDA events (live kernel timing)."""
@@ -152,12 +160,18 @@ class _Mat:
 def _empty_like_kind(ref: _Mat, m: int, n: int):
     if ref.device:
         import torch
-        return torch.zeros((n, m), dtype=torch.float64, device=ref.obj.device).t()
+        out = torch.zeros((n, m), dtype=torch.float64, device=ref.obj.device).t()
+        # the zero fill (and any clone before it) is queued on torch's stream
+        torch.cuda.current_stream(out.device).synchronize()
+        return out
     return np.zeros((m, n), dtype=np.float64, order="F")
 
 
 def _ptr_ld(x):
     if _is_torch(x):
+        import torch
+        # freshly allocated / cloned buffers: order the library after torch's stream
+        torch.cuda.current_stream(x.device).synchronize()
         return x.data_ptr(), max(x.stride(1) if x.shape[1] > 1 else x.shape[0], 1)
     return x.ctypes.data, max(x.shape[0], 1)
 

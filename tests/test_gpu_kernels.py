@@ -62,6 +62,41 @@ def test_cholesky_random_spd(n):
     assert np.linalg.norm(w.T @ w - z) <= 1e-13 * n * np.linalg.norm(z)
 
 
+@pytest.mark.parametrize("n", [700, 2048])
+def test_cholesky_ill_conditioned(n):
+    """Gram of Q diag(1/i): kappa = n^2.  The stable right-looking POTRF must be
+    backward stable (no explicit-inverse multiplies), like the reference's
+    dot-product Cholesky (kernels.cpp:124-146)."""
+    q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 11 + n))
+    a = q / np.arange(1, n + 1)[None, :]
+    z = a.T @ a
+    z = 0.5 * (z + z.T)
+    w, winv = qdwh.cholesky_factor_inverse(z)
+    assert np.all(np.tril(w, -1) == 0.0) and np.all(np.diag(w) > 0)
+    assert np.linalg.norm(w.T @ w - z) <= 1e-14 * n * np.linalg.norm(z)
+    l = np.linalg.cholesky(z)
+    np.testing.assert_allclose(np.diag(w), np.diag(l), rtol=1e-8)
+
+
+def test_cholesky_torch_stream_order(cuda):
+    """Device operands produced by queued torch work (clone, zero fill) right
+    before the call must be visible to the library (stream ordering)."""
+    import torch
+    n = 1024
+    q, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device=cuda,
+                                       generator=torch.Generator(device=cuda).manual_seed(5)))
+    a = q / torch.arange(1, n + 1, dtype=torch.float64, device=cuda)[None, :]
+    z = (a.T @ a)
+    z = (0.5 * (z + z.T)).t().contiguous().t()
+    l = torch.linalg.cholesky(z)
+    for _ in range(4):
+        w, _wi = qdwh.cholesky_factor_inverse(z)
+        d = (w - l.T).abs().max().item()
+        scratch = (w - l.T) * 1e6  # garbage for the allocator to hand back next round
+        assert d <= 1e-12, d
+        del scratch
+
+
 def test_cholesky_indefinite_raises():
     z = np.eye(8)
     z[5, 5] = -1.0
