@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     for (int rl0 = 0; rl0 < BM; rl0 += 64) {
       const int rl = rl0 + 2 * lane;
       const int i = m0 + rl;
-      if (i >= p.M) continue;
+      if ((BM % 64 != 0 && rl >= BM) || i >= p.M) continue;
       double v0 = col[rl], v1 = col[rl + 1];
       if (!split) {
         v0 *= p.alpha;
@@ -525,9 +525,12 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   Be.rows += (nb_ - 1) * ex.b_step_r;
   Be.cols += (nb_ - 1) * ex.b_step_c;
 
-  // Tile choice: 128x128 when the grid fills the machine, else 64x64.
+  // Tile choice: 128x128 when the grid fills the machine, 64x64 below that,
+  // 32x32 when even 64x64 tiles would leave most SMs idle (the small GEMMs on
+  // the recursive POTRF / TRTRI critical path).
   const bool big = ((M + 127) / 128) * ((N + 127) / 128) * nb_ >= ctx.num_sms;
-  const int BMt = big ? 128 : 64;
+  const bool tiny = !big && ((M + 63) / 64) * ((N + 63) / 64) * nb_ * 2 < ctx.num_sms;
+  const int BMt = big ? 128 : tiny ? 32 : 64;
   p.tiles_m = (int)((M + BMt - 1) / BMt);
   p.tiles_n = (int)((N + BMt - 1) / BMt);
   int ntiles = (ex.out != OutMode::Full) ? p.tiles_n * (p.tiles_n + 1) / 2
@@ -552,6 +555,8 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
 
   if (big)
     dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, Ae, Be, p);
+  else if (tiny)
+    dispatch_layout<32, 32, 2, 2, 8>(ctx, ak, bkm, Ae, Be, p);
   else
     dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, Ae, Be, p);
 

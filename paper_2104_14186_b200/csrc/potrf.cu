@@ -24,26 +24,36 @@ namespace {
 constexpr int kDiagThreads = 256;
 
 // 1/sqrt(d) without the libdevice slow-path call (which forces the unrolled
-// register row to the stack): float seed + 3 Newton steps, exponent-scaled so
-// any positive double works.  Non-positive d returns NaN (the caller flags it).
+// register row to the stack): hardware double-precision estimate
+// (rsqrt.approx.f64) refined by two Newton steps.  Non-positive d returns NaN
+// (the caller flags it).
 QDWHG_DEV double rsqrt_newton(double d) {
   if (!(d > 0.0)) return __longlong_as_double(0x7ff8000000000000ll);
-  const int e = ((__double2hiint(d) >> 20) & 0x7ff) - 1023;  // d = m * 2^e, m in [1, 2)
-  const int h = e >> 1;                                       // floor(e/2)
-  const double m = __hiloint2double(__double2hiint(d) - (h << 21), __double2loint(d));  // d / 4^h
-  double y = (double)rsqrtf((float)m);
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(d));
+  const double h = 0.5 * d;
 #pragma unroll
-  for (int it = 0; it < 3; ++it) y = y * (1.5 - 0.5 * m * y * y);
-  return __hiloint2double(__double2hiint(y) - (h << 20), __double2loint(y));  // y / 2^h
+  for (int it = 0; it < 2; ++it) y = y * fma(-h * y, y, 1.5);
+  return y;
 }
+#ifdef QDWHG_DIAG_TRACE
+__device__ long long g_diag_trace[64];
+#define DIAG_MARK(i) \
+  if (threadIdx.x == 0) g_diag_trace[i] = clock64()
+#else
+#define DIAG_MARK(i)
+#endif
 constexpr int kSB = 32;          // sub-block handled by one warp
 constexpr int kLDA = 129;        // padded smem leading dimension (odd -> conflict free)
 
 // One right-looking Cholesky column step of a 32x32 block held as one row per
-// lane; template recursion guarantees compile-time register indices.
+// lane (template recursion: compile-time register indices).  The pivot comes
+// by one shuffle; the scaled column J goes to shared memory (its final place
+// in L) and every lane reads the entries it needs as broadcast loads — half
+// the instructions of shuffling each double.
 template <int J>
 struct CholStep {
-  static QDWHG_DEV void run(double (&row)[kSB], int lane, bool& bad, double& my_inv) {
+  static QDWHG_DEV void run(double (&row)[kSB], double* L, int lane, bool& bad, double& my_inv) {
     const double djj = __shfl_sync(0xffffffffu, row[J], J);
     if (!(djj > 0.0)) bad = true;
     const double inv = rsqrt_newton(djj);
@@ -52,192 +62,251 @@ struct CholStep {
       row[J] = djj * inv;
       my_inv = inv;
     }
+    if (lane >= J) L[J * kLDA + lane] = row[J];
+    __syncwarp();
+    // unpredicated: entries above a lane's diagonal pick up junk that is never
+    // read (the pivot and the written column only use entries on/below it)
 #pragma unroll
-    for (int c = J + 1; c < kSB; ++c) {
-      const double lcj = __shfl_sync(0xffffffffu, row[J], c);
-      if (lane >= c) row[c] -= row[J] * lcj;
-    }
-    CholStep<J + 1>::run(row, lane, bad, my_inv);
+    for (int c = J + 1; c < kSB; ++c) row[c] -= row[J] * L[J * kLDA + c];
+    CholStep<J + 1>::run(row, L, lane, bad, my_inv);
   }
 };
 template <>
 struct CholStep<kSB> {
-  static QDWHG_DEV void run(double (&)[kSB], int, bool&, double&) {}
+  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&) {}
 };
+
+QDWHG_DEV void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+QDWHG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
 // -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
-// all in shared memory, blocked by 32:
-//   per 32-column step: warp 0 factors + inverts the 32x32 diagonal block in
-//   registers (shuffles, no CTA barrier), the panel below is L_p = Z_p D^{-T},
-//   the trailing lower triangle gets a rank-32 update with 4x4 register tiles;
-//   then L^{-1} column block by column block: Linv_ij = -D_i^{-1} sum_k L_ik Linv_kj.
+// all in shared memory (L in place, strict upper kept zero), blocked by 32:
+//   load:    cp.async of the lower triangle (all loads in flight at once);
+//   per 32-column step kb:
+//     warp 0 factors the 32x32 diagonal block (rows in registers, columns broadcast via smem);
+//     panel rows below: forward substitution, one row per thread, the row in
+//       registers (no multiplication by an explicit inverse: u*kappa accuracy);
+//     trailing lower triangle: rank-32 update on DMMA m8n8k4 tiles;
+//   W = L^T written out;
+//   D_kb^{-1} of the four diagonal blocks in parallel (one warp each);
+//   L^{-1} in place, block columns right to left (LAPACK trtri order):
+//     L21 <- -(Linv22 L21) D11^{-1}, both products on DMMA tiles;
+//   Winv = L^{-T} written out.
 // The block is padded to a multiple of 32 with an identity (chol([Z 0;0 I]) = [L 0;0 I]).
+constexpr int kLDT = 97;  // T (R x 32, R <= 96) leading dimension
+
 __global__ void __launch_bounds__(kDiagThreads, 1)
     potrf_diag_kernel(const double* Z, int64_t ldz, double* W, int64_t ldw, double* Winv,
                       int64_t ldwi, int nb, int* flag) {
   extern __shared__ double sm[];
-  double* A = sm;                          // 128 x kLDA, column-major, lower = L
-  double* Dinv = A + 128 * kLDA;           // 4 blocks of 32 x 33 (column-major, lower)
-  double* T = Dinv + 4 * kSB * 33;         // 32 columns x kLDA: panel temp / Linv column block
-  double* S = T + kSB * kLDA;              // 32 x 33 scratch
+  double* A = sm;                    // 128 x kLDA, column-major, lower = L (then L^{-1})
+  double* Dinv = A + 128 * kLDA;     // 4 blocks of 32 x 33 (column-major, lower)
+  double* T = Dinv + 4 * kSB * 33;   // 32 columns x kLDT
+  double* Sinv = T + kSB * kLDT;     // 128: 1 / L_ii
   __shared__ int bad_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;  // DMMA fragment coordinates
   const int nbp = ((nb + kSB - 1) / kSB) * kSB;
   const int nsb = nbp / kSB;
   if (tid == 0) bad_s = 0;
+  DIAG_MARK(20);
 
-  for (int idx = tid; idx < nbp * nbp; idx += kDiagThreads) {
-    const int r = idx % nbp, c = idx / nbp;
-    double v = 0.0;
-    if (r >= c) v = (r < nb && c < nb) ? Z[r + (int64_t)c * ldz] : (r == c ? 1.0 : 0.0);
-    A[c * kLDA + r] = v;
+  // ---- load: lower triangle by cp.async, identity padding, zero strict upper
+  for (int c = warp; c < nbp; c += kDiagThreads / 32) {
+    double* col = A + c * kLDA;
+    for (int r = lane; r < nbp; r += 32) {
+      if (r >= c && r < nb && c < nb)
+        cp_async8(col + r, Z + r + (int64_t)c * ldz);
+      else
+        col[r] = (r == c) ? 1.0 : 0.0;
+    }
   }
+  cp_async_wait_all();
   __syncthreads();
+  DIAG_MARK(0);
 
   for (int kb = 0; kb < nsb; ++kb) {
     const int b0 = kb * kSB;
-    double* D = Dinv + kb * kSB * 33;
     if (warp == 0) {
       // ---- factor the 32x32 diagonal block in registers: lane i owns row i.
       // No division/sqrt library calls in here (their slow-path CALL would push
       // the unrolled register rows to the stack): pivots use rsqrt_newton.
       double row[kSB];
 #pragma unroll
-      for (int c = 0; c < kSB; ++c) row[c] = (c <= lane) ? A[(b0 + c) * kLDA + b0 + lane] : 0.0;
+      for (int c = 0; c < kSB; ++c) row[c] = A[(b0 + c) * kLDA + b0 + lane];  // strict upper is 0
       bool bad = false;
       double my_inv = 0.0;
-      CholStep<0>::run(row, lane, bad, my_inv);  // fully unrolled: registers stay registers
-#pragma unroll
-      for (int c = 0; c < kSB; ++c)
-        if (c <= lane) A[(b0 + c) * kLDA + b0 + lane] = row[c];
+      CholStep<0>::run(row, A + b0 * kLDA + b0, lane, bad, my_inv);  // writes L in place
       if (bad && lane == 0) bad_s = 1;
-      S[lane] = my_inv;  // 1 / L_ii
-      __syncwarp();
-      // ---- D^{-1}: lane j computes column j by forward substitution (registers)
-      double x[kSB];
-#pragma unroll
-      for (int i = 0; i < kSB; ++i) {
-        double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; ++k)
-          if (k >= lane) s -= A[(b0 + k) * kLDA + b0 + i] * x[k];
-        x[i] = (i >= lane) ? s * S[i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < kSB; ++i) D[lane * 33 + i] = x[i];
+      Sinv[b0 + lane] = my_inv;
     }
     __syncthreads();
+    DIAG_MARK(1 + 3 * kb);
     const int p0 = b0 + kSB, R = nbp - p0;
     if (R > 0) {
-      // ---- panel rows below the block by forward substitution (one thread per
-      // row; no multiplication by the explicit inverse, which would cost
-      // u*kappa(D)^2 accuracy on ill-conditioned blocks):
+      // ---- panel rows by forward substitution, one row per thread:
       // L(i, b0+c) = (Z(i, b0+c) - sum_{t<c} L(i, b0+t) L(b0+c, b0+t)) / L(b0+c, b0+c)
-      for (int i = tid; i < R; i += kDiagThreads) {
+      if (tid < R) {
+        const int i = p0 + tid;
+        double x[kSB];
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) x[c] = A[(b0 + c) * kLDA + i];
+#pragma unroll
         for (int c = 0; c < kSB; ++c) {
-          double s = A[(b0 + c) * kLDA + p0 + i];
-          for (int t = 0; t < c; ++t) s -= A[(b0 + t) * kLDA + p0 + i] * A[(b0 + t) * kLDA + b0 + c];
-          A[(b0 + c) * kLDA + p0 + i] = s * S[c];
+          double s0 = x[c], s1 = 0.0;  // two chains: half the FMA latency
+#pragma unroll
+          for (int t = 0; t < c; ++t) {
+            const double l = A[(b0 + t) * kLDA + b0 + c];  // broadcast
+            if (t & 1) s1 -= x[t] * l;
+            else s0 -= x[t] * l;
+          }
+          x[c] = (s0 + s1) * Sinv[b0 + c];
         }
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) A[(b0 + c) * kLDA + i] = x[c];
       }
       __syncthreads();
-      // ---- trailing rank-32 update of the lower triangle, 4x4 register tiles
-      const int tr = R / 4;
-      const int ntiles = tr * (tr + 1) / 2;
-      for (int t = tid; t < ntiles; t += kDiagThreads) {
-        int tj = 0, rem = t;
-        while (rem >= tr - tj) {
-          rem -= tr - tj;
-          ++tj;
+      DIAG_MARK(2 + 3 * kb);
+      // ---- trailing rank-32 update of the lower triangle on 8x8 DMMA tiles:
+      // A(i, j) -= sum_t L(i, b0+t) L(j, b0+t),  i >= j >= p0.  A work unit is
+      // one row tile x up to 4 column tiles (4 independent accumulator chains).
+      const int nt = R / 8;
+      int nunits = 0;
+      for (int ti = 0; ti < nt; ++ti) nunits += ti / 4 + 1;
+      for (int u = warp; u < nunits; u += kDiagThreads / 32) {
+        int ti = 0, rem = u;
+        while (rem >= ti / 4 + 1) {
+          rem -= ti / 4 + 1;
+          ++ti;
         }
-        const int ti = tj + rem;
-        const int i0 = p0 + 4 * ti, j0 = p0 + 4 * tj;
-        double acc[4][4];
+        const int tj0 = 4 * rem;
+        const int i0 = p0 + 8 * ti;
+        double c[4][2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-        for (int c = 0; c < kSB; ++c) {
-          const double* col = A + (b0 + c) * kLDA;
-          double li[4], lj[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            li[a] = col[i0 + a];
-            lj[a] = col[j0 + a];
-          }
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] += li[a] * lj[b];
+        for (int v = 0; v < 4; ++v) {
+          const int j0 = p0 + 8 * min(tj0 + v, ti);
+          c[v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
+          c[v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
         }
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int k4 = 0; k4 < kSB / 4; ++k4) {
+          const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
+          const double a = -lc[i0 + g];
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (i0 + a >= j0 + b) A[(j0 + b) * kLDA + i0 + a] -= acc[a][b];
+          for (int v = 0; v < 4; ++v)
+            dmma_8x8x4(c[v][0], c[v][1], a, lc[p0 + 8 * min(tj0 + v, ti) + g]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int tj = tj0 + v;
+          if (tj > ti) break;
+          const int j0 = p0 + 8 * tj;
+          if (tj != ti || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[v][0];
+          if (tj != ti || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[v][1];
+        }
       }
       __syncthreads();
     }
+    DIAG_MARK(3 + 3 * kb);
   }
   if (tid == 0 && bad_s) atomicExch(flag, 1);
 
   // ---- W = L^T (upper) with explicit zeros below
-  for (int idx = tid; idx < nb * nb; idx += kDiagThreads) {
-    const int r = idx % nb, c = idx / nb;
-    W[r + (int64_t)c * ldw] = (r <= c) ? A[r * kLDA + c] : 0.0;
+  for (int c = warp; c < nb; c += kDiagThreads / 32) {
+    double* wc = W + (int64_t)c * ldw;
+#pragma unroll 4
+    for (int r = lane; r < nb; r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
   }
+  DIAG_MARK(13);
 
-  // ---- L^{-1} by 32-column blocks; Winv = L^{-T}
-  for (int jb = 0; jb < nsb; ++jb) {
-    const int c0 = jb * kSB;
-    for (int idx = tid; idx < kSB * nbp; idx += kDiagThreads) {
-      const int r = idx % nbp, c = idx / nbp;
-      double v = 0.0;
-      if (r >= c0 && r < c0 + kSB) v = Dinv[jb * kSB * 33 + c * 33 + (r - c0)];
-      T[c * kLDA + r] = v;
-    }
-    __syncthreads();
-    for (int ib = jb + 1; ib < nsb; ++ib) {
-      const int r0 = ib * kSB;
-      // S = sum_{k in [c0, r0)} L(r0 + r, k) * Linv(k, c0 + c)
-      {
-        const int r = tid & 31, cb = tid >> 5;  // columns cb + 8q
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k = c0; k < r0; ++k) {
-          const double a = A[k * kLDA + r0 + r];
+  // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each:
+  // lane j computes column j by forward substitution in registers
+  if (warp < nsb) {
+    const int b0 = warp * kSB;
+    double x[kSB];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] += a * T[(cb + 8 * q) * kLDA + k];
+    for (int i = 0; i < kSB; ++i) {
+      double s[4] = {(i == lane) ? 1.0 : 0.0, 0.0, 0.0, 0.0};  // 4 chains
+#pragma unroll
+      for (int k = 0; k < i; ++k) {
+        const double l = A[(b0 + k) * kLDA + b0 + i];  // broadcast
+        s[k & 3] -= l * x[k];  // x[k] == 0 for k < lane: no predicate needed
+      }
+      x[i] = (i >= lane) ? ((s[0] + s[1]) + (s[2] + s[3])) * Sinv[b0 + i] : 0.0;
+    }
+    double* D = Dinv + warp * kSB * 33;
+#pragma unroll
+    for (int i = 0; i < kSB; ++i) D[lane * 33 + i] = x[i];
+  }
+  __syncthreads();
+  DIAG_MARK(14);
+
+  // ---- L^{-1} in place, block columns right to left
+  for (int jb = nsb - 1; jb >= 0; --jb) {
+    const int b0 = jb * kSB, p0 = b0 + kSB, R = nbp - p0;
+    const double* D = Dinv + jb * kSB * 33;
+    if (R > 0) {
+      // T = Linv22 * L21   (R x 32; Linv22 lower: k-tiles up to the diagonal).
+      // Unit = one row tile x the 4 column tiles; heaviest row tiles first.
+      const int nt = R / 8;
+      for (int u = warp; u < nt; u += kDiagThreads / 32) {
+        const int ti = nt - 1 - u;
+        double c[4][2] = {};
+        for (int k4 = 0; k4 < 2 * (ti + 1); ++k4) {
+          const int k = p0 + 4 * k4 + q;
+          const double a = A[k * kLDA + p0 + 8 * ti + g];
+#pragma unroll
+          for (int tj = 0; tj < 4; ++tj)
+            dmma_8x8x4(c[tj][0], c[tj][1], a, A[(b0 + 8 * tj + g) * kLDA + k]);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) S[(cb + 8 * q) * 33 + r] = acc[q];
+        for (int tj = 0; tj < 4; ++tj) {
+          T[(8 * tj + 2 * q) * kLDT + 8 * ti + g] = c[tj][0];
+          T[(8 * tj + 2 * q + 1) * kLDT + 8 * ti + g] = c[tj][1];
+        }
       }
       __syncthreads();
-      const double* Di = Dinv + ib * kSB * 33;
-      {
-        const int r = tid & 31, cb = tid >> 5;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int t = 0; t <= r; ++t) {
-          const double d = Di[t * 33 + r];
+      // L21 <- -T * D^{-1}   (D lower with explicit zeros: full K)
+      for (int u = warp; u < nt; u += kDiagThreads / 32) {
+        const int ti = u;
+        double c[4][2] = {};
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] += d * S[(cb + 8 * q) * 33 + t];
+        for (int k4 = 0; k4 < 8; ++k4) {
+          const int k = 4 * k4 + q;
+          const double a = -T[k * kLDT + 8 * ti + g];
+#pragma unroll
+          for (int tj = 0; tj < 4; ++tj) dmma_8x8x4(c[tj][0], c[tj][1], a, D[(8 * tj + g) * 33 + k]);
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) T[(cb + 8 * q) * kLDA + r0 + r] = -acc[q];
+        for (int tj = 0; tj < 4; ++tj) {
+          A[(b0 + 8 * tj + 2 * q) * kLDA + p0 + 8 * ti + g] = c[tj][0];
+          A[(b0 + 8 * tj + 2 * q + 1) * kLDA + p0 + 8 * ti + g] = c[tj][1];
+        }
       }
-      __syncthreads();
     }
-    // Winv(c0 + c, row) = Linv(row, c0 + c)
-    for (int idx = tid; idx < kSB * nb; idx += kDiagThreads) {
-      const int c = idx & 31, row = idx >> 5;
-      if (c0 + c < nb) Winv[(c0 + c) + (int64_t)row * ldwi] = (row >= c0 + c) ? T[c * kLDA + row] : 0.0;
+    // diagonal block <- D^{-1} (lower; the strict upper stays zero)
+    for (int idx = tid; idx < kSB * kSB; idx += kDiagThreads) {
+      const int r = idx & 31, c = idx >> 5;
+      if (r >= c) A[(b0 + c) * kLDA + b0 + r] = D[c * 33 + r];
     }
     __syncthreads();
   }
+  DIAG_MARK(15);
+
+  // ---- Winv = L^{-T} (upper) with explicit zeros below
+  for (int c = warp; c < nb; c += kDiagThreads / 32) {
+    double* wc = Winv + (int64_t)c * ldwi;
+#pragma unroll 4
+    for (int r = lane; r < nb; r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+  }
+  DIAG_MARK(16);
 }
 
 void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk) {
-  const size_t smem = (size_t)(128 * kLDA + 4 * kSB * 33 + kSB * kLDA + kSB * 33) * 8;
+  const size_t smem = (size_t)(128 * kLDA + 4 * kSB * 33 + kSB * kLDT + 128) * 8;
   static bool set = false;
   if (!set) {
     QDWHG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,0 +1,70 @@
+// Microbenchmark of the POTRF leaf kernel (potrf_diag_kernel) with per-phase
+// clock64 marks.  Build: make -C tools/bench_src diag_bench
+#define QDWHG_DIAG_TRACE 1
+#include "../../paper_2104_14186_b200/csrc/potrf.cu"
+
+#include <cstdio>
+#include <vector>
+
+using namespace qdwhg;
+
+int main() {
+  const int nb = 128;
+  const int64_t ld = 128;
+  std::vector<double> h(ld * nb);
+  // SPD: Z = I*nb + small symmetric
+  for (int j = 0; j < nb; ++j)
+    for (int i = 0; i < nb; ++i) h[i + j * ld] = (i == j ? nb : 0.0) + 1.0 / (1.0 + i + j);
+  double *Z, *W, *Wi;
+  int* flag;
+  cudaMalloc(&Z, 8 * ld * nb);
+  cudaMalloc(&W, 8 * ld * nb);
+  cudaMalloc(&Wi, 8 * ld * nb);
+  cudaMalloc(&flag, 4);
+  cudaMemset(flag, 0, 4);
+  cudaMemcpy(Z, h.data(), 8 * ld * nb, cudaMemcpyHostToDevice);
+  Ctx ctx;
+  ctx.dflag = flag;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int it = 0; it < 5; ++it) launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
+  cudaEventRecord(e0);
+  const int reps = 50;
+  for (int it = 0; it < reps; ++it) launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("potrf_diag nb=%d: %.2f us/launch (%s)\n", nb, 1e3 * ms / reps, cudaGetErrorString(cudaGetLastError()));
+  long long t[64];
+  cudaMemcpyFromSymbol(t, g_diag_trace, sizeof(t));
+  const char* names[21] = {"load", "kb0 chol+Dinv", "kb0 panel", "kb0 trail", "kb1 chol+Dinv", "kb1 panel",
+                           "kb1 trail", "kb2 chol+Dinv", "kb2 panel", "kb2 trail", "kb3 chol+Dinv",
+                           "kb3 panel", "kb3 trail", "W write", "D^-1 blocks", "L^-1 in place", "Winv write",
+                           "", "", "", "start"};
+  long long prev = t[20];
+  for (int i = 0; i <= 16; ++i) {
+    if (i == 11 || i == 12) continue;  // no panel / trailing update in the last block
+    printf("  %-16s %8lld cycles\n", names[i], t[i] - prev);
+    prev = t[i];
+  }
+  printf("  total %lld cycles\n", t[16] - t[20]);
+  // check: W^T W == Z
+  std::vector<double> w(ld * nb), wi(ld * nb);
+  cudaMemcpy(w.data(), W, 8 * ld * nb, cudaMemcpyDeviceToHost);
+  cudaMemcpy(wi.data(), Wi, 8 * ld * nb, cudaMemcpyDeviceToHost);
+  double e = 0, ei = 0;
+  for (int j = 0; j < nb; ++j)
+    for (int i = 0; i < nb; ++i) {
+      double s = 0, si = 0;
+      for (int k = 0; k < nb; ++k) {
+        s += w[k + i * ld] * w[k + j * ld];
+        si += w[i + k * ld] * wi[k + j * ld];
+      }
+      e = std::max(e, std::abs(s - h[i + j * ld]));
+      ei = std::max(ei, std::abs(si - (i == j)));
+    }
+  printf("  max|W^T W - Z| %.3e  max|W Winv - I| %.3e\n", e, ei);
+  return 0;
+}
