@@ -28,6 +28,12 @@ QDWHG_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---------------------------------------------------------------- cp.async
+QDWHG_DEV void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+QDWHG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 QDWHG_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
@@ -58,6 +64,37 @@ QDWHG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Cluster-scope acquire wait (data delivered by peers' st.async).
+QDWHG_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------- DSMEM
+// Address of the same shared-memory location in CTA `rank` of the cluster.
+QDWHG_DEV uint32_t mapa_u32(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+// 16-byte asynchronous store into a peer CTA's shared memory that completes
+// 16 transaction bytes on the peer's mbarrier (no cluster barrier needed).
+QDWHG_DEV void st_async_v2(uint32_t remote_addr, double x, double y, uint32_t remote_mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+          remote_addr),
+      "d"(x), "d"(y), "r"(remote_mbar)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 QDWHG_DEV void tma_prefetch_desc(const void* desc) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(desc)) : "memory");
@@ -72,6 +109,27 @@ QDWHG_DEV void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int 
 }
 
 // ---------------------------------------------------------------- reductions
+// Latency-lean reciprocal / square root for scalar critical paths (panel
+// pivots): hardware f64 estimates + Newton steps, ~1 ulp (not correctly rounded,
+// no library slow path).  x must be finite and nonzero (sqrt: positive).
+QDWHG_DEV double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+QDWHG_DEV double fast_sqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  r = r * fma(-h * r, r, 1.5);
+  r = r * fma(-h * r, r, 1.5);
+  const double s = x * r;
+  return fma(0.5 * r, fma(-s, s, x), s);  // one residual correction
+}
+
 QDWHG_DEV double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -26,6 +26,14 @@ namespace qdwhg {
 
 namespace {
 
+#ifdef QDWHG_PANEL_TRACE
+__device__ long long g_panel_trace[16];
+#define PANEL_MARK(i, col) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (col) == 10) g_panel_trace[i] = clock64()
+#else
+#define PANEL_MARK(i, col)
+#endif
+
 constexpr int kPanelThreads = 256;
 constexpr int kBW = 64;  // max panel width (one thread column per panel column)
 
@@ -118,7 +126,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
   // visible in `tot`
   auto reduce = [&](int col) {
     double* mine = part + (col & 1) * (2 * kBW);
+    PANEL_MARK(3, col);
     panel_partials(S, RP, nr, rbeg, b, col, red, mine);
+    PANEL_MARK(4, col);
     if (CLUSTER) {
       cg::cluster_group cluster = cg::this_cluster();
       cluster.sync();
@@ -140,7 +150,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         const int cc = threadIdx.x % kBW;
         if (cc < b && cc >= col && mine[threadIdx.x] != 0.0) atomicAdd(&buf[threadIdx.x], mine[threadIdx.x]);
       }
+      PANEL_MARK(5, col);
       grid_barrier(bar, gridDim.x, epoch);
+      PANEL_MARK(6, col);
       if (threadIdx.x < 2 * kBW) tot[threadIdx.x] = __ldcg(&buf[threadIdx.x]);
       if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
         double* z = acc + ((col + 2) % 3) * (2 * kBW);
@@ -148,10 +160,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       }
       __syncthreads();
     }
+    PANEL_MARK(7, col);
   };
 
   reduce(0);
   for (int jj = 0; jj < b; ++jj) {
+    PANEL_MARK(0, jj);
     const double x0 = tot[jj];
     const double sig2 = tot[kBW + jj];
     const double normx = sqrt(x0 * x0 + sig2);
@@ -170,6 +184,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       coef[cc] = w;
     }
     __syncthreads();
+    PANEL_MARK(1, jj);
     // apply H_jj to this CTA's rows; column jj -> v' (to V), R_jj
     if (c < b) {
       const double* sj = S + jj * RP;
@@ -201,6 +216,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       if (rl >= 0 && rl < nr) S[jj * RP + rl] = beta;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) tau_out[jj] = taup;
+    PANEL_MARK(2, jj);
     if (jj + 1 < b) reduce(jj + 1);
   }
   if (CLUSTER) cg::this_cluster().sync();  // peers may still read our partials
@@ -211,6 +227,263 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       const int rgl = rbeg + r;
       A[rgl + cc * lda] = (rgl <= cc) ? S[cc * RP + r] : 0.0;
     }
+}
+
+// Register-resident panel factorization (the default for panels up to
+// 148 * 256 rows): thread (c, rg) — c = tid % 64 the panel column, rg = tid / 64
+// the row group — keeps column c of rows rg + NRG*t (t < RPT) of its CTA's row
+// block in registers for the whole panel.  Per column jj there is ONE pass over
+// the registers that applies H_jj to the thread's column AND accumulates the
+// partial sums of column jj+1 (x0, sigma^2, v^T a_c) from column jj+1's updated
+// values, which every thread recomputes from a shared-memory snapshot
+// (bit-identical to the owner's update: same inputs, same fma).  Then one
+// in-CTA combine and one cross-CTA reduction (cluster DSMEM or grid atomics),
+// i.e. two CTA barriers + one cluster/grid barrier per column.
+template <bool CLUSTER, int NRG, int RPT>
+__global__ void __launch_bounds__(64 * NRG, 1)
+    geqr2_panel_reg_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
+                           int b, int rpc, double* acc, unsigned* bar) {
+  constexpr int NT = kBW * NRG;
+  constexpr int RB = NRG * RPT;  // row capacity per CTA (>= rpc)
+  constexpr int RBP = RB + 1;
+  extern __shared__ double smem[];
+  double* stage = smem;                 // [kBW][RBP]: coalesced load / store staging
+  double* snap = stage + kBW * RBP;     // [2 parity][2: column jj, column jj+1][RB]
+  double* red = snap + 4 * RB;          // [NRG][2*kBW]
+  double* part = red + NRG * 2 * kBW;   // [2 parity][2*kBW] this CTA's partials
+  double* tot = part + 4 * kBW;         // [2*kBW] reduced (top | below)
+  double* gbuf = tot + 2 * kBW;         // CLUSTER: [2 parity][16 ranks][2*kBW] pushed partials
+  double* colsc = gbuf + 2 * 16 * 2 * kBW;  // [kBW] 1/v0 (0: no reflector) | [kBW] beta, per column
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(colsc + 2 * kBW);  // CLUSTER: [2] gather barriers
+  const int tid = threadIdx.x;
+  const int c = tid % kBW, rg = tid / kBW;
+  const int rbeg = blockIdx.x * rpc;
+  const int nr = max(0, min(rpc, mp - rbeg));
+  unsigned epoch = 0;
+  namespace cg = cooperative_groups;
+
+  // ---- coalesced load through shared memory, then into registers
+  for (int cc = 0; cc < b; ++cc)  // cp.async: every element in flight at once
+    for (int i = tid; i < nr; i += NT) cp_async8(stage + cc * RBP + i, A + (rbeg + i) + (int64_t)cc * lda);
+  cp_async_wait_all();
+  __syncthreads();
+  double a[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = rg + NRG * t;
+    a[t] = (c < b && i < nr) ? stage[c * RBP + i] : 0.0;  // rows past nr stay exactly 0
+    if (c == 0) snap[i] = a[t];
+    if (c == 1) snap[RB + i] = a[t];
+  }
+  for (int i = tid; i < 2 * RB; i += NT) snap[2 * RB + i] = 0.0;
+  if (CLUSTER) {
+    // gather barriers: column col's partials from all ranks land in
+    // gbuf[col & 1] via st.async, completing tx bytes on mbar[col & 1]
+    if (tid == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      fence_barrier_init();
+    }
+    cg::this_cluster().sync();
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)cg::this_cluster().num_blocks() * 2 * kBW * 8;
+      mbar_arrive_expect_tx(&mbar[0], bytes);
+      if (b > 1) mbar_arrive_expect_tx(&mbar[1], bytes);
+    }
+  }
+  __syncthreads();
+
+  // cross-CTA sum of the per-row-group partials in `red` -> tot
+  auto reduce = [&](int col) {
+    double* mine = part + (col & 1) * (2 * kBW);
+    if (tid < 2 * kBW) {
+      double s = 0.0;
+#pragma unroll
+      for (int g = 0; g < NRG; ++g) s += red[g * 2 * kBW + tid];
+      mine[tid] = s;
+    }
+    if (CLUSTER) {
+      // all-gather by st.async: this CTA's vector goes into slot [my rank] of
+      // every peer, each store completing bytes on the peer's mbar[col & 1];
+      // the local wait then sums the slots in fixed rank order (deterministic)
+      cg::cluster_group cluster = cg::this_cluster();
+      const int nb_ = (int)cluster.num_blocks();
+      const int me = (int)cluster.block_rank();
+      const int q = col & 1;
+      double* g = gbuf + q * (16 * 2 * kBW);
+      __syncthreads();  // `mine` complete
+      if (tid < kBW) {
+        const uint32_t src = smem_u32(g + me * (2 * kBW) + 2 * tid);
+        const uint32_t mb = smem_u32(&mbar[q]);
+        const double x = mine[2 * tid], y = mine[2 * tid + 1];
+        for (int p = 0; p < nb_; ++p) st_async_v2(mapa_u32(src, p), x, y, mapa_u32(mb, p));
+      }
+      if (tid < 2 * kBW) {
+        mbar_wait_cluster(&mbar[q], (col >> 1) & 1);
+        double s = 0.0;
+        for (int p = 0; p < nb_; ++p) s += g[p * 2 * kBW + tid];
+        tot[tid] = s;
+        // re-arm for column col + 2 by a thread that sent nothing (a sender's
+        // release-arrive would wait for its own remote stores to land)
+        if (tid == kBW && col + 2 < b) mbar_arrive_expect_tx(&mbar[q], (uint32_t)nb_ * 2 * kBW * 8);
+      }
+      __syncthreads();
+    } else {
+      double* buf = acc + (col % 3) * (2 * kBW);
+      if (tid < 2 * kBW) {
+        const int cc = tid % kBW;
+        if (cc < b && cc >= col && mine[tid] != 0.0) atomicAdd(&buf[tid], mine[tid]);
+      }
+      grid_barrier(bar, gridDim.x, epoch);
+      if (tid < 2 * kBW) tot[tid] = __ldcg(&buf[tid]);
+      if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
+        double* z = acc + ((col + 2) % 3) * (2 * kBW);
+        if (tid < 2 * kBW) z[tid] = 0.0;
+      }
+      __syncthreads();
+    }
+  };
+
+  // partials of column 0
+  {
+    double top = 0.0, below = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = rg + NRG * t, gr = rbeg + i;
+      if (i < nr && c < b) {
+        if (gr == 0) top = a[t];
+        else below = fma(snap[i], a[t], below);
+      }
+    }
+    red[rg * 2 * kBW + c] = top;
+    red[rg * 2 * kBW + kBW + c] = below;
+    __syncthreads();
+    reduce(0);
+  }
+
+  // Snapshot conventions (shared memory, per parity):
+  //   U = column jj with 0 above row jj (its row-jj entry becomes v0 at step jj),
+  //       so u = v0 * v and a_c -= s_c u is the complete H_jj update of any row;
+  //   P = column jj+1 (raw); its updated value pv is recomputed by every thread
+  //       (same fma as its owner's) for the partial sums of column jj+1.
+  // The pivot column itself is left raw (s_jj = 0) and normalised at the end
+  // (v = a / v0 below the diagonal, beta on it), from per-column scalars.
+  for (int jj = 0; jj < b; ++jj) {
+    PANEL_MARK(8, jj);
+    const int par = jj & 1;
+    double* U = snap + par * 2 * RB;
+    const double* P = U + RB;
+    double* Un = snap + (par ^ 1) * 2 * RB;
+    double* Pn = Un + RB;
+    const double x0 = tot[jj];
+    const double sig2 = tot[kBW + jj];
+    const double nx2 = x0 * x0 + sig2;
+    const bool reflect = (jj < mp - 1) && nx2 > 0.0;
+    double beta = x0, v0 = 1.0, taup = 0.0, inv_v0 = 1.0;
+    if (reflect) {
+      const double normx = fast_sqrt(nx2);
+      beta = x0 >= 0.0 ? -normx : normx;
+      v0 = x0 - beta;
+      taup = (beta - x0) * fast_rcp(beta);
+      inv_v0 = fast_rcp(v0);
+    }
+    // w_c = tau' v^T a_c  (v = [1; x_below / v0]);  s_c = w_c / v0 scales u = v0 v
+    double sc = 0.0, s1 = 0.0;
+    if (reflect && c > jj && c < b) sc = taup * (tot[c] + tot[kBW + c] * inv_v0) * inv_v0;
+    if (reflect && jj + 1 < b) s1 = taup * (tot[jj + 1] + tot[kBW + jj + 1] * inv_v0) * inv_v0;
+    if (tid == 0) {
+      colsc[jj] = reflect ? inv_v0 : 0.0;
+      colsc[kBW + jj] = beta;
+      if (jj >= rbeg && jj < rbeg + nr) U[jj - rbeg] = v0;
+    }
+    if (blockIdx.x == 0 && tid == 0) tau_out[jj] = taup;
+    __syncthreads();
+    PANEL_MARK(9, jj);
+    double top = 0.0, below = 0.0;
+    const int kmask = jj + 1 - rbeg - rg;  // element t has row <= jj+1 iff NRG*t <= kmask
+    if ((tid % kBW) / 32 * 32 + 31 > jj) {  // warps with a column right of the pivot
+      if (kmask < 0) {
+        double bl[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains: FP64 latency, not throughput
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          const int i = rg + NRG * t;
+          const double u = U[i];
+          const double pv = fma(-s1, u, P[i]);
+          const double an = fma(-sc, u, a[t]);
+          a[t] = an;
+          bl[t & 3] = fma(pv, an, bl[t & 3]);
+        }
+        below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
+      } else {
+        double bl[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          const int i = rg + NRG * t;
+          const double u = U[i];
+          const double pv = fma(-s1, u, P[i]);
+          const double an = fma(-sc, u, a[t]);
+          a[t] = an;
+          bl[t & 3] = (NRG * t > kmask) ? fma(pv, an, bl[t & 3]) : bl[t & 3];
+        }
+        below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
+        if (kmask % NRG == 0) {
+#pragma unroll
+          for (int t = 0; t < RPT; ++t)
+            if (NRG * t == kmask) top = a[t];  // row jj+1
+        }
+      }
+    }
+    PANEL_MARK(10, jj);
+    if (!((jj + 1 < b) && c < b && c > jj)) top = below = 0.0;
+    // snapshots of columns jj+1 (zero above its diagonal) and jj+2 (owners only)
+    if (c == jj + 1) {
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) Un[rg + NRG * t] = (NRG * t < kmask) ? 0.0 : a[t];
+    } else if (c == jj + 2) {
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) Pn[rg + NRG * t] = a[t];
+    }
+    if (jj + 1 < b) {
+      red[rg * 2 * kBW + c] = top;
+      red[rg * 2 * kBW + kBW + c] = below;
+      PANEL_MARK(11, jj);
+      __syncthreads();
+      PANEL_MARK(12, jj);
+      reduce(jj + 1);
+      PANEL_MARK(13, jj);
+    }
+  }
+  if (CLUSTER) cg::this_cluster().sync();  // peers may still write into our buffers
+  __syncthreads();
+  // ---- pivot columns: v = a / v0 below the diagonal, beta on it; then R (upper,
+  // zeros below) and V (zeros above, unit diagonal) through staging
+  if (c < b) {
+    const double iv = colsc[c], bt = colsc[kBW + c];
+#pragma unroll
+    for (int t = 0; t < RPT; ++t) {
+      const int i = rg + NRG * t, gr = rbeg + i;
+      double x = a[t];
+      if (gr == c) x = bt;
+      else if (gr > c) x *= iv;
+      if (i < nr) stage[c * RBP + i] = x;
+    }
+  }
+  __syncthreads();
+  for (int cc = 0; cc < b; ++cc)
+    for (int i = tid; i < nr; i += NT) {
+      const int gr = rbeg + i;
+      const double x = stage[cc * RBP + i];
+      A[gr + (int64_t)cc * lda] = (gr <= cc) ? x : 0.0;
+      V[gr + (int64_t)cc * ldv] = (gr < cc) ? 0.0 : (gr == cc ? 1.0 : x);
+    }
+}
+
+template <int NRG, int RPT>
+size_t panel_reg_smem() {
+  constexpr int RB = NRG * RPT;
+  return ((size_t)kBW * (RB + 1) + 4 * RB + NRG * 2 * kBW + 4 * kBW + 2 * kBW + 2 * 16 * 2 * kBW +
+          2 * kBW + 2) *
+         8;
 }
 
 // T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise),
@@ -297,8 +570,127 @@ int cluster_size_limit() {
   return cs;
 }
 
+// Largest cluster the register-resident panel kernel can use (16 non-portable, else 8).
+int reg_cluster_limit() {
+  static int cs = -1;
+  if (cs < 0) {
+    cs = 8;
+    auto kern = geqr2_panel_reg_kernel<true, 8, 32>;
+    const size_t smem = panel_reg_smem<8, 32>();
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+            cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at;
+      at.id = cudaLaunchAttributeClusterDimension;
+      at.val.clusterDim.x = 16;
+      at.val.clusterDim.y = 1;
+      at.val.clusterDim.z = 1;
+      cfg.attrs = &at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) cs = 16;
+    }
+    cudaGetLastError();
+  }
+  return cs;
+}
+
+template <bool CL, int RPT, int NRG = 8>
+void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr, int64_t ldv,
+                      double* tau_dev, int mp, int b, int rpc, double* acc, unsigned* bar) {
+  auto kern = geqr2_panel_reg_kernel<CL, NRG, RPT>;
+  const size_t smem = panel_reg_smem<NRG, RPT>();
+  static bool set = false;
+  if (!set) {
+    QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (CL) QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    set = true;
+  }
+  if (CL) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblk);
+    cfg.blockDim = dim3(64 * NRG);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx.stream;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = nblk;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    QDWHG_CUDA(cudaLaunchKernelEx(&cfg, kern, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar));
+  } else {
+    QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
+    QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+    void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, &mp, &b, &rpc, &acc, &bar};
+    QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(64 * NRG), args, smem,
+                                           ctx.stream));
+  }
+  ctx.count();
+}
+
+// Register-resident panel when the panel fits (cluster of <= 16 CTAs x 256
+// rows, or a cooperative grid of <= #SMs CTAs x 256 rows); false otherwise.
+bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
+                      unsigned* bar) {
+  static const bool disabled = getenv("QDWHG_PANEL_SMEM") != nullptr;
+  if (disabled) return false;
+  const int mp = (int)P.rows, b = (int)P.cols;
+  double* Ap = P.ptr();
+  const int64_t lda = P.ld;
+  double* Vptr = Vp.ptr();
+  const int64_t ldv = Vp.ld;
+  const int csmax = reg_cluster_limit();
+  auto ceil_div = [](int x, int y) { return (x + y - 1) / y; };
+  // cluster (deterministic DSMEM reduction, hardware barrier)
+  if (ceil_div(mp, 8 * 4) <= csmax) {
+    const int cs = ceil_div(mp, 8 * 4), rpc = ceil_div(mp, cs);
+    launch_panel_reg<true, 4>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  if (ceil_div(mp, 8 * 8) <= csmax) {
+    const int cs = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, cs);
+    launch_panel_reg<true, 8>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  if (ceil_div(mp, 8 * 16) <= csmax) {
+    const int cs = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, cs);
+    launch_panel_reg<true, 16>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  if (ceil_div(mp, 8 * 32) <= csmax) {
+    const int cs = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, cs);
+    launch_panel_reg<true, 32>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  // cooperative grid (FP64 atomics + grid barrier)
+  if (ceil_div(mp, 8 * 8) <= ctx.num_sms) {
+    const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
+    launch_panel_reg<false, 8>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  if (ceil_div(mp, 8 * 16) <= ctx.num_sms) {
+    const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
+    launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  if (ceil_div(mp, 8 * 32) <= ctx.num_sms) {
+    const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
+    launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    return true;
+  }
+  return false;
+}
+
 void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
                   unsigned* bar) {
+  if (panel_factor_reg(ctx, P, Vp, tau_dev, acc, bar)) return;
+  // shared-memory panel kernel: panels taller than the register path covers
   int mp = (int)P.rows, b = (int)P.cols;
   static bool set = false;
   if (!set) {

@@ -76,10 +76,6 @@ struct CholStep<kSB> {
   static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&) {}
 };
 
-QDWHG_DEV void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-QDWHG_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
 // -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
