@@ -108,6 +108,30 @@ QDWHG_DEV void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int 
       : "memory");
 }
 
+// ---------------------------------------------------------------- grid barrier
+QDWHG_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+QDWHG_DEV void red_release_add_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// Monotonic grid barrier for cooperative launches (counter zeroed before the
+// launch, all CTAs co-resident).  bar.sync orders the CTA's prior writes before
+// thread 0's gpu-scope release (cumulativity); the acquire poll orders what follows.
+QDWHG_DEV void grid_sync(unsigned* bar, unsigned& epoch) {
+  __syncthreads();
+  ++epoch;
+  if (threadIdx.x == 0) {
+    red_release_add_gpu(bar, 1u);
+    const unsigned target = epoch * gridDim.x;
+    while (ld_acquire_gpu(bar) < target) {
+    }
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- reductions
 // Latency-lean reciprocal / square root for scalar critical paths (panel
 // pivots): hardware f64 estimates + Newton steps, ~1 ulp (not correctly rounded,

@@ -96,7 +96,8 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   gemm(ctx, Op::T, Op::N, w.c, X, X, 0.0, Z, syrk);
   try {
     // kappa(Z) <= 1 + c: the fast recursive Cholesky-and-inverse is accurate here
-    potrf_upper_and_inverse(ctx, Z, Winv, false, false);
+    static const bool stable_env = getenv("QDWHG_CHOL_STABLE") != nullptr;
+    potrf_upper_and_inverse(ctx, Z, Winv, false, stable_env);
   } catch (...) {
     ctx.arena->release_to(mark);
     throw;

@@ -37,29 +37,6 @@ __device__ long long g_panel_trace[16];
 constexpr int kPanelThreads = 256;
 constexpr int kBW = 64;  // max panel width (one thread column per panel column)
 
-QDWHG_DEV unsigned ld_acquire(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-QDWHG_DEV void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-// Monotonic grid barrier (counter zeroed before launch; all CTAs co-resident
-// via cooperative launch).
-QDWHG_DEV void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
-  __syncthreads();
-  ++epoch;
-  if (threadIdx.x == 0) {
-    // bar.sync orders the CTA's prior writes/atomics before thread 0's
-    // gpu-scope release (cumulativity); acquire on the poll orders what follows.
-    red_release_add(bar, 1u);
-    const unsigned target = epoch * nblocks;
-    while (ld_acquire(bar) < target) {
-    }
-  }
-  __syncthreads();
-}
 
 // Partial sums for pivot column `col` over this CTA's rows:
 //   top[c]  = A(col, c)                       (row owner only)
@@ -151,7 +128,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         if (cc < b && cc >= col && mine[threadIdx.x] != 0.0) atomicAdd(&buf[threadIdx.x], mine[threadIdx.x]);
       }
       PANEL_MARK(5, col);
-      grid_barrier(bar, gridDim.x, epoch);
+      grid_sync(bar, epoch);
       PANEL_MARK(6, col);
       if (threadIdx.x < 2 * kBW) tot[threadIdx.x] = __ldcg(&buf[threadIdx.x]);
       if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
@@ -334,7 +311,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
         const int cc = tid % kBW;
         if (cc < b && cc >= col && mine[tid] != 0.0) atomicAdd(&buf[tid], mine[tid]);
       }
-      grid_barrier(bar, gridDim.x, epoch);
+      grid_sync(bar, epoch);
       if (tid < 2 * kBW) tot[tid] = __ldcg(&buf[tid]);
       if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
         double* z = acc + ((col + 2) % 3) * (2 * kBW);

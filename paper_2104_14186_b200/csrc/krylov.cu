@@ -106,6 +106,140 @@ __global__ void sub_qh_kernel(const double* Q, int64_t ldq, int64_t n, int kcoun
   }
 }
 
+
+// ---------------------------------------------------------------- Lanczos
+// The whole m-step Lanczos with two-pass classical Gram-Schmidt
+// reorthogonalisation as ONE cooperative kernel (one CTA per SM): CTA g owns
+// rows [g*chunk, (g+1)*chunk) of every vector; w = A q_j is formed column by
+// column (A symmetric) for the owned indices, so the reorthogonalisation and
+// norms only need cross-CTA sums of short vectors: three grid barriers per
+// step (two CGS passes, the norm), no host round trips, no kernel launches.
+// Partial sums are combined in fixed order (deterministic).
+constexpr int kLzThreads = 512;
+struct LanczosArgs {
+  const double* A;
+  int64_t lda;
+  int n, m;
+  double* Q;  // n x (m+1), column 0 = q_0 (set by the host)
+  int64_t ldq;
+  double* wbuf;        // [2][n] unnormalised next vector, by step parity
+  double* slots;       // [2 passes][G][64] CGS partials
+  double* bslots;      // [2 parity][G] norm partials
+  double* alpha_part;  // [G][64] alpha partials (summed by the host)
+  double* beta2;       // [64]
+  unsigned* bar;
+};
+
+__global__ void __launch_bounds__(kLzThreads, 1) lanczos_kernel(LanczosArgs a) {
+  extern __shared__ double lz_sm[];
+  const int G = gridDim.x, g = blockIdx.x;
+  const int n = a.n;
+  const int chunk = (n + G - 1) / G;
+  const int r0 = min(n, g * chunk), nown = max(0, min(n, r0 + chunk) - r0);
+  double* w_own = lz_sm;       // [chunk]
+  double* hsm = w_own + chunk; // [64]
+  double* red = hsm + 64;      // [32]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = kLzThreads / 32;
+  unsigned epoch = 0;
+  double inv_beta = 1.0;
+  const bool vec2 = ((a.lda & 1) == 0) && ((reinterpret_cast<uintptr_t>(a.A) & 15) == 0) && ((n & 1) == 0);
+  for (int j = 0; j < a.m; ++j) {
+    const double* qsrc = (j == 0) ? a.Q : a.wbuf + ((j - 1) & 1) * (int64_t)n;
+    const double qs = (j == 0) ? 1.0 : inv_beta;
+    double* Qj = a.Q + (int64_t)j * a.ldq;
+    if (j > 0)
+      for (int i = tid; i < nown; i += kLzThreads) Qj[r0 + i] = qsrc[r0 + i] * qs;
+    // ---- w_i = (A q_j)_i for owned i: warp per column, 4 independent chains
+    double alpha_acc = 0.0;
+    for (int ii = warp; ii < nown; ii += NW) {
+      const double* col = a.A + (int64_t)(r0 + ii) * a.lda;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (vec2) {
+        const double2* c2 = reinterpret_cast<const double2*>(col);
+        const double2* q2 = reinterpret_cast<const double2*>(qsrc);
+        const int n2 = n / 2;
+        int r = lane;
+        for (; r + 32 < n2; r += 64) {
+          const double2 x = c2[r], y = c2[r + 32];
+          const double2 u = q2[r], v = q2[r + 32];
+          s0 = fma(x.x, u.x, s0);
+          s1 = fma(x.y, u.y, s1);
+          s2 = fma(y.x, v.x, s2);
+          s3 = fma(y.y, v.y, s3);
+        }
+        if (r < n2) {
+          const double2 x = c2[r], u = q2[r];
+          s0 = fma(x.x, u.x, s0);
+          s1 = fma(x.y, u.y, s1);
+        }
+      } else {
+        for (int r = lane; r < n; r += 32) s0 = fma(col[r], qsrc[r], s0);
+      }
+      const double wv = warp_sum((s0 + s1) + (s2 + s3)) * qs;
+      if (lane == 0) {
+        w_own[ii] = wv;
+        alpha_acc = fma(qsrc[r0 + ii] * qs, wv, alpha_acc);
+      }
+    }
+    if (lane == 0) red[warp] = alpha_acc;
+    __syncthreads();
+    if (tid == 0) {
+      double sa = 0.0;
+      for (int k = 0; k < NW; ++k) sa += red[k];
+      a.alpha_part[g * 64 + j] = sa;
+    }
+    // ---- two CGS passes: h = Q(:, 0:j)^T w, w -= Q(:, 0:j) h
+    for (int pass = 0; pass < 2; ++pass) {
+      double* sl = a.slots + (int64_t)pass * G * 64;
+      for (int t = warp; t <= j; t += NW) {
+        const double* qt = a.Q + (int64_t)t * a.ldq + r0;
+        double sm = 0.0;
+        for (int ii = lane; ii < nown; ii += 32) sm = fma(qt[ii], w_own[ii], sm);
+        sm = warp_sum(sm);
+        if (lane == 0) sl[g * 64 + t] = sm;
+      }
+      grid_sync(a.bar, epoch);
+      for (int t = warp; t <= j; t += NW) {
+        double sm = 0.0;
+        for (int gg = lane; gg < G; gg += 32) sm += __ldcg(&sl[gg * 64 + t]);
+        sm = warp_sum(sm);
+        if (lane == 0) hsm[t] = sm;
+      }
+      __syncthreads();
+      for (int ii = tid; ii < nown; ii += kLzThreads) {
+        double sm = 0.0;
+        for (int t = 0; t <= j; ++t) sm = fma(a.Q[(int64_t)t * a.ldq + r0 + ii], hsm[t], sm);
+        w_own[ii] -= sm;
+      }
+      __syncthreads();
+    }
+    // ---- beta^2 = w^T w; publish the unnormalised w for the next product
+    double* wout = a.wbuf + (j & 1) * (int64_t)n;
+    double b2 = 0.0;
+    for (int ii = tid; ii < nown; ii += kLzThreads) {
+      const double x = w_own[ii];
+      wout[r0 + ii] = x;
+      b2 = fma(x, x, b2);
+    }
+    b2 = block_sum(b2, red);
+    double* bs = a.bslots + (j & 1) * G;
+    if (tid == 0) bs[g] = b2;
+    grid_sync(a.bar, epoch);
+    if (warp == 0) {
+      double sm = 0.0;
+      for (int gg = lane; gg < G; gg += 32) sm += __ldcg(&bs[gg]);
+      sm = warp_sum(sm);
+      if (lane == 0) hsm[0] = sm;
+    }
+    __syncthreads();
+    const double beta2 = hsm[0];
+    if (g == 0 && tid == 0) a.beta2[j] = beta2;
+    inv_beta = 1.0 / sqrt(beta2);
+    __syncthreads();
+  }
+}
+
 struct Vec {
   double* p;
 };
@@ -208,11 +342,7 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps) {
   const int m = (int)std::min<int64_t>(steps, n);
   if (m > 63) throw InvalidArgument("lanczos_min_bound: at most 63 steps supported");
   const Arena::Mark mark = ctx.arena->mark();
-  Krylov K(ctx);
   DMat Q = ctx.arena->alloc(n, m + 1);
-  double* w = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
-  double* h = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 64));
-  double* ab = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * 64));  // alpha | beta^2
   std::vector<double> q0 = host_gaussian(n, 0x6c616e637aull);  // kernels.cpp:379
   {
     double s = 0.0;
@@ -221,31 +351,43 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps) {
     for (double& x : q0) x /= nv;
   }
   QDWHG_CUDA(cudaMemcpyAsync(Q.ptr(), q0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
-  const int gblocks = (int)std::min<int64_t>((n + 255) / 256, 4LL * ctx.num_sms);
-  // All steps are enqueued without host round trips; a breakdown (beta <= tol)
-  // is detected afterwards and the recurrence truncated there, exactly like the
-  // reference's early exit (later entries are never read).
-  for (int j = 0; j < m; ++j) {
-    const double* qj = Q.ptr() + j * Q.ld;
-    K.gemv_t(A, qj, w);                 // w = A q_j (A symmetric)
-    K.dot(qj, w, n, ab + j);            // alpha_j before reorthogonalisation (kernels.cpp:402-404)
-    for (int pass = 0; pass < 2; ++pass) {  // two-pass full reorthogonalisation (CGS2)
-      K.gemv_t(Q.sub(0, 0, n, j + 1), w, h);
-      sub_qh_kernel<<<gblocks, 256, 0, ctx.stream>>>(Q.ptr(), Q.ld, n, j + 1, h, w);
-      QDWHG_CUDA(cudaGetLastError());
-      ctx.count();
-    }
-    K.dot(w, w, n, ab + 64 + j);
-    if (j + 1 < m) {
-      scale_by_invnorm_kernel<<<gblocks, 256, 0, ctx.stream>>>(w, ab + 64 + j, n,
-                                                               Q.ptr() + (j + 1) * Q.ld);
-      QDWHG_CUDA(cudaGetLastError());
-      ctx.count();
-    }
+  // All steps run in one cooperative kernel without host round trips; a
+  // breakdown (beta <= tol) is detected afterwards and the recurrence
+  // truncated there, exactly like the reference's early exit (later entries
+  // are never read).
+  // one CTA per SM (co-resident for the grid barriers), at least 16 rows each
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, n / 16));
+  const int chunk = (int)((n + G - 1) / G);
+  const size_t smem = (size_t)(chunk + 96) * 8;
+  if (smem > 200 * 1024) throw InvalidArgument("lanczos_min_bound: matrix too large");
+  static bool lz_attr = false;
+  if (!lz_attr) {
+    QDWHG_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    lz_attr = true;
   }
-  std::vector<double> hab(128);
-  QDWHG_CUDA(cudaMemcpyAsync(hab.data(), ab, sizeof(double) * 128, cudaMemcpyDeviceToHost, ctx.stream));
+  double* wbuf = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * n));
+  double* slots = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * G * 64));
+  double* bslots = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * G));
+  double* apart = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * G * 64));
+  double* beta2 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 64));
+  unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
+  QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+  LanczosArgs la{A.ptr(), A.ld, (int)n, m, Q.ptr(), Q.ld, wbuf, slots, bslots, apart, beta2, bar};
+  void* largs[] = {&la};
+  QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)lanczos_kernel, dim3(G), dim3(kLzThreads), largs, smem,
+                                         ctx.stream));
+  ctx.count();
+  std::vector<double> hap((size_t)G * 64), hb2(64);
+  QDWHG_CUDA(cudaMemcpyAsync(hap.data(), apart, sizeof(double) * G * 64, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaMemcpyAsync(hb2.data(), beta2, sizeof(double) * 64, cudaMemcpyDeviceToHost, ctx.stream));
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  std::vector<double> hab(128, 0.0);
+  for (int j = 0; j < m; ++j) {
+    double sa = 0.0;
+    for (int gg = 0; gg < G; ++gg) sa += hap[(size_t)gg * 64 + j];
+    hab[j] = sa;
+    hab[64 + j] = hb2[j];
+  }
   const double breakdown_tol = (double)n * eps * std::max(1.0, fro);
   std::vector<double> alpha, beta;
   double beta_last = 0.0;

@@ -32,25 +32,6 @@ namespace {
 constexpr int kTrdThreads = 256;
 constexpr int kTrdNB = 32;
 
-QDWHG_DEV unsigned ld_acquire_u(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-QDWHG_DEV void red_release_add_u(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-QDWHG_DEV void gbar(unsigned* bar, unsigned& epoch) {
-  __syncthreads();
-  ++epoch;
-  if (threadIdx.x == 0) {
-    red_release_add_u(bar, 1u);
-    const unsigned target = epoch * gridDim.x;
-    while (ld_acquire_u(bar) < target) {
-    }
-  }
-  __syncthreads();
-}
 
 // Block-wide sum into one atomic on `dst` (skip zeros).
 QDWHG_DEV void block_atomic_sum(double v, double* dst, double* scratch) {
@@ -108,7 +89,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
     }
     block_atomic_sum(xs, &red[0], scratch);
     block_atomic_sum(alpha_part, &red[1], scratch);
-    gbar(a.bar, epoch);
+    grid_sync(a.bar, epoch);
     // ---- B: reflector for a_c(c+1 : n)
     const double alpha = __ldcg(&red[1]);
     const double xnorm = sqrt(__ldcg(&red[0]));
@@ -128,7 +109,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       if (c + 1 < n) a.e[c] = beta;
       a.tau[c] = taui;
     }
-    gbar(a.bar, epoch);
+    grid_sync(a.bar, epoch);
     // ---- C: y = A(c+1:n, c+1:n) v  (column dots) and t1 = W^T v, t2 = V^T v
     const int m = n - c - 1;
     const int nvirt = m + 2 * i;
@@ -142,7 +123,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       s = warp_sum(s);
       if (lane == 0) a.y[jv] = s;
     }
-    gbar(a.bar, epoch);
+    grid_sync(a.bar, epoch);
     // ---- D: w = tau (y - V t1 - W t2); alpha2 = w . v; w -= tau/2 alpha2 v
     if (tid < 2 * i) vw[tid] = __ldcg(&a.y[m + tid]);  // t1 = vw[0:i], t2 = vw[i:2i]
     __syncthreads();
@@ -156,14 +137,14 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       dotp += w * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
     }
     block_atomic_sum(dotp, &red[2], scratch);
-    gbar(a.bar, epoch);
+    grid_sync(a.bar, epoch);
     const double a2 = -0.5 * taui * __ldcg(&red[2]);
     for (int r = gtid; r < n; r += gsz) {
       double* wp = &a.W[r + (int64_t)i * a.ldp];
       if (r <= c) *wp = 0.0;
       else *wp += a2 * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
     }
-    gbar(a.bar, epoch);
+    grid_sync(a.bar, epoch);
   }
 }
 
