@@ -108,6 +108,16 @@ QDWHG_DEV void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int 
       : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may
+// start while its predecessor finishes; it must call griddep_wait() before its
+// first global-memory access.  griddep_launch_dependents() lets the next such
+// kernel start its prologue.
+QDWHG_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+QDWHG_DEV void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- grid barrier
 QDWHG_DEV unsigned ld_acquire_gpu(const unsigned* p) {
   unsigned v;

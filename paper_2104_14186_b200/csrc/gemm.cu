@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  griddep_wait();  // PDL: everything above overlapped the previous kernel's tail
 
   // Producer = lane 0 of warp 0 (no dedicated warp: 8 warps keep the 255-register
   // budget; 9 would cap at 168 because 3 warps would share one SMSP).
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
       }
     }
   }
+  griddep_launch_dependents();
 }
 
 // Split-K reduction + epilogue: D = alpha * sum_z P_z + beta * Cin (+diag), with
@@ -440,8 +442,7 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
              BM, (int)AK, (int)BK_, p.M, p.N, p.K, p.kmode, p.omode, p.splits, ntiles * p.splits);
     ctx.prof_begin(algorithmic_flops(p), tag);
   }
-  kern<<<grid, threads, smem, ctx.stream>>>(ta, tb, p);
-  QDWHG_CUDA(cudaGetLastError());
+  launch_pdl(ctx, kern, grid, dim3(threads), smem, ta, tb, p);
   if (ctx.profile) ctx.prof_end();
   if (debug) QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
   ctx.gemm_launches++;

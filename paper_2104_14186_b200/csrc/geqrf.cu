@@ -473,6 +473,7 @@ __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, do
   double(*Ts)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm);
   double(*M)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm + kBW * (kBW + 1));
   const int t = threadIdx.x;
+  griddep_wait();
   for (int i = t; i < kBW * kBW; i += blockDim.x) {
     const int r = i % kBW, c = i / kBW;
     Ts[r][c] = (r == c && r < b) ? tau[r] : 0.0;
@@ -727,9 +728,8 @@ void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T)
                                     2 * kBW * (kBW + 1) * 8));
     larft_attr = true;
   }
-  larft_kernel<<<1, 256, 2 * kBW * (kBW + 1) * 8, ctx.stream>>>(G.ptr(), G.ld, tau_dev, T.ptr(),
-                                                               T.ld, (int)G.rows);
-  QDWHG_CUDA(cudaGetLastError());
+  launch_pdl(ctx, larft_kernel, dim3(1), dim3(256), (size_t)(2 * kBW * (kBW + 1) * 8), G.ptr(), G.ld,
+             tau_dev, T.ptr(), T.ld, (int)G.rows);
   ctx.count();
 }
 

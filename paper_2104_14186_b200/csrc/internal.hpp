@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -119,6 +121,25 @@ struct Ctx {
   void prof_end();
   void prof_collect();
 };
+
+// Launch with programmatic stream serialisation (the kernel must call
+// griddep_wait() before touching global memory); QDWHG_NO_PDL disables it.
+template <typename... KArgs, typename... Args>
+void launch_pdl(const Ctx& ctx, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                Args&&... args) {
+  static const bool pdl = getenv("QDWHG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  QDWHG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // ------------------------------------------------------------------ gemm.cu
 // C = alpha * op(A) * op(B) + beta * Cin (+ diag_add on the diagonal of C).

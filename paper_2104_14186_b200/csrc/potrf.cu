@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   const int nsb = nbp / kSB;
   if (tid == 0) bad_s = 0;
   DIAG_MARK(20);
+  griddep_wait();
 
   // ---- load: lower triangle by cp.async, identity padding, zero strict upper
   for (int c = warp; c < nbp; c += kDiagThreads / 32) {
@@ -309,10 +310,8 @@ void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk) {
                                     (int)smem));
     set = true;
   }
-  potrf_diag_kernel<<<1, kDiagThreads, smem, ctx.stream>>>(Zkk.ptr(), Zkk.ld, Wkk.ptr(), Wkk.ld,
-                                                           Wikk.ptr(), Wikk.ld, (int)Zkk.rows,
-                                                           ctx.dflag);
-  QDWHG_CUDA(cudaGetLastError());
+  launch_pdl(ctx, potrf_diag_kernel, dim3(1), dim3(kDiagThreads), smem, Zkk.ptr(), Zkk.ld, Wkk.ptr(),
+             Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag);
   ctx.count();
 }
 
