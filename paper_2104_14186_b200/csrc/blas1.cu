@@ -87,6 +87,19 @@ __global__ void copy_kernel(const double* X, int64_t ldx, double* Y, int64_t ldy
   }
 }
 
+// Y = X^T through 32x32 shared-memory tiles (both sides coalesced)
+__global__ void transpose_kernel(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m,
+                                 int64_t n) {
+  __shared__ double t[32][33];
+  const int64_t i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;  // tile of X: rows i0.., cols j0..
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: 8 rows per pass
+  for (int r = ty; r < 32; r += 8)
+    if (i0 + tx < m && j0 + r < n) t[r][tx] = X[(i0 + tx) + (j0 + r) * ldx];
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8)
+    if (j0 + tx < n && i0 + r < m) Y[(j0 + tx) + (i0 + r) * ldy] = t[tx][r];
+}
+
 // per-block partials: [0] sum x^2, [1] max |x_ij - x_ji|, [2] nonfinite count, [3] max |x|
 __global__ void stats_kernel(const double* X, int64_t ld, int64_t m, int64_t n, int want_asym,
                              double* partial) {
@@ -213,6 +226,14 @@ void copy(Ctx& ctx, const DMat& X, const DMat& Y) {
   if (X.rows * X.cols == 0) return;
   copy_kernel<<<grid_for(ctx, X.rows * X.cols, 256), 256, 0, ctx.stream>>>(X.ptr(), X.ld, Y.ptr(),
                                                                            Y.ld, X.rows, X.cols);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+}
+
+void transpose(Ctx& ctx, const DMat& X, const DMat& Y) {
+  if (X.rows * X.cols == 0) return;
+  dim3 grid((unsigned)((X.rows + 31) / 32), (unsigned)((X.cols + 31) / 32));
+  transpose_kernel<<<grid, 256, 0, ctx.stream>>>(X.ptr(), X.ld, Y.ptr(), Y.ld, X.rows, X.cols);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count();
 }

@@ -108,10 +108,14 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   gemm(ctx, Op::N, Op::N, 1.0, X, Winv, 0.0, Y, t1);
   const double bc = w.b / w.c;
   const double coef = w.a - bc;
+  // W^-T materialised (one transpose pass) so the second TRMM runs in the
+  // faster K-major-B layout instead of reading W^-1 transposed tile by tile
+  DMat WinvT = Z;  // Z is dead after the factorisation
+  transpose(ctx, Winv, WinvT);
   GemmExtra t2;
-  t2.krange = KRange::BLower;  // (W^-1)^T lower
+  t2.krange = KRange::BLower;  // W^-T lower
   t2.cin = &X;                 // fused weight update (b/c) X + (a - b/c) G
-  gemm(ctx, Op::N, Op::T, coef, Y, Winv, bc, Xout, t2);
+  gemm(ctx, Op::N, Op::N, coef, Y, WinvT, bc, Xout, t2);
   ctx.arena->release_to(mark);
 }
 

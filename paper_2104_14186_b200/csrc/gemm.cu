@@ -98,12 +98,29 @@ QDWHG_DEV void tile_coords(const GemmParams& p, int bid, int& tm, int& tn) {
     tm = c + rem;
     return;
   }
-  tm = bid % p.tiles_m;
-  tn = bid / p.tiles_m;
+  // Triangular K ranges: the tile index that sets the work is the slow index,
+  // heaviest first (longest-processing-time order across the waves).
   switch ((KRange)p.kmode) {
-    case KRange::BUpper: tn = p.tiles_n - 1 - tn; break;
-    case KRange::ALower: tm = p.tiles_m - 1 - tm; break;
-    default: break;
+    case KRange::BUpper:  // work grows with tn
+      tm = bid % p.tiles_m;
+      tn = p.tiles_n - 1 - bid / p.tiles_m;
+      break;
+    case KRange::BLower:  // work shrinks with tn
+      tm = bid % p.tiles_m;
+      tn = bid / p.tiles_m;
+      break;
+    case KRange::ALower:  // work grows with tm
+      tn = bid % p.tiles_n;
+      tm = p.tiles_m - 1 - bid / p.tiles_n;
+      break;
+    case KRange::AUpper:  // work shrinks with tm
+      tn = bid % p.tiles_n;
+      tm = bid / p.tiles_n;
+      break;
+    default:
+      tm = bid % p.tiles_m;
+      tn = bid / p.tiles_m;
+      break;
   }
 }
 

@@ -165,6 +165,8 @@ void axpby_identity(Ctx& ctx, const DMat& X, double a, double diag, const DMat& 
 // Y = a * (X + X^T)/2 + diag*I  (square; Y must not alias X unless in place-safe mode)
 void symmetrize_scale(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y);
 void copy(Ctx& ctx, const DMat& X, const DMat& Y);
+// Y = X^T (Y must not alias X)
+void transpose(Ctx& ctx, const DMat& X, const DMat& Y);
 void copy_from_host(Ctx& ctx, const double* h, int64_t ldh, const DMat& Y);
 void copy_to_host(Ctx& ctx, const DMat& X, double* h, int64_t ldh);
 // Reductions (results land in ctx.hscratch after sync): frobenius^2, max |x_ij - x_ji|,

@@ -1,0 +1,55 @@
+"""Kernel timeline (start offset, duration, gap) of one library call via the
+CUDA profiler: python tools/timeline.py chol|qr|potrf [n]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+from paper_2104_14186_b200 import qdwh  # noqa: E402
+
+what = sys.argv[1] if len(sys.argv) > 1 else "chol"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+dev = torch.device("cuda:0")
+h = qdwh.Handle(0)
+h.set_stream(torch.cuda.current_stream().cuda_stream)
+G = qdwh.gaussian_matrix_device(n, n, 3, handle=h)
+X = (G / (G.norm() ** 0.5)).t().contiguous().t()
+Z = (G.T @ G / n + torch.eye(n, dtype=torch.float64, device=dev)).t().contiguous().t()
+
+
+def call():
+    if what == "chol":
+        return qdwh.qdwh_chol_step(X, 0.5, handle=h)
+    if what == "qr":
+        return qdwh.qr_factor(G, handle=h)
+    return qdwh.cholesky_factor_inverse(Z, handle=h)
+
+
+for _ in range(3):
+    call()
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    call()
+    torch.cuda.synchronize()
+ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+ev.sort(key=lambda e: e.time_range.start)
+t0 = ev[0].time_range.start
+prev_end = t0
+tot_gap = 0.0
+agg = {}
+for e in ev:
+    st, en = e.time_range.start, e.time_range.end
+    gap = st - prev_end
+    tot_gap += max(gap, 0)
+    name = e.name.replace("(anonymous namespace)::", "").split("(")[0].replace("qdwhg::", "")[:60]
+    a = agg.setdefault(name, [0, 0.0])
+    a[0] += 1
+    a[1] += en - st
+    if len(sys.argv) > 3:
+        print(f"{(st - t0):9.1f} us  dur {en - st:8.1f}  gap {gap:6.1f}  {name}")
+    prev_end = max(prev_end, en)
+print(f"span {prev_end - t0:.1f} us, busy {sum(v[1] for v in agg.values()):.1f} us, gaps {tot_gap:.1f} us")
+for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:15]:
+    print(f"{v[1]:9.1f} us {v[0]:5d}x  {k}")
