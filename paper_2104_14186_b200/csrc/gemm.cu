@@ -543,25 +543,41 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   Be.rows += (nb_ - 1) * ex.b_step_r;
   Be.cols += (nb_ - 1) * ex.b_step_c;
 
-  // Tile choice: 128x128 when the grid fills the machine, 64x64 below that,
-  // 32x32 when even 64x64 tiles would leave most SMs idle (the small GEMMs on
-  // the recursive POTRF / TRTRI critical path).
-  const bool big = ((M + 127) / 128) * ((N + 127) / 128) * nb_ >= ctx.num_sms;
-  const bool tiny = !big && ((M + 63) / 64) * ((N + 63) / 64) * nb_ * 2 < ctx.num_sms;
-  const int BMt = big ? 128 : tiny ? 32 : 64;
+  // Tile size and split-K from a small wave-quantisation cost model: for each
+  // candidate (128/64/32 tiles, split factor) estimate
+  //   ceil(units / concurrent CTAs) * (tile flops / per-CTA rate + prologue)
+  //   + split-K reduction traffic,
+  // and take the cheapest.  Triangular K ranges count half the K on average.
+  const bool tri = ex.krange != KRange::Full;
+  const double keff = tri ? 0.5 * (double)K : (double)K;
+  const int64_t ktiles = (K + BK - 1) / BK;
+  const double sm_rate = 64.0 * 1.9e9;  // FP64 FMA / s per SM (DMMA)
+  int BMt = 128, splits = 1;
+  double best = 1e30;
+  for (int bm : {128, 64, 32}) {
+    if (nb_ > 1 && (M % bm || N % bm)) continue;  // batched items must tile exactly
+    const int64_t tm = (M + bm - 1) / bm, tn = (N + bm - 1) / bm;
+    const int64_t tiles = (ex.out != OutMode::Full) ? tn * (tn + 1) / 2 : tm * tn;
+    const int per_sm = (bm == 32) ? 2 : 1;
+    const double eff = (bm == 128) ? 0.95 : (bm == 64) ? 0.75 : 0.45;
+    for (int sp : {1, 2, 3, 4, 6, 8, 12, 16}) {
+      if (ex.split_k > 0 && sp != ex.split_k) continue;
+      if (sp > 1 && (nb_ > 1 || ktiles / sp < 4)) continue;
+      const double units = (double)tiles * nb_ * sp;
+      const double waves = std::ceil(units / ((double)ctx.num_sms * per_sm));
+      const double t_unit = (double)bm * bm * (keff / sp) / (sm_rate * eff / per_sm) + 2e-6;
+      double t = waves * t_unit;
+      if (sp > 1) t += (double)(sp + 1) * M * N * 8.0 / 4e12 + 3e-6;
+      if (t < best * 0.97) {  // prefer the earlier (larger-tile, fewer-split) candidate on ties
+        best = t;
+        BMt = bm;
+        splits = sp;
+      }
+    }
+  }
+  const bool big = BMt == 128, tiny = BMt == 32;
   p.tiles_m = (int)((M + BMt - 1) / BMt);
   p.tiles_n = (int)((N + BMt - 1) / BMt);
-  int ntiles = (ex.out != OutMode::Full) ? p.tiles_n * (p.tiles_n + 1) / 2
-                                                 : p.tiles_m * p.tiles_n;
-  // split-K when the output grid leaves SMs idle and K is long
-  int splits = ex.split_k;
-  if (splits <= 0) {
-    splits = 1;
-    const int64_t ktiles = (K + BK - 1) / BK;
-    while (ntiles * nb_ * splits * 2 <= 2 * ctx.num_sms && ktiles / (splits * 2) >= 16 &&
-           splits < 32)
-      splits *= 2;
-  }
   if (nb_ > 1) {
     splits = 1;
     if (M % BMt || N % BMt || K % BK)

@@ -742,7 +742,8 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   // (T = [T1, -T1 (V1^T V2) T2; 0, T2]) so the trailing update of the rest of
   // the matrix — the O(n^3) part — runs as GEMMs with K = 256.
   const int nbi = kBW;
-  const int nbo = 4 * kBW;
+  static const int nbo_env = getenv("QDWHG_QR_NBO") ? atoi(getenv("QDWHG_QR_NBO")) : 0;
+  const int nbo = (nbo_env == 128 || nbo_env == 256 || nbo_env == 512) ? nbo_env : 4 * kBW;
   w.nb = nbo;
   const int64_t nout = (n + nbo - 1) / nbo;
   w.V = ctx.arena->alloc(m, n);
