@@ -258,6 +258,9 @@ qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
     int sms = 148;
     QDWHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     h->ctx.stream = h->stream;
+    QDWHG_CUDA(cudaStreamCreateWithFlags(&h->ctx.side, cudaStreamNonBlocking));
+    QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_main, cudaEventDisableTiming));
+    QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_side, cudaEventDisableTiming));
     h->ctx.arena = &h->arena;
     h->ctx.num_sms = sms;
     QDWHG_CUDA(cudaMalloc(&h->ctx.dscratch, 1 << 16));
@@ -280,6 +283,10 @@ qdwhg_status qdwhg_destroy(qdwhg_handle* h) {
   cudaFree(h->ctx.dscratch);
   cudaFreeHost(h->ctx.hscratch);
   cudaFree(h->ctx.dflag);
+  cudaStreamSynchronize(h->ctx.side);
+  cudaStreamDestroy(h->ctx.side);
+  cudaEventDestroy(h->ctx.ev_main);
+  cudaEventDestroy(h->ctx.ev_side);
   cudaStreamDestroy(h->stream);
   delete h;
   return QDWHG_OK;

@@ -283,29 +283,53 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
   const bool vec = ((reinterpret_cast<uintptr_t>(D) & 15) == 0) && ((ldd & 1) == 0) &&
                    (split || p.beta == 0.0 ||
                     (((reinterpret_cast<uintptr_t>(Cinp) & 15) == 0) && ((p.ldcin & 1) == 0)));
-  for (int cl = warp; cl < BN; cl += NW) {
+  // Cin (beta != 0) for every (column, row pair) of this lane is loaded up
+  // front — all loads in flight at once instead of one global round trip per
+  // column — then combined with the tile and stored.
+  constexpr int NCOL = (BN + NW - 1) / NW, NCH = (BM + 63) / 64;
+  double2 cinv[NCOL][NCH];
+  const bool use_cin = !split && p.beta != 0.0;
+  if (use_cin) {
+#pragma unroll
+    for (int ci = 0; ci < NCOL; ++ci) {
+      const int cl = warp + ci * NW;
+      const int j = n0 + cl;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int rl = ch * 64 + 2 * lane;
+        const int i = m0 + rl;
+        double2 c2 = make_double2(0.0, 0.0);
+        if (cl < BN && j < p.N && rl < BM && i < p.M) {
+          const double* cin = Cinp + i + (size_t)j * p.ldcin;
+          if (vec && i + 1 < p.M) {
+            c2 = *reinterpret_cast<const double2*>(cin);
+          } else {
+            c2.x = cin[0];
+            if (i + 1 < p.M) c2.y = cin[1];
+          }
+        }
+        cinv[ci][ch] = c2;
+      }
+    }
+  }
+#pragma unroll
+  for (int ci = 0; ci < NCOL; ++ci) {
+    const int cl = warp + ci * NW;
     const int j = n0 + cl;
-    if (j >= p.N) break;
+    if (cl >= BN || j >= p.N) break;
     const double* col = Cs + cl * LDC;
 #pragma unroll
-    for (int rl0 = 0; rl0 < BM; rl0 += 64) {
-      const int rl = rl0 + 2 * lane;
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int rl = ch * 64 + 2 * lane;
       const int i = m0 + rl;
       if ((BM % 64 != 0 && rl >= BM) || i >= p.M) continue;
       double v0 = col[rl], v1 = col[rl + 1];
       if (!split) {
         v0 *= p.alpha;
         v1 *= p.alpha;
-        if (p.beta != 0.0) {
-          const double* cin = Cinp + i + (size_t)j * p.ldcin;
-          if (vec && i + 1 < p.M) {
-            const double2 c2 = *reinterpret_cast<const double2*>(cin);
-            v0 += p.beta * c2.x;
-            v1 += p.beta * c2.y;
-          } else {
-            v0 += p.beta * cin[0];
-            if (i + 1 < p.M) v1 += p.beta * cin[1];
-          }
+        if (use_cin) {
+          v0 += p.beta * cinv[ci][ch].x;
+          v1 += p.beta * cinv[ci][ch].y;
         }
         if (i == j) v0 += p.diag_add;
         if (i + 1 == j) v1 += p.diag_add;

@@ -753,6 +753,16 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW));
   unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
   DMat G = ctx.arena->alloc(nbo, nbo);
+  static const bool no_la = getenv("QDWHG_QR_NO_LOOKAHEAD") != nullptr;
+  const bool lookahead = !no_la && ctx.side != nullptr && n > 2 * nbo;
+  // side-stream scratch lives for the whole factorisation (never rewound
+  // while side-stream kernels may still read it)
+  DMat SW1, SW2;
+  if (lookahead) {
+    SW1 = ctx.arena->alloc(nbo, n);
+    SW2 = ctx.arena->alloc(nbo, n);
+  }
+  bool side_pending = false;
   const Arena::Mark mark = ctx.arena->mark();
   for (int64_t po = 0; po < nout; ++po) {
     const int64_t jo = po * nbo;
@@ -809,19 +819,50 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
         blocks.swap(next);
       }
     }
-    // ---- trailing update of the rest: C = C - V T^T (V^T C), K = bo
+    // ---- trailing update of the rest: C = C - V T^T (V^T C), K = bo.
+    // Look-ahead: the next outer block's columns are updated first on the main
+    // stream (its panels can start right away); the remaining columns are
+    // updated on the side stream, overlapping the next block's latency-bound
+    // panel chain.  Column ranges are disjoint; events order the hand-offs.
     if (nc > 0) {
       const DMat Vo = w.V.sub(jo, jo, mo, bo);
-      const DMat C = A.sub(jo, jo + bo, mo, nc);
-      DMat W1 = ctx.arena->alloc(bo, nc), W2 = ctx.arena->alloc(bo, nc);
-      gemm(ctx, Op::T, Op::N, 1.0, Vo, C, 0.0, W1);
-      GemmExtra e;
-      e.krange = KRange::ALower;
-      gemm(ctx, Op::T, Op::N, 1.0, To, W1, 0.0, W2, e);
-      gemm(ctx, Op::N, Op::N, -1.0, Vo, W2, 1.0, C);
-      ctx.arena->release_to(mark);
+      const int64_t bn = lookahead ? std::min<int64_t>(nbo, nc) : nc;
+      if (side_pending) QDWHG_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_side, 0));
+      {
+        const DMat C = A.sub(jo, jo + bo, mo, bn);
+        DMat W1 = ctx.arena->alloc(bo, bn), W2 = ctx.arena->alloc(bo, bn);
+        gemm(ctx, Op::T, Op::N, 1.0, Vo, C, 0.0, W1);
+        GemmExtra e;
+        e.krange = KRange::ALower;
+        gemm(ctx, Op::T, Op::N, 1.0, To, W1, 0.0, W2, e);
+        gemm(ctx, Op::N, Op::N, -1.0, Vo, W2, 1.0, C);
+        ctx.arena->release_to(mark);
+      }
+      if (nc > bn) {
+        QDWHG_CUDA(cudaEventRecord(ctx.ev_main, ctx.stream));
+        cudaStream_t main_stream = ctx.stream;
+        ctx.stream = ctx.side;
+        QDWHG_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_main, 0));
+        const int64_t nr = nc - bn;
+        const DMat C = A.sub(jo, jo + bo + bn, mo, nr);
+        const DMat W1 = SW1.sub(0, 0, bo, nr), W2 = SW2.sub(0, 0, bo, nr);
+        GemmExtra e0;
+        e0.split_k = 1;  // no arena scratch on the side stream
+        gemm(ctx, Op::T, Op::N, 1.0, Vo, C, 0.0, W1, e0);
+        GemmExtra e;
+        e.krange = KRange::ALower;
+        e.split_k = 1;
+        gemm(ctx, Op::T, Op::N, 1.0, To, W1, 0.0, W2, e);
+        gemm(ctx, Op::N, Op::N, -1.0, Vo, W2, 1.0, C, e0);
+        QDWHG_CUDA(cudaEventRecord(ctx.ev_side, ctx.stream));
+        ctx.stream = main_stream;
+        side_pending = true;
+      } else {
+        side_pending = false;
+      }
     }
   }
+  if (side_pending) QDWHG_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_side, 0));
 }
 
 void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, const DMat& Q) {

@@ -100,6 +100,8 @@ enum class OutMode { Full, LowerMirror, Lower };
 
 struct Ctx {
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // look-ahead stream (handle-owned)
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr;  // cross-stream ordering
   Arena* arena = nullptr;
   int num_sms = 148;
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
