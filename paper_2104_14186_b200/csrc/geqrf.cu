@@ -472,8 +472,15 @@ __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, do
   extern __shared__ double larft_sm[];
   double(*Ts)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm);
   double(*M)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm + kBW * (kBW + 1));
+  double(*Gs)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(larft_sm + 2 * kBW * (kBW + 1));
   const int t = threadIdx.x;
   griddep_wait();
+  // G (upper part used) and tau staged in shared memory once: the doubling
+  // loops below only touch shared memory
+  for (int i = t; i < b * b; i += blockDim.x) {
+    const int r = i % b, c = i / b;
+    Gs[r][c] = G[r + (int64_t)c * ldg];
+  }
   for (int i = t; i < kBW * kBW; i += blockDim.x) {
     const int r = i % kBW, c = i / kBW;
     Ts[r][c] = (r == c && r < b) ? tau[r] : 0.0;
@@ -482,12 +489,12 @@ __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, do
   for (int s = 1; s < b; s *= 2) {
     // M(a+r, a+s+c) = sum_{k=r}^{s-1} T11(r, k) G(a+k, a+s+c)
     for (int i = t; i < b * s; i += blockDim.x) {
-      const int r = i % s, rest = i / s;          // rest = a/(2s) * s + c  over all pairs
+      const int r = i % s, rest = i / s;
       const int pair = rest / s, c = rest % s;
       const int a = pair * 2 * s;
       if (a + s + c >= b) continue;
       double acc = 0.0;
-      for (int k = r; k < s; ++k) acc += Ts[a + r][a + k] * G[(a + k) + (int64_t)(a + s + c) * ldg];
+      for (int k = r; k < s; ++k) acc = fma(Ts[a + r][a + k], Gs[a + k][a + s + c], acc);
       M[a + r][a + s + c] = acc;
     }
     __syncthreads();
@@ -498,7 +505,7 @@ __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, do
       const int a = pair * 2 * s;
       if (a + s + c >= b) continue;
       double acc = 0.0;
-      for (int k = 0; k <= c; ++k) acc += M[a + r][a + s + k] * Ts[a + s + k][a + s + c];
+      for (int k = 0; k <= c; ++k) acc = fma(M[a + r][a + s + k], Ts[a + s + k][a + s + c], acc);
       Ts[a + r][a + s + c] = -acc;
     }
     __syncthreads();
@@ -725,10 +732,10 @@ void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T)
   static bool larft_attr = false;
   if (!larft_attr) {
     QDWHG_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kBW * (kBW + 1) * 8));
+                                    3 * kBW * (kBW + 1) * 8));
     larft_attr = true;
   }
-  launch_pdl(ctx, larft_kernel, dim3(1), dim3(256), (size_t)(2 * kBW * (kBW + 1) * 8), G.ptr(), G.ld,
+  launch_pdl(ctx, larft_kernel, dim3(1), dim3(512), (size_t)(3 * kBW * (kBW + 1) * 8), G.ptr(), G.ld,
              tau_dev, T.ptr(), T.ld, (int)G.rows);
   ctx.count();
 }
