@@ -53,8 +53,9 @@ constexpr int kLDA = 129;        // padded smem leading dimension (odd -> confli
 // the instructions of shuffling each double.
 template <int J>
 struct CholStep {
-  static QDWHG_DEV void run(double (&row)[kSB], double* L, int lane, bool& bad, double& my_inv) {
-    const double djj = __shfl_sync(0xffffffffu, row[J], J);
+  // djj: the pivot L_JJ^2, already broadcast by the previous step (look-ahead)
+  static QDWHG_DEV void run(double (&row)[kSB], double* L, int lane, bool& bad, double& my_inv,
+                            double djj) {
     if (!(djj > 0.0)) bad = true;
     const double inv = rsqrt_newton(djj);
     if (lane > J) row[J] *= inv;
@@ -62,18 +63,23 @@ struct CholStep {
       row[J] = djj * inv;
       my_inv = inv;
     }
+    // look-ahead: lane J+1 updates its own diagonal from its own register
+    // (same fma as the loop below) and broadcasts the next pivot right away, so
+    // the next step's rsqrt does not wait for the shared-memory round trip
+    double dnext = 0.0;
+    if (J + 1 < kSB) dnext = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[(J + 1) % kSB]), (J + 1) % kSB);
     if (lane >= J) L[J * kLDA + lane] = row[J];
     __syncwarp();
     // unpredicated: entries above a lane's diagonal pick up junk that is never
     // read (the pivot and the written column only use entries on/below it)
 #pragma unroll
     for (int c = J + 1; c < kSB; ++c) row[c] -= row[J] * L[J * kLDA + c];
-    CholStep<J + 1>::run(row, L, lane, bad, my_inv);
+    CholStep<J + 1>::run(row, L, lane, bad, my_inv, dnext);
   }
 };
 template <>
 struct CholStep<kSB> {
-  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&) {}
+  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&, double) {}
 };
 
 
@@ -136,7 +142,8 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
       for (int c = 0; c < kSB; ++c) row[c] = A[(b0 + c) * kLDA + b0 + lane];  // strict upper is 0
       bool bad = false;
       double my_inv = 0.0;
-      CholStep<0>::run(row, A + b0 * kLDA + b0, lane, bad, my_inv);  // writes L in place
+      CholStep<0>::run(row, A + b0 * kLDA + b0, lane, bad, my_inv,
+                       __shfl_sync(0xffffffffu, row[0], 0));  // writes L in place
       if (bad && lane == 0) bad_s = 1;
       Sinv[b0 + lane] = my_inv;
     }
@@ -266,6 +273,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
         }
       }
       __syncthreads();
+      DIAG_MARK(22 + 2 * jb);
       // L21 <- -T * D^{-1}   (D lower with explicit zeros: full K)
       for (int u = warp; u < nt; u += kDiagThreads / 32) {
         const int ti = u;
@@ -284,6 +292,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
         }
       }
     }
+    DIAG_MARK(21 + 2 * jb);
     // diagonal block <- D^{-1} (lower; the strict upper stays zero)
     for (int idx = tid; idx < kSB * kSB; idx += kDiagThreads) {
       const int r = idx & 31, c = idx >> 5;

@@ -50,6 +50,8 @@ int main() {
     prev = t[i];
   }
   printf("  total %lld cycles\n", t[16] - t[20]);
+  printf("  inverse: jb2 prod1 %lld prod2 %lld | jb1 prod1 %lld prod2 %lld | jb0 prod1 %lld prod2 %lld\n",
+         t[26] - t[14], t[25] - t[26], t[24] - t[25] - 0, t[23] - t[24], t[22] - t[23], t[21] - t[22]);
   // check: W^T W == Z
   std::vector<double> w(ld * nb), wi(ld * nb);
   cudaMemcpy(w.data(), W, 8 * ld * nb, cudaMemcpyDeviceToHost);
