@@ -84,8 +84,11 @@ void StageClock::finish(double* stage_seconds, double* total) {
 }
 
 // ----------------------------------------------------------------- QDWH steps
-void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout) {
+void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout,
+                    bool symmetric) {
   // polar.cpp:82-128:  Z = I + c sym(X^T X);  W = chol(Z);  X+ = (b/c) X + (a - b/c) X W^-1 W^-T
+  // symmetric: X is symmetric, so is G = X Z^-1 (a function of X): only its lower
+  // triangle is computed and mirrored (1/3 fewer TRMM flops, X+ exactly symmetric)
   const int64_t m = X.rows, n = X.cols;
   const Arena::Mark mark = ctx.arena->mark();
   DMat Z = ctx.arena->alloc(n, n);
@@ -115,6 +118,7 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   GemmExtra t2;
   t2.krange = KRange::BLower;  // W^-T lower
   t2.cin = &X;                 // fused weight update (b/c) X + (a - b/c) G
+  if (symmetric && X.rows == X.cols) t2.out = OutMode::LowerMirror;
   gemm(ctx, Op::N, Op::N, coef, Y, WinvT, bc, Xout, t2);
   ctx.arena->release_to(mark);
 }
@@ -161,8 +165,11 @@ FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_
       qdwh_qr_step(ctx, X, w, X);
       ++r.iters_qr;
     } else {
-      qdwh_chol_step(ctx, X, w, X);
+      qdwh_chol_step(ctx, X, w, X, symmetric);  // symmetric output by construction
       ++r.iters_chol;
+      r.ell = w.ell_out;
+      r.trace.push_back(r.ell);
+      continue;
     }
     if (symmetric) symmetrize_scale(ctx, X, 1.0, 0.0, X);
     r.ell = w.ell_out;

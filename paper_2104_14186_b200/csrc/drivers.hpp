@@ -29,7 +29,8 @@ struct StageClock {
 };
 
 // polar.cpp:82-128.  Xout may alias X.
-void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout);
+void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout,
+                    bool symmetric = false);
 // polar.cpp:53-80.  Xout may alias X.
 void qdwh_qr_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout);
 
