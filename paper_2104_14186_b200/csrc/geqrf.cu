@@ -750,7 +750,11 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   // the matrix — the O(n^3) part — runs as GEMMs with K = 256.
   const int nbi = kBW;
   static const int nbo_env = getenv("QDWHG_QR_NBO") ? atoi(getenv("QDWHG_QR_NBO")) : 0;
-  const int nbo = (nbo_env == 128 || nbo_env == 256 || nbo_env == 512) ? nbo_env : 4 * kBW;
+  // outer block: 256 columns; 512 for very wide matrices, where the K = 512
+  // trailing GEMMs' efficiency gain outweighs the longer inner chain (cfg4:
+  // QR 286 -> 265 ms; at n <= 8192 256 is faster)
+  const int nbo = (nbo_env == 128 || nbo_env == 256 || nbo_env == 512) ? nbo_env
+                  : (n >= 12288) ? 8 * kBW : 4 * kBW;
   w.nb = nbo;
   const int64_t nout = (n + nbo - 1) / nbo;
   w.V = ctx.arena->alloc(m, n);
