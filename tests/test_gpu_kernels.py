@@ -222,3 +222,28 @@ def test_polar_config_errors():
         qdwh.polar_decompose(a, qdwh.PolarConfig(ell0=1e-6, max_iters=1))
     with pytest.raises(ValueError):
         qdwh.polar_decompose(O.gaussian_matrix(3, 4, 1))
+
+
+@pytest.mark.parametrize("nbo", ["128", "512"])
+def test_qr_outer_block_sizes(nbo):
+    """The 128/512-column outer blocking (512 is the default from n = 12288) on a
+    small matrix, in a subprocess so the size knob is read fresh."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "from oracle import qdwh_oracle as O\n"
+        "from paper_2104_14186_b200 import qdwh\n"
+        "a = O.gaussian_matrix(1500, 1300, 91)\n"
+        "q, r = qdwh.qr_factor(a)\n"
+        "assert np.linalg.norm(q.T @ q - np.eye(1500)) <= 50 * 1500 * O.EPS\n"
+        "assert np.linalg.norm(q @ r - a) <= 50 * 1500 * O.EPS * np.linalg.norm(a)\n"
+        "qn, rn = np.linalg.qr(a, mode='complete')\n"
+        "np.testing.assert_allclose(np.diag(r), np.diag(rn), rtol=1e-10, atol=1e-12)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QDWHG_QR_NBO=nbo, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
