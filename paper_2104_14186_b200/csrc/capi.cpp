@@ -258,7 +258,12 @@ qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
     int sms = 148;
     QDWHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     h->ctx.stream = h->stream;
-    QDWHG_CUDA(cudaStreamCreateWithFlags(&h->ctx.side, cudaStreamNonBlocking));
+    {
+      int least = 0, greatest = 0;
+      QDWHG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      QDWHG_CUDA(cudaStreamCreateWithPriority(&h->ctx.side, cudaStreamNonBlocking, least));
+      QDWHG_CUDA(cudaStreamCreateWithPriority(&h->ctx.hi, cudaStreamNonBlocking, greatest));
+    }
     QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_main, cudaEventDisableTiming));
     QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_side, cudaEventDisableTiming));
     h->ctx.arena = &h->arena;
@@ -284,7 +289,9 @@ qdwhg_status qdwhg_destroy(qdwhg_handle* h) {
   cudaFreeHost(h->ctx.hscratch);
   cudaFree(h->ctx.dflag);
   cudaStreamSynchronize(h->ctx.side);
+  cudaStreamSynchronize(h->ctx.hi);
   cudaStreamDestroy(h->ctx.side);
+  cudaStreamDestroy(h->ctx.hi);
   cudaEventDestroy(h->ctx.ev_main);
   cudaEventDestroy(h->ctx.ev_side);
   cudaStreamDestroy(h->stream);

@@ -340,18 +340,17 @@ void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigm
     const Arena::Mark mark = ctx.arena->mark();
     // Householder (not CholeskyQR2: A Q2 can be ill-conditioned and R's accuracy
     // sets the small singular values' relative accuracy)
-    DMat Q = ctx.arena->alloc(m, n), R = ctx.arena->alloc(n, n);
-    {
-      DMat Aw = ctx.arena->alloc(m, n);
-      copy(ctx, A, Aw);
-      QrWork qw;
-      geqrf(ctx, Aw, qw);
-      orgqr_cols(ctx, qw, m, n, 0, Q);
-      copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
-    }
-    DMat UR = ctx.arena->alloc(n, n);
-    svd_polar(ctx, R, UR, sigma, V);
-    gemm(ctx, Op::N, Op::N, 1.0, Q, UR, 0.0, U);
+    DMat R = ctx.arena->alloc(n, n);
+    DMat Aw = ctx.arena->alloc(m, n);
+    copy(ctx, A, Aw);
+    QrWork qw;
+    geqrf(ctx, Aw, qw);
+    copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
+    svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V);
+    // U = Q [U_R; 0]: the reflectors applied to U_R directly (no explicit Q,
+    // no m x n x n GEMM)
+    fill(ctx, U.sub(n, 0, m - n, n), 0.0, 0.0);
+    ormqr_left(ctx, qw, m, n, U);
     ctx.arena->release_to(mark);
     return;
   }

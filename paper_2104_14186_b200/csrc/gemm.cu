@@ -579,6 +579,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   int BMt = 128, splits = 1;
   double best = 1e30;
   for (int bm : {128, 64, 32}) {
+    if (ex.force_bm && bm != ex.force_bm) continue;
     if (nb_ > 1 && (M % bm || N % bm)) continue;  // batched items must tile exactly
     const int64_t tm = (M + bm - 1) / bm, tn = (N + bm - 1) / bm;
     const int64_t tiles = (ex.out != OutMode::Full) ? tn * (tn + 1) / 2 : tm * tn;

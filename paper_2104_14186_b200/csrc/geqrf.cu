@@ -271,7 +271,9 @@ __global__ void __launch_bounds__(64 * NRG, 1)
   __syncthreads();
 
   // cross-CTA sum of the per-row-group partials in `red` -> tot
-  auto reduce = [&](int col) {
+  // side(): work for threads that are not on the reduction's critical path
+  // (snapshot writes), run while the partials are in flight
+  auto reduce = [&](int col, auto&& side) {
     double* mine = part + (col & 1) * (2 * kBW);
     if (tid < 2 * kBW) {
       double s = 0.0;
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
         const double x = mine[2 * tid], y = mine[2 * tid + 1];
         for (int p = 0; p < nb_; ++p) st_async_v2(mapa_u32(src, p), x, y, mapa_u32(mb, p));
       }
+      side();
       if (tid < 2 * kBW) {
         mbar_wait_cluster(&mbar[q], (col >> 1) & 1);
         double s = 0.0;
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
         const int cc = tid % kBW;
         if (cc < b && cc >= col && mine[tid] != 0.0) atomicAdd(&buf[tid], mine[tid]);
       }
+      side();
       grid_sync(bar, epoch);
       if (tid < 2 * kBW) tot[tid] = __ldcg(&buf[tid]);
       if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     red[rg * 2 * kBW + c] = top;
     red[rg * 2 * kBW + kBW + c] = below;
     __syncthreads();
-    reduce(0);
+    reduce(0, [] {});
   }
 
   // Snapshot conventions (shared memory, per parity):
@@ -368,13 +372,11 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     double sc = 0.0, s1 = 0.0;
     if (reflect && c > jj && c < b) sc = taup * (tot[c] + tot[kBW + c] * inv_v0) * inv_v0;
     if (reflect && jj + 1 < b) s1 = taup * (tot[jj + 1] + tot[kBW + jj + 1] * inv_v0) * inv_v0;
-    if (tid == 0) {
+    if (tid == 0) {  // read after the last step's barriers
       colsc[jj] = reflect ? inv_v0 : 0.0;
       colsc[kBW + jj] = beta;
-      if (jj >= rbeg && jj < rbeg + nr) U[jj - rbeg] = v0;
     }
     if (blockIdx.x == 0 && tid == 0) tau_out[jj] = taup;
-    __syncthreads();
     PANEL_MARK(9, jj);
     double top = 0.0, below = 0.0;
     const int kmask = jj + 1 - rbeg - rg;  // element t has row <= jj+1 iff NRG*t <= kmask
@@ -396,7 +398,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
           const int i = rg + NRG * t;
-          const double u = U[i];
+          const double u = (NRG * t == kmask - 1) ? v0 : U[i];  // row jj: u = v0 (v = 1)
           const double pv = fma(-s1, u, P[i]);
           const double an = fma(-sc, u, a[t]);
           a[t] = an;
@@ -412,21 +414,24 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     }
     PANEL_MARK(10, jj);
     if (!((jj + 1 < b) && c < b && c > jj)) top = below = 0.0;
-    // snapshots of columns jj+1 (zero above its diagonal) and jj+2 (owners only)
-    if (c == jj + 1) {
+    // snapshots of columns jj+1 (zero above its diagonal) and jj+2 (owners
+    // only), written while the partial sums are in flight
+    auto snapshots = [&] {
+      if (c == jj + 1) {
 #pragma unroll
-      for (int t = 0; t < RPT; ++t) Un[rg + NRG * t] = (NRG * t < kmask) ? 0.0 : a[t];
-    } else if (c == jj + 2) {
+        for (int t = 0; t < RPT; ++t) Un[rg + NRG * t] = (NRG * t < kmask) ? 0.0 : a[t];
+      } else if (c == jj + 2) {
 #pragma unroll
-      for (int t = 0; t < RPT; ++t) Pn[rg + NRG * t] = a[t];
-    }
+        for (int t = 0; t < RPT; ++t) Pn[rg + NRG * t] = a[t];
+      }
+    };
     if (jj + 1 < b) {
       red[rg * 2 * kBW + c] = top;
       red[rg * 2 * kBW + kBW + c] = below;
       PANEL_MARK(11, jj);
       __syncthreads();
       PANEL_MARK(12, jj);
-      reduce(jj + 1);
+      reduce(jj + 1, snapshots);
       PANEL_MARK(13, jj);
     }
   }
@@ -648,11 +653,8 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
     launch_panel_reg<true, 16>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
     return true;
   }
-  if (ceil_div(mp, 8 * 32) <= csmax) {
-    const int cs = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, cs);
-    launch_panel_reg<true, 32>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
-    return true;
-  }
+  // (a 16-CTA cluster of 256-row CTAs is slower than the grid path at 4096
+  // rows: 3.13 vs 2.60 us/column — the per-column register pass dominates)
   // cooperative grid (FP64 atomics + grid barrier)
   if (ceil_div(mp, 8 * 8) <= ctx.num_sms) {
     const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
@@ -774,6 +776,17 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     SW2 = ctx.arena->alloc(nbo, n);
   }
   bool side_pending = false;
+  // with look-ahead the latency-bound chain (panels, inner updates, next-block
+  // update) runs on the high-priority stream so the side stream's big GEMM
+  // tiles yield SMs to it as they retire
+  cudaStream_t caller = ctx.stream;
+  static const bool no_prio = getenv("QDWHG_NO_PRIORITY") != nullptr;
+  const bool use_hi = lookahead && !no_prio && ctx.hi != nullptr;
+  if (use_hi) {
+    QDWHG_CUDA(cudaEventRecord(ctx.ev_main, caller));
+    QDWHG_CUDA(cudaStreamWaitEvent(ctx.hi, ctx.ev_main, 0));
+    ctx.stream = ctx.hi;
+  }
   const Arena::Mark mark = ctx.arena->mark();
   for (int64_t po = 0; po < nout; ++po) {
     const int64_t jo = po * nbo;
@@ -855,16 +868,30 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
         ctx.stream = ctx.side;
         QDWHG_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_main, 0));
         const int64_t nr = nc - bn;
-        const DMat C = A.sub(jo, jo + bo + bn, mo, nr);
-        const DMat W1 = SW1.sub(0, 0, bo, nr), W2 = SW2.sub(0, 0, bo, nr);
+        // The side GEMMs run in column chunks of at most ~64 128x128 tiles:
+        // the next panel is a cooperative launch that needs its SMs free at
+        // once, so the side stream must never occupy the whole machine.
         GemmExtra e0;
         e0.split_k = 1;  // no arena scratch on the side stream
-        gemm(ctx, Op::T, Op::N, 1.0, Vo, C, 0.0, W1, e0);
+        e0.force_bm = 128;
         GemmExtra e;
         e.krange = KRange::ALower;
         e.split_k = 1;
-        gemm(ctx, Op::T, Op::N, 1.0, To, W1, 0.0, W2, e);
-        gemm(ctx, Op::N, Op::N, -1.0, Vo, W2, 1.0, C, e0);
+        e.force_bm = 128;
+        const int64_t cap_tiles = 64;
+        const int64_t cw1 = std::max<int64_t>(128, (cap_tiles / ((bo + 127) / 128)) * 128);
+        const int64_t cw2 = std::max<int64_t>(128, (cap_tiles / ((mo + 127) / 128)) * 128);
+        const DMat C = A.sub(jo, jo + bo + bn, mo, nr);
+        const DMat W1 = SW1.sub(0, 0, bo, nr), W2 = SW2.sub(0, 0, bo, nr);
+        for (int64_t c0 = 0; c0 < nr; c0 += cw1) {
+          const int64_t w = std::min(cw1, nr - c0);
+          gemm(ctx, Op::T, Op::N, 1.0, Vo, C.col_block(c0, w), 0.0, W1.col_block(c0, w), e0);
+          gemm(ctx, Op::T, Op::N, 1.0, To, W1.col_block(c0, w), 0.0, W2.col_block(c0, w), e);
+        }
+        for (int64_t c0 = 0; c0 < nr; c0 += cw2) {
+          const int64_t w = std::min(cw2, nr - c0);
+          gemm(ctx, Op::N, Op::N, -1.0, Vo, W2.col_block(c0, w), 1.0, C.col_block(c0, w), e0);
+        }
         QDWHG_CUDA(cudaEventRecord(ctx.ev_side, ctx.stream));
         ctx.stream = main_stream;
         side_pending = true;
@@ -874,6 +901,11 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     }
   }
   if (side_pending) QDWHG_CUDA(cudaStreamWaitEvent(ctx.stream, ctx.ev_side, 0));
+  if (use_hi) {
+    QDWHG_CUDA(cudaEventRecord(ctx.ev_main, ctx.hi));
+    QDWHG_CUDA(cudaStreamWaitEvent(caller, ctx.ev_main, 0));
+    ctx.stream = caller;
+  }
 }
 
 void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, const DMat& Q) {
@@ -905,6 +937,32 @@ void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, con
     e.krange = KRange::AUpper;  // T upper
     gemm(ctx, Op::N, Op::N, 1.0, Tp, W1, 0.0, W2, e);
     gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, C);
+    ctx.arena->release_to(mark);
+  }
+}
+
+void ormqr_left(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, const DMat& C) {
+  // C <- Q C with Q = H_0 ... H_{p-1} of geqrf (p = min(m-1, n)): blocks applied
+  // last to first, C(j0:, :) -= V T (V^T C(j0:, :)) — ORGQR without the
+  // identity start, so Q (m x n) never has to be formed when only Q M is needed
+  const int64_t nc = C.cols;
+  const int nb = w.nb;
+  const int64_t npan = (n + nb - 1) / nb;
+  const Arena::Mark mark = ctx.arena->mark();
+  for (int64_t p = npan - 1; p >= 0; --p) {
+    const int64_t j0 = p * nb;
+    const int64_t b = std::min<int64_t>(nb, n - j0);
+    const int64_t mp = m - j0;
+    const DMat Vp = w.V.sub(j0, j0, mp, b);
+    const DMat Tp = w.T.sub(0, p * nb, b, b);
+    const DMat Cp = C.sub(j0, 0, mp, nc);
+    DMat W1 = ctx.arena->alloc(b, nc);
+    DMat W2 = ctx.arena->alloc(b, nc);
+    gemm(ctx, Op::T, Op::N, 1.0, Vp, Cp, 0.0, W1);
+    GemmExtra e;
+    e.krange = KRange::AUpper;  // T upper
+    gemm(ctx, Op::N, Op::N, 1.0, Tp, W1, 0.0, W2, e);
+    gemm(ctx, Op::N, Op::N, -1.0, Vp, W2, 1.0, Cp);
     ctx.arena->release_to(mark);
   }
 }

@@ -100,7 +100,8 @@ enum class OutMode { Full, LowerMirror, Lower };
 
 struct Ctx {
   cudaStream_t stream = nullptr;
-  cudaStream_t side = nullptr;        // look-ahead stream (handle-owned)
+  cudaStream_t side = nullptr;        // look-ahead stream (handle-owned, lowest priority)
+  cudaStream_t hi = nullptr;          // critical-path stream (handle-owned, highest priority)
   cudaEvent_t ev_main = nullptr, ev_side = nullptr;  // cross-stream ordering
   Arena* arena = nullptr;
   int num_sms = 148;
@@ -152,6 +153,7 @@ struct GemmExtra {
   const DMat* cin = nullptr;
   double diag_add = 0.0;
   int split_k = 0;  // 0 = automatic
+  int force_bm = 0;  // 0 = automatic; 128 / 64 / 32 pins the tile size
   // Batched launch: item b uses A/B/C shifted by b * (step_r rows, step_c cols)
   // of their stored matrices (items must tile exactly; no split-K).
   int batch = 1;
@@ -205,6 +207,8 @@ struct QrWork {
 void geqrf(Ctx& ctx, const DMat& A, QrWork& work);
 // Q(:, c0 : c0+ncols) of the m x m Q = H_0 H_1 ... H_{p-1} into Qout (m x ncols).
 void orgqr_cols(Ctx& ctx, const QrWork& work, int64_t m, int64_t p, int64_t c0, const DMat& Qout);
+// C <- Q C (C is m x ncols, Q = H_0 ... H_{p-1} of an m x n geqrf).
+void ormqr_left(Ctx& ctx, const QrWork& work, int64_t m, int64_t n, const DMat& C);
 // diag(R) to host (n values).
 void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d);
 

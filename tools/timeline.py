@@ -19,7 +19,18 @@ X = (G / (G.norm() ** 0.5)).t().contiguous().t()
 Z = (G.T @ G / n + torch.eye(n, dtype=torch.float64, device=dev)).t().contiguous().t()
 
 
+Ysvd = None
+if what == "svd":
+    m2 = int(sys.argv[4]) if len(sys.argv) > 4 else 8 * n
+    q1, _ = qdwh.qr_factor(qdwh.gaussian_matrix_device(m2, n, 5, handle=h), handle=h)
+    q2, _ = qdwh.qr_factor(qdwh.gaussian_matrix_device(n, n, 6, handle=h), handle=h)
+    sig = 1.0 / torch.arange(1, n + 1, dtype=torch.float64, device=dev)
+    Ysvd = ((q1[:, :n] * sig[None, :]) @ q2.T).t().contiguous().t()
+
+
 def call():
+    if what == "svd":
+        return qdwh.svd_dense(Ysvd, handle=h)
     if what == "chol":
         return qdwh.qdwh_chol_step(X, 0.5, handle=h)
     if what == "qr":
@@ -47,7 +58,7 @@ for e in ev:
     a = agg.setdefault(name, [0, 0.0])
     a[0] += 1
     a[1] += en - st
-    if len(sys.argv) > 3:
+    if len(sys.argv) > 3 and sys.argv[3] == "v":
         print(f"{(st - t0):9.1f} us  dur {en - st:8.1f}  gap {gap:6.1f}  {name}")
     prev_end = max(prev_end, en)
 print(f"span {prev_end - t0:.1f} us, busy {sum(v[1] for v in agg.values()):.1f} us, gaps {tot_gap:.1f} us")
