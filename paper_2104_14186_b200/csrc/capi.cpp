@@ -266,6 +266,7 @@ qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
     }
     QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_main, cudaEventDisableTiming));
     QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_side, cudaEventDisableTiming));
+    QDWHG_CUDA(cudaEventCreateWithFlags(&h->ctx.ev_side2, cudaEventDisableTiming));
     h->ctx.arena = &h->arena;
     h->ctx.num_sms = sms;
     QDWHG_CUDA(cudaMalloc(&h->ctx.dscratch, 1 << 16));
@@ -294,6 +295,7 @@ qdwhg_status qdwhg_destroy(qdwhg_handle* h) {
   cudaStreamDestroy(h->ctx.hi);
   cudaEventDestroy(h->ctx.ev_main);
   cudaEventDestroy(h->ctx.ev_side);
+  cudaEventDestroy(h->ctx.ev_side2);
   cudaStreamDestroy(h->stream);
   delete h;
   return QDWHG_OK;

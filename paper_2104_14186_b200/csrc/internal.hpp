@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <cstdlib>
 #include <utility>
 #include <stdexcept>
@@ -102,7 +103,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // look-ahead stream (handle-owned, lowest priority)
   cudaStream_t hi = nullptr;          // critical-path stream (handle-owned, highest priority)
-  cudaEvent_t ev_main = nullptr, ev_side = nullptr;  // cross-stream ordering
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr, ev_side2 = nullptr;  // cross-stream ordering
   Arena* arena = nullptr;
   int num_sms = 148;
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
@@ -193,6 +194,11 @@ void zero_strict_lower(Ctx& ctx, const DMat& X);
 // only for the QDWH Cholesky steps where kappa(Z) <= 1 + c).
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false,
                              bool stable = true);
+
+// Top-level split of the fast variant with overlap hooks (see potrf.cu).
+void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
+                      const std::function<void()>& z22_ready,
+                      const std::function<void()>& left_done);
 
 // ------------------------------------------------------------------ geqrf.cu
 struct QrWork {

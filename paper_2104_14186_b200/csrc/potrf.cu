@@ -13,6 +13,7 @@
 // A non-positive pivot raises the device flag; the host turns it into
 // NotPositiveDefinite, matching kernels.cpp:136-138.
 #include <cstdlib>
+#include <functional>
 
 #include "common.cuh"
 #include "internal.hpp"
@@ -457,6 +458,50 @@ void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int6
 }
 
 }  // namespace
+
+// Top level of the fast recursive Cholesky-and-inverse with hooks so a caller
+// can overlap independent work on its side stream (qdwh_chol_step):
+//   z22_ready(): enqueued right before Z22 is first read (the caller may have
+//                produced Z22 on another stream and waits for it here);
+//   left_done(): enqueued once W11 and W11^-1 are final (they are not written
+//                again), e.g. to start Y(:, 0:n1) = X(:, 0:n1) W11^-1.
+// Z is overwritten (lower triangle workspace), Winv receives W^-1 (upper).
+void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
+                      const std::function<void()>& z22_ready,
+                      const std::function<void()>& left_done) {
+  const int64_t n = Z.rows;
+  const int nb = 128;
+  if (n1 % nb || n1 <= 0 || n1 >= n) throw InvalidArgument("potrf_fast_split: bad split");
+  QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat W = ctx.arena->alloc(n, n);
+  fill(ctx, W, 0.0, 0.0);
+  fill(ctx, Winv, 0.0, 0.0);
+  const int64_t n2 = n - n1;
+  chol_inv_rec(ctx, Z, W, Winv, 0, n1, nb);
+  left_done();
+  GemmExtra e1;
+  e1.krange = KRange::ALower;  // op(A) = W11^-T lower
+  gemm(ctx, Op::T, Op::T, 1.0, Winv.sub(0, 0, n1, n1), Z.sub(n1, 0, n2, n1), 0.0, W.sub(0, n1, n1, n2), e1);
+  z22_ready();
+  GemmExtra e2;
+  e2.out = OutMode::Lower;
+  const DMat W12 = W.sub(0, n1, n1, n2);
+  gemm(ctx, Op::T, Op::N, -1.0, W12, W12, 1.0, Z.sub(n1, n1, n2, n2), e2);
+  chol_inv_rec(ctx, Z, W, Winv, n1, n2, nb);
+  DMat T = ctx.arena->alloc(n1, n2);
+  GemmExtra e3;
+  e3.krange = KRange::BUpper;  // W22^-1 upper
+  gemm(ctx, Op::N, Op::N, 1.0, W12, Winv.sub(n1, n1, n2, n2), 0.0, T, e3);
+  GemmExtra e4;
+  e4.krange = KRange::AUpper;  // W11^-1 upper
+  gemm(ctx, Op::N, Op::N, -1.0, Winv.sub(0, 0, n1, n1), T, 0.0, Winv.sub(0, n1, n1, n2), e4);
+  int hflag = 0;
+  QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  ctx.arena->release_to(mark);
+  if (hflag) throw NotPositiveDefinite("cholesky: pivot is not positive");
+}
 
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w, bool stable) {
   const int64_t n = Z.rows;
