@@ -166,6 +166,7 @@ typedef struct qdwhg_kernel_stats {
   uint64_t gemm_timed_launches; /* since the last get_kernel_stats */
   double gemm_seconds;          /* sum of event-timed GEMM durations */
   double gemm_flops;            /* sum of algorithmic flops of those launches */
+  double gemm_busy_seconds;     /* union of the launch intervals (concurrent launches counted once) */
 } qdwhg_kernel_stats;
 qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable);
 qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out);

@@ -57,7 +57,7 @@ class PolarInfo(ctypes.Structure):
 
 class KernelStats(ctypes.Structure):
     _fields_ = [("gemm_launches", _U64), ("other_launches", _U64), ("gemm_timed_launches", _U64),
-                ("gemm_seconds", _D), ("gemm_flops", _D)]
+                ("gemm_seconds", _D), ("gemm_flops", _D), ("gemm_busy_seconds", _D)]
 
 
 class EigRequest(ctypes.Structure):

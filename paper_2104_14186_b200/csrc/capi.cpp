@@ -94,6 +94,27 @@ void Ctx::prof_collect() {
   QDWHG_CUDA(cudaEventSynchronize(ev_pool[2 * ev_used - 1]));
   static const char* log_path = getenv("QDWHG_PROFILE_LOG");
   FILE* log = log_path ? fopen(log_path, "a") : nullptr;
+  // union of the launch intervals (GEMMs on the main and side streams may run
+  // concurrently: the busy time must not count the overlap twice)
+  std::vector<std::pair<float, float>> iv(ev_used);
+  for (size_t i = 0; i < ev_used; ++i) {
+    QDWHG_CUDA(cudaEventElapsedTime(&iv[i].first, ev_pool[0], ev_pool[2 * i]));
+    QDWHG_CUDA(cudaEventElapsedTime(&iv[i].second, ev_pool[0], ev_pool[2 * i + 1]));
+  }
+  std::sort(iv.begin(), iv.end());
+  {
+    float cs = iv[0].first, ce = iv[0].second;
+    for (size_t i = 1; i < iv.size(); ++i) {
+      if (iv[i].first > ce) {
+        gemm_busy_ms += ce - cs;
+        cs = iv[i].first;
+        ce = iv[i].second;
+      } else {
+        ce = std::max(ce, iv[i].second);
+      }
+    }
+    gemm_busy_ms += ce - cs;
+  }
   for (size_t i = 0; i < ev_used; ++i) {
     float ms = 0.f;
     QDWHG_CUDA(cudaEventElapsedTime(&ms, ev_pool[2 * i], ev_pool[2 * i + 1]));
@@ -338,8 +359,10 @@ qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out) {
     out->gemm_timed_launches = h->ctx.gemm_timed;
     out->gemm_seconds = h->ctx.gemm_ms * 1e-3;
     out->gemm_flops = h->ctx.gemm_flops;
+    out->gemm_busy_seconds = h->ctx.gemm_busy_ms * 1e-3;
     h->ctx.gemm_timed = 0;
     h->ctx.gemm_ms = 0.0;
+    h->ctx.gemm_busy_ms = 0.0;
     h->ctx.gemm_flops = 0.0;
   });
 }

@@ -119,7 +119,7 @@ struct Ctx {
   std::vector<double> ev_flops;  // algorithmic flops of launch i (events 2i, 2i+1)
   std::vector<std::string> ev_tag;  // per-launch shape tag (QDWHG_PROFILE_LOG)
   size_t ev_used = 0;
-  double gemm_ms = 0.0, gemm_flops = 0.0;
+  double gemm_ms = 0.0, gemm_flops = 0.0, gemm_busy_ms = 0.0;
   uint64_t gemm_timed = 0;
   void prof_begin(double flops, const std::string& tag = std::string());
   void prof_end();

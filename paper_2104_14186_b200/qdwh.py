@@ -90,7 +90,7 @@ class Handle:
         self.check(self.lib.qdwhg_get_kernel_stats(self.h, ctypes.byref(st)))
         return dict(gemm_launches=st.gemm_launches, other_launches=st.other_launches,
                     gemm_timed_launches=st.gemm_timed_launches, gemm_seconds=st.gemm_seconds,
-                    gemm_flops=st.gemm_flops)
+                    gemm_flops=st.gemm_flops, gemm_busy_seconds=st.gemm_busy_seconds)
 
     def close(self):
         if self.h:
