@@ -441,7 +441,15 @@ double algorithmic_flops(const GemmParams& p) {
     const double full = std::min(len, kmax);
     return full * (full + 1) / 2 + std::max(0.0, len - kmax) * kmax;
   };
-  if (p.omode != (int)OutMode::Full) return K * N * (N + 1);
+  if (p.omode != (int)OutMode::Full) {
+    if ((KRange)p.kmode == KRange::AUpper) {
+      // lower tiles, k from the row index: sum_i 2 (i+1)(K-i)  (LAUUM-shaped)
+      double f = 0.0;
+      for (int64_t i = 0; i < p.N; ++i) f += 2.0 * (double)(i + 1) * std::max(0.0, K - (double)i);
+      return f;
+    }
+    return K * N * (N + 1);
+  }
   switch ((KRange)p.kmode) {
     case KRange::BUpper: return 2 * M * tri(M, N, K);
     case KRange::BLower: return 2 * M * tri(M, std::min(N, K), K);  // sum_j (K - j)
