@@ -421,26 +421,52 @@ static void syev_dc(Ctx& ctx, const DMat& A, std::vector<double>& vals, const DM
   ctx.arena->release_to(mark);
 }
 
-bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
+                  double vhi, int64_t* sel0);
 
 void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
+  int64_t i0;
+  syev_range(ctx, S, vals, Vout, -INFINITY, INFINITY, &i0);
+}
+
+int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
+                   double vhi, int64_t* sel0) {
   // Jacobi (n <= 32) / tridiagonal + bisection + inverse iteration (faster and
   // better orthogonality from n ~ 48 up: measured 0.87 vs 0.96 ms at n = 49,
   // 2.2 vs 12 ms at n = 130); the QDWH spectral divide-and-conquer remains the
-  // fallback for tight clusters.
+  // fallback for tight clusters.  Only the eigenvectors of the eigenvalues in
+  // (vlo, vhi) are formed (the tridiagonal path skips the others entirely).
   static const bool force_dc = getenv("QDWHG_SYEV_DC") != nullptr;
   static const int jac_max =
       getenv("QDWHG_JACOBI_MAX") ? std::min(atoi(getenv("QDWHG_JACOBI_MAX")), kJacobiMaxN) : 32;
-  if (S.rows > jac_max && !force_dc) {
-    if (syev_tridiag(ctx, S, vals, Vout)) return;
+  const int64_t n = S.rows;
+  if (n > jac_max && !force_dc) {
+    if (syev_tridiag(ctx, S, vals, Vout, vlo, vhi, sel0)) {
+      int64_t c = 0;
+      for (double v : vals) c += (v > vlo && v < vhi);
+      return c;
+    }
   }
-  syev_dc(ctx, S, vals, Vout, 0);
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat Wall = ctx.arena->alloc(n, n);
+  syev_dc(ctx, S, vals, Wall, 0);
+  int64_t i0 = 0, i1 = 0;
+  while (i0 < n && !(vals[i0] > vlo)) ++i0;
+  i1 = i0;
+  while (i1 < n && vals[i1] < vhi) ++i1;
+  if (i1 > i0) copy(ctx, Wall.sub(0, i0, n, i1 - i0), Vout.sub(0, 0, n, i1 - i0));
+  ctx.arena->release_to(mark);
+  *sel0 = i0;
+  return i1 - i0;
 }
 
-void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V) {
+int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V,
+                  double cut) {
   // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order.
   // Tall A (m > n) is first reduced to its n x n triangular factor (A = Q R), so
   // every QDWH iteration runs on n x n instead of m x n; U = Q U_R.
+  // All n singular values are returned; singular vectors only for sigma > cut
+  // (their count is returned): U(:, 0:k), V(:, 0:k).
   const int64_t m = A.rows, n = A.cols;
   if (m > n) {
     const Arena::Mark mark = ctx.arena->mark();
@@ -452,13 +478,15 @@ void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigm
     QrWork qw;
     geqrf(ctx, Aw, qw);
     copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
-    svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V);
+    const int64_t k = svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V, cut);
     // U = Q [U_R; 0]: the reflectors applied to U_R directly (no explicit Q,
-    // no m x n x n GEMM)
-    fill(ctx, U.sub(n, 0, m - n, n), 0.0, 0.0);
-    ormqr_left(ctx, qw, m, n, U);
+    // no m x n x k GEMM)
+    if (k > 0) {
+      fill(ctx, U.sub(n, 0, m - n, k), 0.0, 0.0);
+      ormqr_left(ctx, qw, m, n, U.sub(0, 0, m, k));
+    }
     ctx.arena->release_to(mark);
-    return;
+    return k;
   }
   const Arena::Mark mark = ctx.arena->mark();
   DMat Up = ctx.arena->alloc(m, n);
@@ -468,18 +496,21 @@ void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigm
   polar_decompose(ctx, A, cfg, Up, H);
   std::vector<double> vals;
   DMat W = ctx.arena->alloc(n, n);
-  syev(ctx, H, vals, W);
-  // reverse to descending
-  std::vector<int> order(n);
-  for (int64_t j = 0; j < n; ++j) order[j] = (int)(n - 1 - j);
+  int64_t i0 = 0;
+  const int64_t k = syev_range(ctx, H, vals, W, cut, INFINITY, &i0);  // ascending, top-k block
   sigma.resize(n);
-  for (int64_t j = 0; j < n; ++j) sigma[j] = std::max(0.0, vals[order[j]]);
-  permute_cols(ctx, W, order, V);  // V(:, j) = W(:, n-1-j)
-  gemm(ctx, Op::N, Op::N, 1.0, Up, V, 0.0, U);
+  for (int64_t j = 0; j < n; ++j) sigma[j] = std::max(0.0, vals[n - 1 - j]);
+  if (k > 0) {
+    // descending: V(:, j) = W(:, k-1-j)
+    std::vector<int> order(k);
+    for (int64_t j = 0; j < k; ++j) order[j] = (int)(k - 1 - j);
+    permute_cols(ctx, W.sub(0, 0, n, k), order, V.sub(0, 0, n, k));
+    gemm(ctx, Op::N, Op::N, 1.0, Up, V.sub(0, 0, n, k), 0.0, U.sub(0, 0, m, k));
+  }
   ctx.arena->release_to(mark);
+  return k;
 }
 
-// ----------------------------------------------------------------- drivers
 static void check_finite(Ctx& ctx, const DMat& A, const char* who, MatStats* out = nullptr,
                          bool asym = false) {
   if (A.rows == 0 || A.cols == 0) throw InvalidArgument(std::string(who) + ": empty matrix");
@@ -553,7 +584,8 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
   if (clk) clk->mark(4);
   std::vector<double> vals;
   DMat W = ctx.arena->alloc(ell, ell);
-  syev(ctx, S, vals, W);
+  int64_t sel0 = 0;
+  syev_range(ctx, S, vals, W, -INFINITY, 0.0, &sel0);  // vectors for the negative Ritz values only
   if (clk) clk->mark(5);
   double max_abs_ritz = 0.0;
   for (double v : vals) max_abs_ritz = std::max(max_abs_ritz, std::abs(v));
@@ -643,9 +675,9 @@ SvdOut partial_svd(Ctx& ctx, const DMat& A, double s, double s_abs, double tol, 
   if (clk) clk->mark(4);
   DMat Us = ctx.arena->alloc(m, ell), Vs = ctx.arena->alloc(ell, ell);
   std::vector<double> sig;
-  svd_polar(ctx, Y, Us, sig, Vs);
-  if (clk) clk->mark(5);
   const double cutoff = s * out.alpha;
+  svd_polar(ctx, Y, Us, sig, Vs, cutoff);  // vectors only for sigma > cutoff (partial.cpp:151)
+  if (clk) clk->mark(5);
   int64_t k = 0;
   while (k < (int64_t)sig.size() && sig[k] > cutoff) ++k;
   const double l = (double)ell;

@@ -62,7 +62,9 @@ PolarOut polar_decompose(Ctx& ctx, const DMat& A, const PolarCfg& cfg, const DMa
 
 // svd_dense (kernels.cpp:217-330) restated for the device as polar + EIG
 // (fullsolve.cpp:82-103): U (m x n), sigma descending (host), V (n x n).
-void svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V);
+// Returns the number k of singular vectors formed (those with sigma > cut).
+int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V,
+                  double cut = -1.0);
 
 struct EigOut {
   std::vector<double> lambda;  // ascending

@@ -223,6 +223,11 @@ void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d);
 // `vals`, vectors into Vout (n x n).  Jacobi for small n, QDWH spectral
 // divide-and-conquer above the Jacobi cutoff.
 void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
+// All eigenvalues (ascending) into vals; eigenvectors only for the eigenvalues
+// in (vlo, vhi) — a contiguous index range starting at *sel0 — into
+// Vout(:, 0:count).  Returns count.
+int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
+                   double vhi, int64_t* sel0);
 
 // ------------------------------------------------------------------ krylov.cu
 double two_norm_estimate(Ctx& ctx, const DMat& A);

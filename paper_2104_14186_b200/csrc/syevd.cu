@@ -189,12 +189,14 @@ __global__ void bisect_kernel(const double* d, const double* e2, int n, double l
 // Inverse iteration for eigenvalue w[k]: (T - w I) z = b with partial pivoting,
 // 3 solves, normalised.  Z is stored transposed: Zt[k + i*n] = z_k(i).
 // Factor storage (per thread, transposed likewise): u1 diag, u2 super, u3 super2, l, piv.
-__global__ void inviter_kernel(const double* d, const double* e, int n, const double* w,
-                               double tnorm, double* Zt, double* U1, double* U2, double* U3,
-                               double* L, unsigned char* P) {
+__global__ void inviter_kernel(const double* d, const double* e, int n, const double* w, int k0,
+                               int cnt, double tnorm, double* Zt, double* U1, double* U2,
+                               double* U3, double* L, unsigned char* P) {
+  // eigenvector k0 + k (k < cnt); per-thread arrays are stored transposed with
+  // stride cnt: element i of thread k at [k + i*cnt] (coalesced across threads)
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const double lam = w[k];
+  if (k >= cnt) return;
+  const double lam = w[k0 + k];
   const double eps = 2.220446049250313e-16;
   const double tiny = eps * tnorm;
   // ---- LU with partial pivoting of the tridiagonal (dlagtf shape)
@@ -204,7 +206,7 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
     const double cc = e[i];              // sub-diagonal below row i
     const double dn = d[i + 1] - lam;
     const double bn = (i + 2 < n) ? e[i + 1] : 0.0;
-    const size_t o = (size_t)k + (size_t)i * n;
+    const size_t o = (size_t)k + (size_t)i * cnt;
     if (fabs(a) >= fabs(cc)) {
       // no swap: row i stays; multiplier l = cc / a
       const double piv = (a == 0.0) ? tiny : a;
@@ -229,20 +231,20 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
     }
   }
   {
-    const size_t o = (size_t)k + (size_t)(n - 1) * n;
+    const size_t o = (size_t)k + (size_t)(n - 1) * cnt;
     U1[o] = (a == 0.0) ? tiny : a;
     U2[o] = 0.0;
     U3[o] = 0.0;
   }
   // ---- iterations: forward apply L (with pivots), back-solve U
   // start vector: ones (dstein uses random; ones is adequate after 3 solves)
-  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] = 1.0;
+  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] = 1.0;
   for (int it = 0; it < 3; ++it) {
     if (it > 0) {
       // forward: apply the row swaps/multipliers to the rhs
       for (int i = 0; i < n - 1; ++i) {
-        const size_t o = (size_t)k + (size_t)i * n;
-        double zi = Zt[o], zn = Zt[o + n];
+        const size_t o = (size_t)k + (size_t)i * cnt;
+        double zi = Zt[o], zn = Zt[o + cnt];
         if (P[o]) {
           const double t = zi;
           zi = zn;
@@ -250,13 +252,13 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
         }
         zn -= L[o] * zi;
         Zt[o] = zi;
-        Zt[o + n] = zn;
+        Zt[o + cnt] = zn;
       }
     }
     // back substitution U z = rhs, with scaling against overflow
     double z2 = 0.0, z1 = 0.0, nrm = 0.0;
     for (int i = n - 1; i >= 0; --i) {
-      const size_t o = (size_t)k + (size_t)i * n;
+      const size_t o = (size_t)k + (size_t)i * cnt;
       double v = Zt[o] - U2[o] * z1 - U3[o] * z2;
       v /= U1[o];
       Zt[o] = v;
@@ -266,29 +268,29 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
     }
     // normalise (inf-norm first, then 2-norm at the end)
     const double s = (nrm > 0.0) ? 1.0 / nrm : 1.0;
-    for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] *= s;
+    for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] *= s;
   }
   double s2 = 0.0;
   for (int i = 0; i < n; ++i) {
-    const double v = Zt[(size_t)k + (size_t)i * n];
+    const double v = Zt[(size_t)k + (size_t)i * cnt];
     s2 += v * v;
   }
   const double inv = 1.0 / sqrt(s2);
-  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * n] *= inv;
+  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] *= inv;
 }
 
-// Z(i, k) = Zt[k + i*n]
-__global__ void transpose_kernel(const double* Zt, int n, double* Z, int64_t ldz) {
+// Z(i, k) = Zt[k + i*cnt]   (i < n rows, k < cnt vectors)
+__global__ void transpose_kernel(const double* Zt, int n, int cnt, double* Z, int64_t ldz) {
   __shared__ double tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int i = by + r, k = bx + threadIdx.x;
-    tile[r][threadIdx.x] = (i < n && k < n) ? Zt[(size_t)k + (size_t)i * n] : 0.0;
+    tile[r][threadIdx.x] = (i < n && k < cnt) ? Zt[(size_t)k + (size_t)i * cnt] : 0.0;
   }
   __syncthreads();
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int k = bx + r, i = by + threadIdx.x;
-    if (i < n && k < n) Z[i + (int64_t)k * ldz] = tile[threadIdx.x][r];
+    if (i < n && k < cnt) Z[i + (int64_t)k * ldz] = tile[threadIdx.x][r];
   }
 }
 
@@ -302,7 +304,8 @@ __global__ void square_kernel(const double* e, int n, double* e2) {
 void syev_dc_fallback(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
 
 // Returns false if the eigenvectors could not be orthogonalised cheaply (caller falls back).
-bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
+bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
+                  double vhi, int64_t* sel0) {
   const int n = (int)S.rows;
   const Arena::Mark mark = ctx.arena->mark();
   DMat A = ctx.arena->alloc(n, n);
@@ -370,21 +373,36 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   const double pivmin = std::max(1e-300, eps * eps * tnorm * tnorm * 1e-10);
   bisect_kernel<<<(32 * n + 127) / 128, 128, 0, ctx.stream>>>(dd, e2, n, lo, hi, pivmin, 2 * eps * tnorm * 1e-3,
                                                      wv);
-  const size_t nn = (size_t)n * n;
-  double* Zt = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
-  double* U1 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
-  double* U2 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
-  double* U3 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
-  double* Lm = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nn));
-  unsigned char* Pv = static_cast<unsigned char*>(ctx.arena->alloc_bytes(nn));
-  inviter_kernel<<<(n + 63) / 64, 64, 0, ctx.stream>>>(dd, ee, n, wv, tnorm, Zt, U1, U2, U3, Lm, Pv);
-  DMat Z = ctx.arena->alloc(n, n);
-  transpose_kernel<<<dim3((n + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx.stream>>>(Zt, n, Z.ptr(),
-                                                                                     Z.ld);
+  // eigenvalues to the host now: only the selected eigenvectors are formed
+  vals.resize(n);
+  QDWHG_CUDA(cudaMemcpyAsync(vals.data(), wv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  int i0 = 0;
+  while (i0 < n && !(vals[i0] > vlo)) ++i0;
+  int i1 = i0;
+  while (i1 < n && vals[i1] < vhi) ++i1;
+  const int cnt = i1 - i0;
+  *sel0 = i0;
+  if (cnt == 0) {
+    ctx.arena->release_to(mark);
+    return true;
+  }
+  const size_t nc = (size_t)n * cnt;
+  double* Zt = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
+  double* U1 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
+  double* U2 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
+  double* U3 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
+  double* Lm = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
+  unsigned char* Pv = static_cast<unsigned char*>(ctx.arena->alloc_bytes(nc));
+  inviter_kernel<<<(cnt + 63) / 64, 64, 0, ctx.stream>>>(dd, ee, n, wv, i0, cnt, tnorm, Zt, U1, U2, U3,
+                                                        Lm, Pv);
+  DMat Z = ctx.arena->alloc(n, cnt);
+  transpose_kernel<<<dim3((cnt + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx.stream>>>(
+      Zt, n, cnt, Z.ptr(), Z.ld);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count(4);
   // ---- Lowdin: E = Z^T Z - I;  Z <- Z (I - E/2 + 3/8 E^2)
-  DMat E = ctx.arena->alloc(n, n);
+  DMat E = ctx.arena->alloc(cnt, cnt);
   GemmExtra gr;
   gr.out = OutMode::LowerMirror;
   gr.diag_add = -1.0;
@@ -394,15 +412,14 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     ctx.arena->release_to(mark);
     return false;
   }
-  DMat F = ctx.arena->alloc(n, n);
+  DMat F = ctx.arena->alloc(cnt, cnt);
   GemmExtra f2;
   f2.cin = &E;  // F = 3/8 E^2 - 1/2 E + I
   f2.diag_add = 1.0;
   gemm(ctx, Op::N, Op::N, 0.375, E, E, -0.5, F, f2);
-  DMat Z2 = ctx.arena->alloc(n, n);
-  gemm(ctx, Op::N, Op::N, 1.0, Z, F, 0.0, Z2);
-  // ---- back-transform: Vout = Q Z2, Q = H_0 ... H_{n-2}, blocks applied last to first
-  copy(ctx, Z2, Vout);
+  // ---- back-transform: Vout = Q Z F, Q = H_0 ... H_{n-2}, blocks applied last to first
+  const DMat Vsel = Vout.sub(0, 0, n, cnt);
+  gemm(ctx, Op::N, Op::N, 1.0, Z, F, 0.0, Vsel);
   DMat G = ctx.arena->alloc(nb, nb), Tb = ctx.arena->alloc(nb, nb);
   for (int p = npan - 1; p >= 0; --p) {
     const int j0 = p * nb;
@@ -413,8 +430,8 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     gemm(ctx, Op::T, Op::N, 1.0, Vb, Vb, 0.0, G.sub(0, 0, b, b));
     larft_launch(ctx, G.sub(0, 0, b, b), tau + j0, Tb.sub(0, 0, b, b));
     const Arena::Mark m2 = ctx.arena->mark();
-    DMat W1 = ctx.arena->alloc(b, n), W2 = ctx.arena->alloc(b, n);
-    const DMat C = Vout.sub(r0, 0, mp, n);
+    DMat W1 = ctx.arena->alloc(b, cnt), W2 = ctx.arena->alloc(b, cnt);
+    const DMat C = Vout.sub(r0, 0, mp, cnt);
     gemm(ctx, Op::T, Op::N, 1.0, Vb, C, 0.0, W1);
     GemmExtra eu;
     eu.krange = KRange::AUpper;
@@ -422,9 +439,6 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     gemm(ctx, Op::N, Op::N, -1.0, Vb, W2, 1.0, C);
     ctx.arena->release_to(m2);
   }
-  vals.resize(n);
-  QDWHG_CUDA(cudaMemcpyAsync(vals.data(), wv, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
-  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
   ctx.arena->release_to(mark);
   return true;
 }
