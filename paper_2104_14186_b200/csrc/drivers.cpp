@@ -461,7 +461,7 @@ int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMa
 }
 
 int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V,
-                  double cut) {
+                  double cut, double ell0) {
   // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order.
   // Tall A (m > n) is first reduced to its n x n triangular factor (A = Q R), so
   // every QDWH iteration runs on n x n instead of m x n; U = Q U_R.
@@ -478,7 +478,28 @@ int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& s
     QrWork qw;
     geqrf(ctx, Aw, qw);
     copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
-    const int64_t k = svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V, cut);
+    // l0 for the polar of R: a lower bound of sigma_min(R / alpha) from R^-1
+    // (one triangular inverse, ~n^3/3 flops): sigma_min(R) = 1 / ||R^-1||_2,
+    // estimated by the power iteration with a 2x safety margin, floored by the
+    // guaranteed 1 / ||R^-1||_F.  A good l0 saves QDWH iterations, the QR-based
+    // ones above all (iterations_to_converge: 1e-15 -> 2 QR + 4 Cholesky steps,
+    // 1e-4 -> 1 QR + 3 Cholesky steps).
+    double l0 = 1e-15;
+    {
+      const Arena::Mark m2 = ctx.arena->mark();
+      DMat Ri = ctx.arena->alloc(n, n);
+      if (trtri_upper(ctx, R, Ri)) {
+        const MatStats st = mat_stats(ctx, Ri, false);
+        if (st.nonfinite == 0 && st.fro2 > 0) {
+          const double alpha = two_norm_estimate(ctx, R);  // the polar's own (deterministic) alpha
+          const double inv2 = two_norm_estimate(ctx, Ri);   // ~||R^-1||_2 (x1.05)
+          const double lb = std::max(1.0 / (std::sqrt(st.fro2) * alpha), 1.0 / (2.0 * inv2 * alpha));
+          if (std::isfinite(lb) && lb > l0) l0 = std::min(1.0, lb);
+        }
+      }
+      ctx.arena->release_to(m2);
+    }
+    const int64_t k = svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V, cut, l0);
     // U = Q [U_R; 0]: the reflectors applied to U_R directly (no explicit Q,
     // no m x n x k GEMM)
     if (k > 0) {
@@ -492,7 +513,7 @@ int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& s
   DMat Up = ctx.arena->alloc(m, n);
   DMat H = ctx.arena->alloc(n, n);
   PolarCfg cfg;
-  cfg.ell0 = 1e-15;
+  cfg.ell0 = ell0;
   polar_decompose(ctx, A, cfg, Up, H);
   std::vector<double> vals;
   DMat W = ctx.arena->alloc(n, n);

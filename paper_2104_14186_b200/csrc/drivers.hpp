@@ -64,7 +64,7 @@ PolarOut polar_decompose(Ctx& ctx, const DMat& A, const PolarCfg& cfg, const DMa
 // (fullsolve.cpp:82-103): U (m x n), sigma descending (host), V (n x n).
 // Returns the number k of singular vectors formed (those with sigma > cut).
 int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V,
-                  double cut = -1.0);
+                  double cut = -1.0, double ell0 = 1e-15);
 
 struct EigOut {
   std::vector<double> lambda;  // ascending

@@ -195,6 +195,10 @@ void zero_strict_lower(Ctx& ctx, const DMat& X);
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false,
                              bool stable = true);
 
+// R^{-1} (upper, explicit zeros below) of an upper-triangular R; false if a
+// diagonal entry is zero / non-finite.
+bool trtri_upper(Ctx& ctx, const DMat& R, const DMat& Rinv);
+
 // Top-level split of the fast variant with overlap hooks (see potrf.cu).
 void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
                       const std::function<void()>& z22_ready,

@@ -103,7 +103,7 @@ constexpr int kLDT = 97;  // T (R x 32, R <= 96) leading dimension
 
 __global__ void __launch_bounds__(kDiagThreads, 1)
     potrf_diag_kernel(const double* Z, int64_t ldz, double* W, int64_t ldw, double* Winv,
-                      int64_t ldwi, int nb, int* flag) {
+                      int64_t ldwi, int nb, int* flag, int invert_only) {
   extern __shared__ double sm[];
   double* A = sm;                    // 128 x kLDA, column-major, lower = L (then L^{-1})
   double* Dinv = A + 128 * kLDA;     // 4 blocks of 32 x 33 (column-major, lower)
@@ -118,6 +118,22 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   DIAG_MARK(20);
   griddep_wait();
 
+  if (invert_only) {
+    // Z holds an upper-triangular R: L = R^T is loaded (transposed reads), the
+    // factorisation is skipped, and only L^{-1} (-> Winv = R^{-1}) is formed
+    for (int c = warp; c < nbp; c += kDiagThreads / 32) {
+      double* col = A + c * kLDA;
+      for (int r = lane; r < nbp; r += 32)
+        col[r] = (r >= c && r < nb && c < nb) ? Z[c + (int64_t)r * ldz] : (r == c ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    if (tid < nbp) {
+      const double d = A[tid * kLDA + tid];
+      if (!(d != 0.0) || !isfinite(d)) bad_s = 1;
+      Sinv[tid] = 1.0 / d;
+    }
+    __syncthreads();
+  } else {
   // ---- load: lower triangle by cp.async, identity padding, zero strict upper
   for (int c = warp; c < nbp; c += kDiagThreads / 32) {
     double* col = A + c * kLDA;
@@ -217,8 +233,6 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
     }
     DIAG_MARK(3 + 3 * kb);
   }
-  if (tid == 0 && bad_s) atomicExch(flag, 1);
-
   // ---- W = L^T (upper) with explicit zeros below
   for (int c = warp; c < nb; c += kDiagThreads / 32) {
     double* wc = W + (int64_t)c * ldw;
@@ -226,6 +240,8 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
     for (int r = lane; r < nb; r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
   }
   DIAG_MARK(13);
+  }  // !invert_only
+  if (tid == 0 && bad_s) atomicExch(flag, 1);
 
   // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each:
   // lane j computes column j by forward substitution in registers
@@ -312,7 +328,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   DIAG_MARK(16);
 }
 
-void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk) {
+void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, int invert_only = 0) {
   const size_t smem = (size_t)(128 * kLDA + 4 * kSB * 33 + kSB * kLDT + 128) * 8;
   static bool set = false;
   if (!set) {
@@ -321,7 +337,7 @@ void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk) {
     set = true;
   }
   launch_pdl(ctx, potrf_diag_kernel, dim3(1), dim3(kDiagThreads), smem, Zkk.ptr(), Zkk.ld, Wkk.ptr(),
-             Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag);
+             Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag, invert_only);
   ctx.count();
 }
 
@@ -501,6 +517,29 @@ void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
   ctx.arena->release_to(mark);
   if (hflag) throw NotPositiveDefinite("cholesky: pivot is not positive");
+}
+
+bool trtri_upper(Ctx& ctx, const DMat& R, const DMat& Rinv) {
+  // R^{-1} of an upper-triangular R: 128-block inverses by the leaf kernel in
+  // invert-only mode, then the recursive block assembly used for W^{-1}
+  const int64_t n = R.rows;
+  if (R.cols != n) throw InvalidArgument("trtri: matrix not square");
+  const int nb = 128;
+  QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
+  fill(ctx, Rinv, 0.0, 0.0);
+  for (int64_t k = 0; k < n; k += nb) {
+    const int64_t b = std::min<int64_t>(nb, n - k);
+    launch_diag(ctx, R.sub(k, k, b, b), Rinv.sub(k, k, b, b), Rinv.sub(k, k, b, b), 1);
+  }
+  const int64_t nblk = n / nb;
+  if (n % nb == 0 && (nblk & (nblk - 1)) == 0)
+    trtri_levels(ctx, R, Rinv, n, nb);
+  else
+    trtri_rec(ctx, R, Rinv, 0, n, nb);
+  int hflag = 0;
+  QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  return hflag == 0;
 }
 
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w, bool stable) {
