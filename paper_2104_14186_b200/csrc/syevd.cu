@@ -55,10 +55,24 @@ struct TrdArgs {
   int n, j0, nb;
 };
 
-// One panel of dlatrd (lower).  Columns c = j0 .. j0+nb-1.
+// One panel of dlatrd (lower).  Columns c = j0 .. j0+nb-1, three grid barriers
+// per column:
+//   A   a_c(r) -= sum_t V(r,t) W(c,t) + W(r,t) V(c,t)  (r >= c), with W taken as
+//       W_raw + a2_t V (the rank-one correction of each W column is applied
+//       lazily, see D); partial sums of |a_c(c+2:)|^2 and a_c(c+1)   | barrier
+//   BC  reflector scalars (every CTA), V(:, i) = scal x + (1 - scal x0) e_{c+1}
+//       written, and the SYMV run on the UNnormalised x = a_c(c+1:): y_raw =
+//       A22 x, t1_raw = W_raw^T x, t2_raw = V^T x (linear in x, so the
+//       normalisation is folded in afterwards — no barrier between the
+//       reflector and the SYMV)                                     | barrier
+//   D   y, t1, t2 assembled; w = tau (y - V t1 - W t2); w . v partial sums;
+//       W_raw(:, i) = w                                              | barrier
+//   a2_i = -tau/2 (w . v) is known to every CTA after the last barrier; at the
+//   end of the panel each thread applies W += a2 V to its rows.
 __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) {
   __shared__ double scratch[32];
-  __shared__ double vw[2 * kTrdNB];  // V(c, 0:i), W(c, 0:i)  /  t1, t2
+  __shared__ double vw[2 * kTrdNB];   // V(c, 0:i), W_true(c, 0:i)  /  t1, t2
+  __shared__ double a2s[kTrdNB];      // lazy W corrections
   const int n = a.n;
   const int tid = threadIdx.x;
   const int gtid = blockIdx.x * kTrdThreads + tid;
@@ -71,17 +85,21 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
     double* red = a.red + (i % 4) * 8;
     // zero the slot used two columns ahead (last read before the barrier below)
     if (blockIdx.x == 0 && tid < 8) a.red[((i + 2) % 4) * 8 + tid] = 0.0;
-    // ---- A: a_c(r) -= sum_t V(r,t) W(c,t) + W(r,t) V(c,t), r >= c
+    // ---- A: column update with the panel so far (W_true = W_raw + a2 V)
     if (tid < i) {
-      vw[tid] = a.V[c + (int64_t)tid * a.ldp];
-      vw[kTrdNB + tid] = a.W[c + (int64_t)tid * a.ldp];
+      const double vct = a.V[c + (int64_t)tid * a.ldp];
+      vw[tid] = vct;
+      vw[kTrdNB + tid] = a.W[c + (int64_t)tid * a.ldp] + a2s[tid] * vct;
     }
     __syncthreads();
     double xs = 0.0, alpha_part = 0.0;
     for (int r = c + gtid; r < n; r += gsz) {
       double v = a.A[r + (int64_t)c * a.lda];
-      for (int t = 0; t < i; ++t)
-        v -= a.V[r + (int64_t)t * a.ldp] * vw[kTrdNB + t] + a.W[r + (int64_t)t * a.ldp] * vw[t];
+      for (int t = 0; t < i; ++t) {
+        const double vr = a.V[r + (int64_t)t * a.ldp];
+        const double wr = a.W[r + (int64_t)t * a.ldp] + a2s[t] * vr;
+        v -= vr * vw[kTrdNB + t] + wr * vw[t];
+      }
       a.A[r + (int64_t)c * a.lda] = v;
       if (r >= c + 2) xs += v * v;
       if (r == c + 1) alpha_part = v;
@@ -90,7 +108,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
     block_atomic_sum(xs, &red[0], scratch);
     block_atomic_sum(alpha_part, &red[1], scratch);
     grid_sync(a.bar, epoch);
-    // ---- B: reflector for a_c(c+1 : n)
+    // ---- BC: reflector + SYMV on the unnormalised column
     const double alpha = __ldcg(&red[1]);
     const double xnorm = sqrt(__ldcg(&red[0]));
     double beta = alpha, taui = 0.0, scal = 0.0;
@@ -99,53 +117,63 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       taui = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
+    const double head = 1.0 - scal * alpha;  // v = scal x + head e_{c+1}
     for (int r = gtid; r < n; r += gsz) {
       double v = 0.0;
       if (r == c + 1) v = 1.0;
-      else if (r > c + 1) v = a.A[r + (int64_t)c * a.lda] * scal;
+      else if (r > c + 1) v = __ldcg(&a.A[r + (int64_t)c * a.lda]) * scal;
       a.V[r + (int64_t)i * a.ldp] = v;
     }
     if (gtid == 0) {
       if (c + 1 < n) a.e[c] = beta;
       a.tau[c] = taui;
     }
-    grid_sync(a.bar, epoch);
-    // ---- C: y = A(c+1:n, c+1:n) v  (column dots) and t1 = W^T v, t2 = V^T v
     const int m = n - c - 1;
     const int nvirt = m + 2 * i;
+    const double* xcol = a.A + (int64_t)c * a.lda;  // x(r) = A(r, c), r > c
     for (int jv = gwarp; jv < nvirt; jv += warps_total) {
       const double* col;
       if (jv < m) col = a.A + (int64_t)(c + 1 + jv) * a.lda;
       else if (jv < m + i) col = a.W + (int64_t)(jv - m) * a.ldp;
       else col = a.V + (int64_t)(jv - m - i) * a.ldp;
-      double s = 0.0;
-      for (int r = c + 1 + lane; r < n; r += 32) s += col[r] * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
-      s = warp_sum(s);
-      if (lane == 0) a.y[jv] = s;
+      double sm = 0.0;
+      for (int r = c + 1 + lane; r < n; r += 32) sm += col[r] * __ldcg(&xcol[r]);
+      sm = warp_sum(sm);
+      if (lane == 0) a.y[jv] = sm;
     }
     grid_sync(a.bar, epoch);
-    // ---- D: w = tau (y - V t1 - W t2); alpha2 = w . v; w -= tau/2 alpha2 v
-    if (tid < 2 * i) vw[tid] = __ldcg(&a.y[m + tid]);  // t1 = vw[0:i], t2 = vw[i:2i]
+    // ---- D: w = tau (y - V t1 - W_true t2) with y = scal y_raw + head A22(:, 0),
+    // t = scal t_raw + head (row c+1);  W_true t2 = W_raw t2 + V (a2 .* t2)
+    if (tid < i) {
+      const double t2 = scal * __ldcg(&a.y[m + i + tid]) + head * a.V[(c + 1) + (int64_t)tid * a.ldp];
+      const double wrow = a.W[(c + 1) + (int64_t)tid * a.ldp];
+      const double t1raw = scal * __ldcg(&a.y[m + tid]) + head * wrow;  // W_raw^T v
+      // coefficient of V(:, t): t1_true + a2 t2 = t1raw + 2 a2 t2 (t1_true = t1raw + a2 t2)
+      vw[tid] = t1raw + 2.0 * a2s[tid] * t2;
+      vw[kTrdNB + tid] = t2;
+    }
     __syncthreads();
     double dotp = 0.0;
-    for (int r = c + 1 + gtid; r < n; r += gsz) {
-      double w = __ldcg(&a.y[r - c - 1]);
-      for (int t = 0; t < i; ++t)
-        w -= a.V[r + (int64_t)t * a.ldp] * vw[t] + a.W[r + (int64_t)t * a.ldp] * vw[i + t];
-      w *= taui;
+    for (int r = gtid; r < n; r += gsz) {
+      double w = 0.0;
+      if (r > c) {
+        w = scal * __ldcg(&a.y[r - c - 1]) + head * a.A[r + (int64_t)(c + 1) * a.lda];
+        for (int t = 0; t < i; ++t)
+          w -= a.V[r + (int64_t)t * a.ldp] * vw[t] + a.W[r + (int64_t)t * a.ldp] * vw[kTrdNB + t];
+        w *= taui;
+        dotp += w * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
+      }
       a.W[r + (int64_t)i * a.ldp] = w;
-      dotp += w * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
     }
     block_atomic_sum(dotp, &red[2], scratch);
     grid_sync(a.bar, epoch);
-    const double a2 = -0.5 * taui * __ldcg(&red[2]);
-    for (int r = gtid; r < n; r += gsz) {
-      double* wp = &a.W[r + (int64_t)i * a.ldp];
-      if (r <= c) *wp = 0.0;
-      else *wp += a2 * __ldcg(&a.V[r + (int64_t)i * a.ldp]);
-    }
-    grid_sync(a.bar, epoch);
+    if (tid == 0) a2s[i] = -0.5 * taui * __ldcg(&red[2]);
+    __syncthreads();
   }
+  // ---- W += a2 V (the deferred corrections), rows owned by this thread
+  for (int r = gtid; r < n; r += gsz)
+    for (int t = 0; t < a.nb; ++t)
+      a.W[r + (int64_t)t * a.ldp] += a2s[t] * a.V[r + (int64_t)t * a.ldp];
 }
 
 // Sturm count: number of eigenvalues of T (d, e) strictly below x.
