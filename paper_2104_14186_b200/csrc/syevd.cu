@@ -29,7 +29,15 @@ void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T)
 
 namespace {
 
+#ifdef QDWHG_TRD_TRACE
+__device__ long long g_trd_trace[16];
+#define TRD_MARK(k, col) \
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (col) == 5) g_trd_trace[k] = clock64()
+#else
+#define TRD_MARK(k, col)
+#endif
 constexpr int kTrdThreads = 256;
+constexpr size_t kTrdDynSmem = (kTrdThreads / 32) * (32 * 33 + 64) * sizeof(double);
 constexpr int kTrdNB = 32;
 
 
@@ -49,7 +57,8 @@ struct TrdArgs {
   double* d;    // diag (n)
   double* e;    // sub-diagonal (n-1)
   double* tau;  // n
-  double* y;    // n scratch (SYMV result, with 2*nb extra slots for t1/t2)
+  double* y;    // n scratch (virtual-column dots t1/t2 at [m, m + 2i))
+  double* ypart;  // SYMV tile partials: [TI][TI * 32] (TI = ceil(m / 32)), L2-resident
   double* red;  // 4 x 8 rotating reduction slots
   unsigned* bar;
   int n, j0, nb;
@@ -85,6 +94,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
     double* red = a.red + (i % 4) * 8;
     // zero the slot used two columns ahead (last read before the barrier below)
     if (blockIdx.x == 0 && tid < 8) a.red[((i + 2) % 4) * 8 + tid] = 0.0;
+    TRD_MARK(0, i);
     // ---- A: column update with the panel so far (W_true = W_raw + a2 V)
     if (tid < i) {
       const double vct = a.V[c + (int64_t)tid * a.ldp];
@@ -105,9 +115,12 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       if (r == c + 1) alpha_part = v;
       if (r == c) a.d[c] = v;
     }
+    TRD_MARK(1, i);
     block_atomic_sum(xs, &red[0], scratch);
     block_atomic_sum(alpha_part, &red[1], scratch);
+    TRD_MARK(2, i);
     grid_sync(a.bar, epoch);
+    TRD_MARK(3, i);
     // ---- BC: reflector + SYMV on the unnormalised column
     const double alpha = __ldcg(&red[1]);
     const double xnorm = sqrt(__ldcg(&red[0]));
@@ -128,20 +141,81 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       if (c + 1 < n) a.e[c] = beta;
       a.tau[c] = taui;
     }
+    TRD_MARK(4, i);
     const int m = n - c - 1;
-    const int nvirt = m + 2 * i;
     const double* xcol = a.A + (int64_t)c * a.lda;  // x(r) = A(r, c), r > c
-    for (int jv = gwarp; jv < nvirt; jv += warps_total) {
-      const double* col;
-      if (jv < m) col = a.A + (int64_t)(c + 1 + jv) * a.lda;
-      else if (jv < m + i) col = a.W + (int64_t)(jv - m) * a.ldp;
-      else col = a.V + (int64_t)(jv - m - i) * a.ldp;
-      double sm = 0.0;
-      for (int r = c + 1 + lane; r < n; r += 32) sm += col[r] * __ldcg(&xcol[r]);
-      sm = warp_sum(sm);
-      if (lane == 0) a.y[jv] = sm;
+    // SYMV over the LOWER triangle of A22 only (half the HBM traffic): one warp
+    // per 32x32 lower tile (ti >= tj); the tile serves both y_ti += A x_tj
+    // and (off the diagonal) y_tj += A^T x_ti, accumulated into y by FP64
+    // atomics (y is zeroed row by row in phase D after its use).
+    const int TI = (m + 31) / 32, mpad = TI * 32;
+    const int ntiles = TI * (TI + 1) / 2;
+    {
+      // per-warp 32x33 tile + 64 x values in dynamic shared memory
+      extern __shared__ double trd_dyn[];
+      double(*tl)[33] = reinterpret_cast<double(*)[33]>(trd_dyn + (tid >> 5) * (32 * 33 + 64));
+      double* xw = trd_dyn + (tid >> 5) * (32 * 33 + 64) + 32 * 33;
+      for (int tt = gwarp; tt < ntiles + 2 * i; tt += warps_total) {
+        if (tt >= ntiles) {  // virtual columns: t1_raw = W_raw^T x, t2_raw = V^T x
+          const int jv = tt - ntiles;
+          const double* col = (jv < i) ? a.W + (int64_t)jv * a.ldp : a.V + (int64_t)(jv - i) * a.ldp;
+          double s0 = 0.0, s1 = 0.0;
+          int r = c + 1 + lane;
+          for (; r + 32 < n; r += 64) {
+            s0 = fma(col[r], __ldcg(&xcol[r]), s0);
+            s1 = fma(col[r + 32], __ldcg(&xcol[r + 32]), s1);
+          }
+          if (r < n) s0 = fma(col[r], __ldcg(&xcol[r]), s0);
+          const double sm = warp_sum(s0 + s1);
+          if (lane == 0) a.y[m + jv] = sm;
+          continue;
+        }
+        int tj = 0, rem = tt;  // column-major enumeration of the lower tiles
+        while (rem >= TI - tj) {
+          rem -= TI - tj;
+          ++tj;
+        }
+        const int ti = tj + rem;
+        const int lr = ti * 32 + lane, lc0 = tj * 32;  // local row / first local column
+        const int r = c + 1 + lr;
+        const bool diag = (ti == tj);
+        {
+          // all 32 column loads of the tile in flight at once (8 KB per warp)
+          double v[32];
+          const double* base = a.A + r + (int64_t)(c + 1 + lc0) * a.lda;
+          const int ncol = min(32, m - lc0);
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc)
+            v[cc] = (lr < m && cc < ncol && (!diag || lane >= cc)) ? base[(int64_t)cc * a.lda] : 0.0;
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) tl[lane][cc] = v[cc];
+        }
+        xw[lane] = (lc0 + lane < m) ? __ldcg(&xcol[c + 1 + lc0 + lane]) : 0.0;
+        xw[32 + lane] = (lr < m) ? __ldcg(&xcol[r]) : 0.0;
+        __syncwarp();
+        double yr = 0.0, yc = 0.0;
+        if (diag) {
+#pragma unroll 8
+          for (int cc = 0; cc < 32; ++cc) {
+            const double v = (cc <= lane) ? tl[lane][cc] : tl[cc][lane];
+            yr = fma(v, xw[cc], yr);
+          }
+        } else {
+#pragma unroll 8
+          for (int cc = 0; cc < 32; ++cc) {
+            yr = fma(tl[lane][cc], xw[cc], yr);        // row part: rows of ti
+            yc = fma(tl[cc][lane], xw[32 + cc], yc);   // column part: rows of tj
+          }
+        }
+        // y (zeroed by phase D of the previous column) accumulates by atomics
+        if (lr < m) atomicAdd(&a.y[lr], yr);
+        if (!diag && lc0 + lane < m) atomicAdd(&a.y[lc0 + lane], yc);
+        __syncwarp();
+      }
     }
+    TRD_MARK(5, i);
     grid_sync(a.bar, epoch);
+    TRD_MARK(6, i);
     // ---- D: w = tau (y - V t1 - W_true t2) with y = scal y_raw + head A22(:, 0),
     // t = scal t_raw + head (row c+1);  W_true t2 = W_raw t2 + V (a2 .* t2)
     if (tid < i) {
@@ -157,7 +231,10 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
     for (int r = gtid; r < n; r += gsz) {
       double w = 0.0;
       if (r > c) {
-        w = scal * __ldcg(&a.y[r - c - 1]) + head * a.A[r + (int64_t)(c + 1) * a.lda];
+        const int lr = r - c - 1;
+        const double yraw = __ldcg(&a.y[lr]);
+        a.y[lr] = 0.0;  // ready for the next column's atomics
+        w = scal * yraw + head * a.A[r + (int64_t)(c + 1) * a.lda];
         for (int t = 0; t < i; ++t)
           w -= a.V[r + (int64_t)t * a.ldp] * vw[t] + a.W[r + (int64_t)t * a.ldp] * vw[kTrdNB + t];
         w *= taui;
@@ -165,8 +242,10 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_panel_kernel(TrdArgs a) 
       }
       a.W[r + (int64_t)i * a.ldp] = w;
     }
+    TRD_MARK(7, i);
     block_atomic_sum(dotp, &red[2], scratch);
     grid_sync(a.bar, epoch);
+    TRD_MARK(8, i);
     if (tid == 0) a2s[i] = -0.5 * taui * __ldcg(&red[2]);
     __syncthreads();
   }
@@ -346,11 +425,20 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   double* ee = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
   double* tau = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (npan * nb + 8)));
   double* y = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 2 * nb + 8)));
+  const int64_t tin = (n + 31) / 32;
+  double* ypart = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * tin * tin * 32 + 64));
   double* red = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 64));
   unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
   QDWHG_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (npan * nb + 8), ctx.stream));
   QDWHG_CUDA(cudaMemsetAsync(ee, 0, sizeof(double) * (n + 8), ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (n + 2 * nb + 8), ctx.stream));  // SYMV atomics
   fill(ctx, Vfull, 0.0, 0.0);
+  static bool trd_attr = false;
+  if (!trd_attr) {
+    QDWHG_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kTrdDynSmem));
+    trd_attr = true;
+  }
   // all SMs: the per-column SYMV streams the trailing matrix (HBM/L2 bound)
   const int grid = std::max(1, std::min(ctx.num_sms, (n + 31) / 32));
   for (int p = 0; p < npan; ++p) {
@@ -358,10 +446,10 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     const int b = std::min(nb, n - 1 - j0);
     QDWHG_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * 64, ctx.stream));
     QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
-    TrdArgs args{A.ptr(), A.ld, Vp.ptr(), Wp.ptr(), Vp.ld, dd, ee, tau, y, red, bar, n, j0, b};
+    TrdArgs args{A.ptr(), A.ld, Vp.ptr(), Wp.ptr(), Vp.ld, dd, ee, tau, y, ypart, red, bar, n, j0, b};
     void* kargs[] = {&args};
     QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, dim3(grid), dim3(kTrdThreads),
-                                           kargs, 0, ctx.stream));
+                                           kargs, kTrdDynSmem, ctx.stream));
     ctx.count();
     copy(ctx, Vp.sub(0, 0, n, b), Vfull.sub(0, j0, n, b));
     const int r0 = j0 + b;
@@ -369,8 +457,10 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     if (rest > 0) {
       const DMat Vr = Vp.sub(r0, 0, rest, b), Wr = Wp.sub(r0, 0, rest, b);
       const DMat At = A.sub(r0, r0, rest, rest);
-      gemm(ctx, Op::N, Op::T, -1.0, Vr, Wr, 1.0, At);
-      gemm(ctx, Op::N, Op::T, -1.0, Wr, Vr, 1.0, At);
+      GemmExtra lo;  // the panel kernel reads only the lower triangle of A
+      lo.out = OutMode::Lower;
+      gemm(ctx, Op::N, Op::T, -1.0, Vr, Wr, 1.0, At, lo);
+      gemm(ctx, Op::N, Op::T, -1.0, Wr, Vr, 1.0, At, lo);
     }
   }
   // last diagonal entry (and the one before if the last panel ended early)
