@@ -36,7 +36,7 @@ __device__ long long g_trd_trace[16];
 #else
 #define TRD_MARK(k, col)
 #endif
-constexpr int kTrdThreads = 256;
+constexpr int kTrdThreads = 512;
 constexpr size_t kTrdDynSmem = (kTrdThreads / 32) * (32 * 33 + 64) * sizeof(double);
 constexpr int kTrdNB = 32;
 
