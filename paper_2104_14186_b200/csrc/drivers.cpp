@@ -600,8 +600,9 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
   DMat AQ = ctx.arena->alloc(n, ell);
   gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ);
   DMat S = ctx.arena->alloc(ell, ell);
-  gemm(ctx, Op::T, Op::N, 1.0, Q2, AQ, 0.0, S);
-  symmetrize_scale(ctx, S, 1.0, 0.0, S);
+  GemmExtra rr;  // S = Q2^T (A Q2) is symmetric: lower tiles, mirrored (exactly symmetric)
+  rr.out = OutMode::LowerMirror;
+  gemm(ctx, Op::T, Op::N, 1.0, Q2, AQ, 0.0, S, rr);
   if (clk) clk->mark(4);
   std::vector<double> vals;
   DMat W = ctx.arena->alloc(ell, ell);
