@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(64 * NRG, 1)
   constexpr int RBP = RB + 1;
   extern __shared__ double smem[];
   double* stage = smem;                 // [kBW][RBP]: coalesced load / store staging
-  double* snap = stage + kBW * RBP;     // [2 parity][2: column jj, column jj+1][RB]
+  // [2 parity][RB] x (u, p): column jj and column jj+1 interleaved, so each
+  // row's pair is ONE broadcast 16-byte shared load in the hot loop
+  double* snap = stage + kBW * RBP;
   double* red = snap + 4 * RB;          // [NRG][2*kBW]
   double* part = red + NRG * 2 * kBW;   // [2 parity][2*kBW] this CTA's partials
   double* tot = part + 4 * kBW;         // [2*kBW] reduced (top | below)
@@ -249,8 +251,8 @@ __global__ void __launch_bounds__(64 * NRG, 1)
   for (int t = 0; t < RPT; ++t) {
     const int i = rg + NRG * t;
     a[t] = (c < b && i < nr) ? stage[c * RBP + i] : 0.0;  // rows past nr stay exactly 0
-    if (c == 0) snap[i] = a[t];
-    if (c == 1) snap[RB + i] = a[t];
+    if (c == 0) snap[2 * i] = a[t];
+    if (c == 1) snap[2 * i + 1] = a[t];
   }
   for (int i = tid; i < 2 * RB; i += NT) snap[2 * RB + i] = 0.0;
   if (CLUSTER) {
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
       const int i = rg + NRG * t, gr = rbeg + i;
       if (i < nr && c < b) {
         if (gr == 0) top = a[t];
-        else below = fma(snap[i], a[t], below);
+        else below = fma(snap[2 * i], a[t], below);
       }
     }
     red[rg * 2 * kBW + c] = top;
@@ -352,10 +354,8 @@ __global__ void __launch_bounds__(64 * NRG, 1)
   for (int jj = 0; jj < b; ++jj) {
     PANEL_MARK(8, jj);
     const int par = jj & 1;
-    double* U = snap + par * 2 * RB;
-    const double* P = U + RB;
-    double* Un = snap + (par ^ 1) * 2 * RB;
-    double* Pn = Un + RB;
+    const double2* UP = reinterpret_cast<const double2*>(snap) + par * RB;  // (u, p) per row
+    double* UPn = snap + (par ^ 1) * 2 * RB;                               // next step's pairs
     const double x0 = tot[jj];
     const double sig2 = tot[kBW + jj];
     const double nx2 = x0 * x0 + sig2;
@@ -386,8 +386,9 @@ __global__ void __launch_bounds__(64 * NRG, 1)
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
           const int i = rg + NRG * t;
-          const double u = U[i];
-          const double pv = fma(-s1, u, P[i]);
+          const double2 up = UP[i];
+          const double u = up.x;
+          const double pv = fma(-s1, u, up.y);
           const double an = fma(-sc, u, a[t]);
           a[t] = an;
           bl[t & 3] = fma(pv, an, bl[t & 3]);
@@ -398,8 +399,9 @@ __global__ void __launch_bounds__(64 * NRG, 1)
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
           const int i = rg + NRG * t;
-          const double u = (NRG * t == kmask - 1) ? v0 : U[i];  // row jj: u = v0 (v = 1)
-          const double pv = fma(-s1, u, P[i]);
+          const double2 up = UP[i];
+          const double u = (NRG * t == kmask - 1) ? v0 : up.x;  // row jj: u = v0 (v = 1)
+          const double pv = fma(-s1, u, up.y);
           const double an = fma(-sc, u, a[t]);
           a[t] = an;
           bl[t & 3] = (NRG * t > kmask) ? fma(pv, an, bl[t & 3]) : bl[t & 3];
@@ -419,10 +421,10 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     auto snapshots = [&] {
       if (c == jj + 1) {
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) Un[rg + NRG * t] = (NRG * t < kmask) ? 0.0 : a[t];
+        for (int t = 0; t < RPT; ++t) UPn[2 * (rg + NRG * t)] = (NRG * t < kmask) ? 0.0 : a[t];
       } else if (c == jj + 2) {
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) Pn[rg + NRG * t] = a[t];
+        for (int t = 0; t < RPT; ++t) UPn[2 * (rg + NRG * t) + 1] = a[t];
       }
     };
     if (jj + 1 < b) {
@@ -653,8 +655,9 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
     launch_panel_reg<true, 16>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
     return true;
   }
-  // (a 16-CTA cluster of 256-row CTAs is slower than the grid path at 4096
+  // (a 16-CTA cluster of 256-row CTAs was slower than the grid path at 4096
   // rows: 3.13 vs 2.60 us/column — the per-column register pass dominates)
+
   // cooperative grid (FP64 atomics + grid barrier)
   if (ceil_div(mp, 8 * 8) <= ctx.num_sms) {
     const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
