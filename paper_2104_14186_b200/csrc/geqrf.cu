@@ -474,6 +474,47 @@ size_t panel_reg_smem() {
 // by recursive doubling instead of the column recurrence:
 //   T = [T11, -T11 (V1^T V2) T22; 0, T22],  V1^T V2 = G12,
 // block size s = 1, 2, 4, ... — 2 barriers per level, log2(b) levels.
+// One doubling level of larft with compile-time block size S: the k loops are
+// fully unrolled (zero terms by predicate) so every thread's shared loads are
+// in flight together instead of one load-FMA round trip per term.
+template <int S>
+QDWHG_DEV void larft_level(double (*Ts)[kBW + 1], double (*M)[kBW + 1], double (*Gs)[kBW + 1], int b,
+                           int t) {
+  if (S >= b) return;
+  // M(a+r, a+S+c) = sum_{k=r}^{S-1} T11(r, k) G(a+k, a+S+c)
+  for (int i = t; i < b * S; i += blockDim.x) {
+    const int r = i % S, rest = i / S;
+    const int pair = rest / S, c = rest % S;
+    const int a = pair * 2 * S;
+    if (a + S + c >= b) continue;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double v = (k >= r) ? Ts[a + r][a + k] * Gs[a + k][a + S + c] : 0.0;
+      if (k & 1) acc1 += v;
+      else acc0 += v;
+    }
+    M[a + r][a + S + c] = acc0 + acc1;
+  }
+  __syncthreads();
+  // T12(r, c) = -sum_{k=0}^{c} M(a+r, a+S+k) T22(k, c)
+  for (int i = t; i < b * S; i += blockDim.x) {
+    const int r = i % S, rest = i / S;
+    const int pair = rest / S, c = rest % S;
+    const int a = pair * 2 * S;
+    if (a + S + c >= b) continue;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double v = (k <= c) ? M[a + r][a + S + k] * Ts[a + S + k][a + S + c] : 0.0;
+      if (k & 1) acc1 += v;
+      else acc0 += v;
+    }
+    Ts[a + r][a + S + c] = -(acc0 + acc1);
+  }
+  __syncthreads();
+}
+
 __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, double* T,
                              int64_t ldt, int b) {
   extern __shared__ double larft_sm[];
@@ -493,30 +534,12 @@ __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, do
     Ts[r][c] = (r == c && r < b) ? tau[r] : 0.0;
   }
   __syncthreads();
-  for (int s = 1; s < b; s *= 2) {
-    // M(a+r, a+s+c) = sum_{k=r}^{s-1} T11(r, k) G(a+k, a+s+c)
-    for (int i = t; i < b * s; i += blockDim.x) {
-      const int r = i % s, rest = i / s;
-      const int pair = rest / s, c = rest % s;
-      const int a = pair * 2 * s;
-      if (a + s + c >= b) continue;
-      double acc = 0.0;
-      for (int k = r; k < s; ++k) acc = fma(Ts[a + r][a + k], Gs[a + k][a + s + c], acc);
-      M[a + r][a + s + c] = acc;
-    }
-    __syncthreads();
-    // T12(r, c) = -sum_{k=0}^{c} M(a+r, a+s+k) T22(k, c)
-    for (int i = t; i < b * s; i += blockDim.x) {
-      const int r = i % s, rest = i / s;
-      const int pair = rest / s, c = rest % s;
-      const int a = pair * 2 * s;
-      if (a + s + c >= b) continue;
-      double acc = 0.0;
-      for (int k = 0; k <= c; ++k) acc = fma(M[a + r][a + s + k], Ts[a + s + k][a + s + c], acc);
-      Ts[a + r][a + s + c] = -acc;
-    }
-    __syncthreads();
-  }
+  larft_level<1>(Ts, M, Gs, b, t);
+  larft_level<2>(Ts, M, Gs, b, t);
+  larft_level<4>(Ts, M, Gs, b, t);
+  larft_level<8>(Ts, M, Gs, b, t);
+  larft_level<16>(Ts, M, Gs, b, t);
+  larft_level<32>(Ts, M, Gs, b, t);
   for (int i = t; i < b * b; i += blockDim.x) {
     const int r = i % b, cc = i / b;
     T[r + (int64_t)cc * ldt] = Ts[r][cc];
