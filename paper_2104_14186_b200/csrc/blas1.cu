@@ -248,13 +248,95 @@ void copy_to_host(Ctx& ctx, const DMat& X, double* h, int64_t ldh) {
                                cudaMemcpyDeviceToHost, ctx.stream));
 }
 
+// Square matrices with the symmetry check: 32x32 tile pairs (T_ij, T_ji) through
+// shared memory, so both the direct and the transposed reads are coalesced.
+__global__ void stats_sym_kernel(const double* X, int64_t ld, int64_t n, double* partial) {
+  __shared__ double scratch[32];
+  __shared__ double t1[32][33], t2[32][33];
+  const int64_t nt = (n + 31) / 32;
+  const int64_t npairs = nt * (nt + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  double s = 0.0, asym = 0.0, nf = 0.0, mx = 0.0;
+  // contiguous chunk of the column-major lower-tile enumeration per block: the
+  // (ti, tj) of the first pair is found once, then stepped
+  const int64_t chunk = (npairs + gridDim.x - 1) / gridDim.x;
+  const int64_t p0 = blockIdx.x * chunk, p1 = min(npairs, p0 + chunk);
+  int64_t tj = 0, ti = 0;
+  {
+    int64_t rem = p0;
+    while (tj < nt && rem >= nt - tj) {
+      rem -= nt - tj;
+      ++tj;
+    }
+    ti = tj + rem;
+  }
+  for (int64_t pidx = p0; pidx < p1; ++pidx, ++ti) {
+    if (ti >= nt) {
+      ++tj;
+      ti = tj;
+    }
+    const int64_t i0 = ti * 32, j0 = tj * 32;
+    for (int r = ty; r < 32; r += 8) {
+      // t1(r, tx) = X(i0 + tx, j0 + r) (column j0+r of tile ij), t2 likewise for tile ji
+      const int64_t ia = i0 + tx, ja = j0 + r, ib = j0 + tx, jb = i0 + r;
+      t1[r][tx] = (ia < n && ja < n) ? X[ia + ja * ld] : 0.0;
+      t2[r][tx] = (ib < n && jb < n) ? X[ib + jb * ld] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t ia = i0 + tx, ja = j0 + r;
+      if (ia < n && ja < n) {
+        const double x = t1[r][tx];  // X(ia, ja), ia >= ja region of the pair
+        if (!isfinite(x)) nf += 1.0;
+        else {
+          s += x * x;
+          mx = fmax(mx, fabs(x));
+        }
+        // X(ja, ia) = t2(tx, r)
+        if (ti != tj || tx > r) asym = fmax(asym, fabs(x - t2[tx][r]));
+      }
+      if (ti != tj) {  // the transposed tile's own entries
+        const int64_t ib = j0 + tx, jb = i0 + r;
+        if (ib < n && jb < n) {
+          const double y = t2[r][tx];
+          if (!isfinite(y)) nf += 1.0;
+          else {
+            s += y * y;
+            mx = fmax(mx, fabs(y));
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  s = block_sum(s, scratch);
+  __syncthreads();
+  asym = block_max(asym, scratch);
+  __syncthreads();
+  nf = block_sum(nf, scratch);
+  __syncthreads();
+  mx = block_max(mx, scratch);
+  if (threadIdx.x == 0) {
+    partial[4 * blockIdx.x + 0] = s;
+    partial[4 * blockIdx.x + 1] = asym;
+    partial[4 * blockIdx.x + 2] = nf;
+    partial[4 * blockIdx.x + 3] = mx;
+  }
+}
+
 MatStats mat_stats(Ctx& ctx, const DMat& X, bool want_asym) {
   MatStats st;
   if (X.rows * X.cols == 0) return st;
-  const int blocks = std::min(grid_for(ctx, X.rows * X.cols, 256), 2 * ctx.num_sms);
+  int blocks = std::min(grid_for(ctx, X.rows * X.cols, 256), 2 * ctx.num_sms);
   double* partial = ctx.dscratch + 64;
-  stats_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, X.rows, X.cols, want_asym ? 1 : 0,
-                                               partial);
+  if (want_asym && X.rows == X.cols) {
+    const int64_t nt = (X.rows + 31) / 32;
+    blocks = (int)std::max<int64_t>(1, std::min<int64_t>(nt * (nt + 1) / 2, 4LL * ctx.num_sms));
+    stats_sym_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, X.rows, partial);
+  } else {
+    stats_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, X.rows, X.cols, want_asym ? 1 : 0,
+                                                 partial);
+  }
   stats_final_kernel<<<1, 256, 0, ctx.stream>>>(partial, blocks, ctx.dscratch);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count(2);
