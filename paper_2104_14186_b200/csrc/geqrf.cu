@@ -681,21 +681,37 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
   // (a 16-CTA cluster of 256-row CTAs was slower than the grid path at 4096
   // rows: 3.13 vs 2.60 us/column — the per-column register pass dominates)
 
-  // cooperative grid (FP64 atomics + grid barrier)
-  if (ceil_div(mp, 8 * 8) <= ctx.num_sms) {
+  // cooperative grid (FP64 atomics + grid barrier); while a look-ahead side
+  // stream runs, the grid is capped (ctx.panel_max_ctas) so the panel does not
+  // need the whole machine at once
+  const int max_ctas =
+      ctx.panel_max_ctas > 0 ? std::min(ctx.panel_max_ctas, ctx.num_sms) : ctx.num_sms;
+  if (ceil_div(mp, 8 * 8) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
     launch_panel_reg<false, 8>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
     return true;
   }
-  if (ceil_div(mp, 8 * 16) <= ctx.num_sms) {
+  if (ceil_div(mp, 8 * 16) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
     launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
     return true;
   }
-  if (ceil_div(mp, 8 * 32) <= ctx.num_sms) {
+  if (ceil_div(mp, 8 * 32) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
     launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
     return true;
+  }
+  if (max_ctas < ctx.num_sms) {  // taller than the cap allows: uncapped
+    if (ceil_div(mp, 8 * 16) <= ctx.num_sms) {
+      const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
+      launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+      return true;
+    }
+    if (ceil_div(mp, 8 * 32) <= ctx.num_sms) {
+      const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
+      launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+      return true;
+    }
   }
   return false;
 }
@@ -813,6 +829,10 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     QDWHG_CUDA(cudaStreamWaitEvent(ctx.hi, ctx.ev_main, 0));
     ctx.stream = ctx.hi;
   }
+  // measured: cap 64 -> cfg4 QR 247 -> 239 ms, cfg3 66.8 -> 63.2 ms
+  static const int pcap_env = getenv("QDWHG_PANEL_CAP") ? atoi(getenv("QDWHG_PANEL_CAP")) : 64;
+  const int saved_cap = ctx.panel_max_ctas;
+  ctx.panel_max_ctas = lookahead ? pcap_env : 0;
   const Arena::Mark mark = ctx.arena->mark();
   for (int64_t po = 0; po < nout; ++po) {
     const int64_t jo = po * nbo;
@@ -935,6 +955,7 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
     QDWHG_CUDA(cudaStreamWaitEvent(caller, ctx.ev_main, 0));
     ctx.stream = caller;
   }
+  ctx.panel_max_ctas = saved_cap;
 }
 
 void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, const DMat& Q) {

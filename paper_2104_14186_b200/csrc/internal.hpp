@@ -106,6 +106,7 @@ struct Ctx {
   cudaEvent_t ev_main = nullptr, ev_side = nullptr, ev_side2 = nullptr;  // cross-stream ordering
   Arena* arena = nullptr;
   int num_sms = 148;
+  int panel_max_ctas = 0;  // GEQRF grid-panel CTA cap while a side stream runs (0 = none)
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
   double* hscratch = nullptr;   // pinned host mirror of dscratch
   int* dflag = nullptr;         // device status flag
