@@ -26,16 +26,20 @@ constexpr int kDiagThreads = 256;
 
 // 1/sqrt(d) without the libdevice slow-path call (which forces the unrolled
 // register row to the stack): hardware double-precision estimate
-// (rsqrt.approx.f64) refined by two Newton steps.  Non-positive d returns NaN
+// (rsqrt.approx.f64) refined by one third-order step.  Non-positive d returns NaN
 // (the caller flags it).
 QDWHG_DEV double rsqrt_newton(double d) {
-  if (!(d > 0.0)) return __longlong_as_double(0x7ff8000000000000ll);
+  // branch-free (a branch here splits the unrolled Cholesky step into basic
+  // blocks and stops the scheduler from hiding this chain behind the updates)
+  // One third-order step from the ~2^-20 hardware estimate: with
+  // e = 1 - d y^2, y' = y + y e (1/2 + 3/8 e) (error 5/16 e^3 < 2^-56),
+  // dependency depth 4 instead of 6 for two Newton steps.
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(d));
-  const double h = 0.5 * d;
-#pragma unroll
-  for (int it = 0; it < 2; ++it) y = y * fma(-h * y, y, 1.5);
-  return y;
+  const double e = fma(-d * y, y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  y = fma(y * e, p, y);
+  return (d > 0.0) ? y : __longlong_as_double(0x7ff8000000000000ll);
 }
 #ifdef QDWHG_DIAG_TRACE
 __device__ long long g_diag_trace[64];
@@ -45,7 +49,9 @@ __device__ long long g_diag_trace[64];
 #define DIAG_MARK(i)
 #endif
 constexpr int kSB = 32;          // sub-block handled by one warp
-constexpr int kLDA = 129;        // padded smem leading dimension (odd -> conflict free)
+// padded smem leading dimension: 132 = 4 (mod 16) makes the DMMA fragment loads
+// (8 rows x 4 k, or 4 k x 8 columns, one double per lane) bank-conflict free
+constexpr int kLDA = 132;
 
 // One right-looking Cholesky column step of a 32x32 block held as one row per
 // lane (template recursion: compile-time register indices).  The pivot comes
@@ -83,6 +89,17 @@ struct CholStep<kSB> {
   static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&, double) {}
 };
 
+// D^{-1} of a factored 32x32 lower block by forward substitution, one warp,
+// lane j computing column j in registers (x[i] = 0 above the diagonal)
+QDWHG_DEV void block_inverse(const double* Lb, const double* sinv, int lane, double (&x)[kSB]) {
+#pragma unroll
+  for (int i = 0; i < kSB; ++i) {
+    double s[4] = {(i == lane) ? 1.0 : 0.0, 0.0, 0.0, 0.0};  // 4 chains
+#pragma unroll
+    for (int k = 0; k < i; ++k) s[k & 3] -= Lb[k * kLDA + i] * x[k];  // x[k] == 0 for k < lane
+    x[i] = (i >= lane) ? ((s[0] + s[1]) + (s[2] + s[3])) * sinv[i] : 0.0;
+  }
+}
 
 // Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
 // -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
@@ -93,22 +110,26 @@ struct CholStep<kSB> {
 //     panel rows below: forward substitution, one row per thread, the row in
 //       registers (no multiplication by an explicit inverse: u*kappa accuracy);
 //     trailing lower triangle: rank-32 update on DMMA m8n8k4 tiles;
-//   W = L^T written out;
-//   D_kb^{-1} of the four diagonal blocks in parallel (one warp each);
-//   L^{-1} in place, block columns right to left (LAPACK trtri order):
-//     L21 <- -(Linv22 L21) D11^{-1}, both products on DMMA tiles;
-//   Winv = L^{-T} written out.
+//   W = L^T written out (unless kDiagNoW);
+//   D_kb^{-1} of the four diagonal blocks in parallel (one warp each, in place);
+//   L^{-1} in place by recursive doubling (32 -> 64 -> 128):
+//     L^{-1}_QP = -Q^{-1} (L_QP P^{-1}), both products on DMMA tiles, all pairs
+//     of a level at once (2 levels x 2 products instead of 3 x 2 block columns);
+//   Winv = L^{-T} written out (upper triangle only with kDiagUpperOnly).
 // The block is padded to a multiple of 32 with an identity (chol([Z 0;0 I]) = [L 0;0 I]).
-constexpr int kLDT = 97;  // T (R x 32, R <= 96) leading dimension
+constexpr int kLDT = 68;  // T (<= 64 x 64, the doubling products' scratch) leading dimension
+// launch flags
+constexpr int kDiagInvertOnly = 1;  // input is an upper R: only R^{-1}
+constexpr int kDiagNoW = 2;         // W = L^T is not wanted (not written)
+constexpr int kDiagUpperOnly = 4;   // outputs pre-zeroed: write the upper triangles only
 
 __global__ void __launch_bounds__(kDiagThreads, 1)
     potrf_diag_kernel(const double* Z, int64_t ldz, double* W, int64_t ldw, double* Winv,
-                      int64_t ldwi, int nb, int* flag, int invert_only) {
+                      int64_t ldwi, int nb, int* flag, int flags) {
   extern __shared__ double sm[];
   double* A = sm;                    // 128 x kLDA, column-major, lower = L (then L^{-1})
-  double* Dinv = A + 128 * kLDA;     // 4 blocks of 32 x 33 (column-major, lower)
-  double* T = Dinv + 4 * kSB * 33;   // 32 columns x kLDT
-  double* Sinv = T + kSB * kLDT;     // 128: 1 / L_ii
+  double* T = A + 128 * kLDA;        // 64 columns x kLDT
+  double* Sinv = T + 64 * kLDT;      // 128: 1 / L_ii
   __shared__ int bad_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;  // DMMA fragment coordinates
@@ -118,7 +139,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   DIAG_MARK(20);
   griddep_wait();
 
-  if (invert_only) {
+  if (flags & kDiagInvertOnly) {
     // Z holds an upper-triangular R: L = R^T is loaded (transposed reads), the
     // factorisation is skipped, and only L^{-1} (-> Winv = R^{-1}) is formed
     for (int c = warp; c < nbp; c += kDiagThreads / 32) {
@@ -234,102 +255,109 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
     DIAG_MARK(3 + 3 * kb);
   }
   // ---- W = L^T (upper) with explicit zeros below
-  for (int c = warp; c < nb; c += kDiagThreads / 32) {
-    double* wc = W + (int64_t)c * ldw;
+  if (!(flags & kDiagNoW)) {
+    const int rend = (flags & kDiagUpperOnly) ? 0 : nb;
+    for (int c = warp; c < nb; c += kDiagThreads / 32) {
+      double* wc = W + (int64_t)c * ldw;
 #pragma unroll 4
-    for (int r = lane; r < nb; r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+      for (int r = lane; r < max(c + 1, rend); r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+    }
   }
   DIAG_MARK(13);
   }  // !invert_only
   if (tid == 0 && bad_s) atomicExch(flag, 1);
 
-  // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each:
-  // lane j computes column j by forward substitution in registers
+  // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each, in place
   if (warp < nsb) {
     const int b0 = warp * kSB;
     double x[kSB];
+    block_inverse(A + b0 * kLDA + b0, Sinv + b0, lane, x);
+    __syncwarp();
+    double* D = A + (b0 + lane) * kLDA + b0;  // column lane of the block (zeros above)
 #pragma unroll
-    for (int i = 0; i < kSB; ++i) {
-      double s[4] = {(i == lane) ? 1.0 : 0.0, 0.0, 0.0, 0.0};  // 4 chains
-#pragma unroll
-      for (int k = 0; k < i; ++k) {
-        const double l = A[(b0 + k) * kLDA + b0 + i];  // broadcast
-        s[k & 3] -= l * x[k];  // x[k] == 0 for k < lane: no predicate needed
-      }
-      x[i] = (i >= lane) ? ((s[0] + s[1]) + (s[2] + s[3])) * Sinv[b0 + i] : 0.0;
-    }
-    double* D = Dinv + warp * kSB * 33;
-#pragma unroll
-    for (int i = 0; i < kSB; ++i) D[lane * 33 + i] = x[i];
+    for (int i = 0; i < kSB; ++i) D[i] = x[i];
   }
   __syncthreads();
   DIAG_MARK(14);
 
-  // ---- L^{-1} in place, block columns right to left
-  for (int jb = nsb - 1; jb >= 0; --jb) {
-    const int b0 = jb * kSB, p0 = b0 + kSB, R = nbp - p0;
-    const double* D = Dinv + jb * kSB * 33;
-    if (R > 0) {
-      // T = Linv22 * L21   (R x 32; Linv22 lower: k-tiles up to the diagonal).
-      // Unit = one row tile x the 4 column tiles; heaviest row tiles first.
-      const int nt = R / 8;
-      for (int u = warp; u < nt; u += kDiagThreads / 32) {
-        const int ti = nt - 1 - u;
-        double c[4][2] = {};
-        for (int k4 = 0; k4 < 2 * (ti + 1); ++k4) {
-          const int k = p0 + 4 * k4 + q;
-          const double a = A[k * kLDA + p0 + 8 * ti + g];
-#pragma unroll
-          for (int tj = 0; tj < 4; ++tj)
-            dmma_8x8x4(c[tj][0], c[tj][1], a, A[(b0 + 8 * tj + g) * kLDA + k]);
-        }
-#pragma unroll
-        for (int tj = 0; tj < 4; ++tj) {
-          T[(8 * tj + 2 * q) * kLDT + 8 * ti + g] = c[tj][0];
-          T[(8 * tj + 2 * q + 1) * kLDT + 8 * ti + g] = c[tj][1];
-        }
+  // ---- L^{-1} by recursive doubling over the diagonal blocks: for each pair of
+  // adjacent groups (P = [a0, a0+h), Q = [a0+h, a0+2h)) with P^{-1}, Q^{-1} in
+  // place:  L^{-1}_QP = -Q^{-1} (L_QP P^{-1}).  Two levels for nb = 128, each
+  // two DMMA products over all pairs at once (a unit = one 8-row tile x 32 columns).
+  for (int h = kSB; h < nbp; h *= 2) {
+    const int npairs = (nbp - h + 2 * h - 1) / (2 * h);  // pairs with a non-empty Q
+    const int cgs = h / kSB;                             // 32-column groups per pair
+    int units = 0;
+    for (int p = 0; p < npairs; ++p) units += min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+    // phase 1: T_p = L_QP * P^{-1}   (P^{-1} lower: k >= column)
+    for (int u = warp; u < units; u += kDiagThreads / 32) {
+      int p = 0, rem = u;
+      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
+        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+        ++p;
       }
-      __syncthreads();
-      DIAG_MARK(22 + 2 * jb);
-      // L21 <- -T * D^{-1}   (D lower with explicit zeros: full K)
-      for (int u = warp; u < nt; u += kDiagThreads / 32) {
-        const int ti = u;
-        double c[4][2] = {};
+      const int ti = rem / cgs, cg = rem % cgs;
+      const int a0 = 2 * p * h, q0 = a0 + h;
+      double c[4][2] = {};
+      for (int k4 = 8 * cg; k4 < h / 4; ++k4) {
+        const int k = a0 + 4 * k4 + q;
+        const double a = A[k * kLDA + q0 + 8 * ti + g];
 #pragma unroll
-        for (int k4 = 0; k4 < 8; ++k4) {
-          const int k = 4 * k4 + q;
-          const double a = -T[k * kLDT + 8 * ti + g];
-#pragma unroll
-          for (int tj = 0; tj < 4; ++tj) dmma_8x8x4(c[tj][0], c[tj][1], a, D[(8 * tj + g) * 33 + k]);
-        }
-#pragma unroll
-        for (int tj = 0; tj < 4; ++tj) {
-          A[(b0 + 8 * tj + 2 * q) * kLDA + p0 + 8 * ti + g] = c[tj][0];
-          A[(b0 + 8 * tj + 2 * q + 1) * kLDA + p0 + 8 * ti + g] = c[tj][1];
-        }
+        for (int tj = 0; tj < 4; ++tj)
+          dmma_8x8x4(c[tj][0], c[tj][1], a, A[(a0 + kSB * cg + 8 * tj + g) * kLDA + k]);
       }
-    }
-    DIAG_MARK(21 + 2 * jb);
-    // diagonal block <- D^{-1} (lower; the strict upper stays zero)
-    for (int idx = tid; idx < kSB * kSB; idx += kDiagThreads) {
-      const int r = idx & 31, c = idx >> 5;
-      if (r >= c) A[(b0 + c) * kLDA + b0 + r] = D[c * 33 + r];
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int col = p * h + kSB * cg + 8 * tj + 2 * q;
+        T[col * kLDT + 8 * ti + g] = c[tj][0];
+        T[(col + 1) * kLDT + 8 * ti + g] = c[tj][1];
+      }
     }
     __syncthreads();
+    // phase 2: L^{-1}_QP = -Q^{-1} T_p   (Q^{-1} lower: k <= row), heaviest rows first
+    for (int u = warp; u < units; u += kDiagThreads / 32) {
+      int p = 0, rem = u;
+      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
+        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+        ++p;
+      }
+      const int nti = min(h, nbp - (2 * p + 1) * h) / 8;
+      const int ti = nti - 1 - rem / cgs, cg = rem % cgs;
+      const int a0 = 2 * p * h, q0 = a0 + h;
+      double c[4][2] = {};
+      for (int k4 = 0; k4 < 2 * (ti + 1); ++k4) {
+        const int k = 4 * k4 + q;
+        const double a = -A[(q0 + k) * kLDA + q0 + 8 * ti + g];
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+          dmma_8x8x4(c[tj][0], c[tj][1], a, T[(p * h + kSB * cg + 8 * tj + g) * kLDT + k]);
+      }
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int col = a0 + kSB * cg + 8 * tj + 2 * q;
+        A[col * kLDA + q0 + 8 * ti + g] = c[tj][0];
+        A[(col + 1) * kLDA + q0 + 8 * ti + g] = c[tj][1];
+      }
+    }
+    __syncthreads();
+    DIAG_MARK(21 + h / kSB);
   }
   DIAG_MARK(15);
 
   // ---- Winv = L^{-T} (upper) with explicit zeros below
-  for (int c = warp; c < nb; c += kDiagThreads / 32) {
-    double* wc = Winv + (int64_t)c * ldwi;
+  {
+    const int rend = (flags & kDiagUpperOnly) ? 0 : nb;
+    for (int c = warp; c < nb; c += kDiagThreads / 32) {
+      double* wc = Winv + (int64_t)c * ldwi;
 #pragma unroll 4
-    for (int r = lane; r < nb; r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+      for (int r = lane; r < max(c + 1, rend); r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+    }
   }
   DIAG_MARK(16);
 }
 
-void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, int invert_only = 0) {
-  const size_t smem = (size_t)(128 * kLDA + 4 * kSB * 33 + kSB * kLDT + 128) * 8;
+void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, int flags = 0) {
+  const size_t smem = (size_t)(128 * kLDA + 64 * kLDT + 128) * 8;
   static bool set = false;
   if (!set) {
     QDWHG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -337,7 +365,7 @@ void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, i
     set = true;
   }
   launch_pdl(ctx, potrf_diag_kernel, dim3(1), dim3(kDiagThreads), smem, Zkk.ptr(), Zkk.ld, Wkk.ptr(),
-             Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag, invert_only);
+             Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag, flags);
   ctx.count();
 }
 
@@ -443,15 +471,15 @@ void launch_panel_trsm(Ctx& ctx, const DMat& Wkk, const DMat& Zr, const DMat& X)
 // sweep), so almost all flops run at full DMMA rate; leaves are the 128-block
 // diag kernel.  Only the lower triangle of Z is read/updated.
 void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
-                  int nb) {
+                  int nb, int leaf_flags) {
   if (n <= nb) {
-    launch_diag(ctx, Z.sub(r0, r0, n, n), W.sub(r0, r0, n, n), Winv.sub(r0, r0, n, n));
+    launch_diag(ctx, Z.sub(r0, r0, n, n), W.sub(r0, r0, n, n), Winv.sub(r0, r0, n, n), leaf_flags);
     return;
   }
   int64_t n1 = ((n / 2 + nb - 1) / nb) * nb;
   if (n1 >= n) n1 = n - nb;
   const int64_t n2 = n - n1;
-  chol_inv_rec(ctx, Z, W, Winv, r0, n1, nb);
+  chol_inv_rec(ctx, Z, W, Winv, r0, n1, nb, leaf_flags);
   const int64_t r1 = r0 + n1;
   GemmExtra e1;
   e1.krange = KRange::ALower;  // op(A) = W11^-T lower
@@ -461,7 +489,7 @@ void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int6
   e2.out = OutMode::Lower;
   const DMat W12 = W.sub(r0, r1, n1, n2);
   gemm(ctx, Op::T, Op::N, -1.0, W12, W12, 1.0, Z.sub(r1, r1, n2, n2), e2);
-  chol_inv_rec(ctx, Z, W, Winv, r1, n2, nb);
+  chol_inv_rec(ctx, Z, W, Winv, r1, n2, nb, leaf_flags);
   const Arena::Mark mark = ctx.arena->mark();
   DMat T = ctx.arena->alloc(n1, n2);
   GemmExtra e3;
@@ -494,7 +522,9 @@ void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
   fill(ctx, W, 0.0, 0.0);
   fill(ctx, Winv, 0.0, 0.0);
   const int64_t n2 = n - n1;
-  chol_inv_rec(ctx, Z, W, Winv, 0, n1, nb);
+  // W and W^-1 are pre-zeroed; W's diagonal blocks are never read
+  const int leaf = kDiagUpperOnly | kDiagNoW;
+  chol_inv_rec(ctx, Z, W, Winv, 0, n1, nb, leaf);
   left_done();
   GemmExtra e1;
   e1.krange = KRange::ALower;  // op(A) = W11^-T lower
@@ -504,7 +534,7 @@ void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
   e2.out = OutMode::Lower;
   const DMat W12 = W.sub(0, n1, n1, n2);
   gemm(ctx, Op::T, Op::N, -1.0, W12, W12, 1.0, Z.sub(n1, n1, n2, n2), e2);
-  chol_inv_rec(ctx, Z, W, Winv, n1, n2, nb);
+  chol_inv_rec(ctx, Z, W, Winv, n1, n2, nb, leaf);
   DMat T = ctx.arena->alloc(n1, n2);
   GemmExtra e3;
   e3.krange = KRange::BUpper;  // W22^-1 upper
@@ -529,7 +559,8 @@ bool trtri_upper(Ctx& ctx, const DMat& R, const DMat& Rinv) {
   fill(ctx, Rinv, 0.0, 0.0);
   for (int64_t k = 0; k < n; k += nb) {
     const int64_t b = std::min<int64_t>(nb, n - k);
-    launch_diag(ctx, R.sub(k, k, b, b), Rinv.sub(k, k, b, b), Rinv.sub(k, k, b, b), 1);
+    launch_diag(ctx, R.sub(k, k, b, b), Rinv.sub(k, k, b, b), Rinv.sub(k, k, b, b),
+                kDiagInvertOnly | kDiagUpperOnly);
   }
   const int64_t nblk = n / nb;
   if (n % nb == 0 && (nblk & (nblk - 1)) == 0)
@@ -553,14 +584,14 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   fill(ctx, W, 0.0, 0.0);
   fill(ctx, Winv, 0.0, 0.0);
   if (!stable) {
-    chol_inv_rec(ctx, Z, W, Winv, 0, n, nb);
+    chol_inv_rec(ctx, Z, W, Winv, 0, n, nb, kDiagUpperOnly | (want_w ? 0 : kDiagNoW));
   } else {
     // right-looking, panel by forward substitution (no explicit inverse in the
     // factorisation: backward stable like the reference's dot-product Cholesky)
     for (int64_t k = 0; k < n; k += nb) {
       const int64_t b = std::min<int64_t>(nb, n - k);
       const int64_t rest = n - k - b;
-      launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b));
+      launch_diag(ctx, Z.sub(k, k, b, b), W.sub(k, k, b, b), Winv.sub(k, k, b, b), kDiagUpperOnly);
       if (rest > 0) {
         launch_panel_trsm(ctx, W.sub(k, k, b, b), Z.sub(k + b, k, rest, b), W.sub(k, k + b, b, rest));
         GemmExtra e2;

@@ -3,12 +3,45 @@
 #define QDWHG_DIAG_TRACE 1
 #include "../../paper_2104_14186_b200/csrc/potrf.cu"
 
+#include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <vector>
 
 using namespace qdwhg;
 
+__global__ void rsqrt_probe(const double* d, double* y, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = rsqrt_newton(d[i]);
+}
+
+static void check_rsqrt() {
+  const int n = 1 << 20;
+  std::vector<double> d(n), y(n);
+  uint64_t st = 12345;
+  for (int i = 0; i < n; ++i) {
+    st = st * 6364136223846793005ull + 1442695040888963407ull;
+    const double u = (double)(st >> 11) / 9007199254740992.0;
+    d[i] = std::ldexp(1.0 + u, (int)(st % 200) - 100);
+  }
+  double *dd, *dy;
+  cudaMalloc(&dd, 8 * n);
+  cudaMalloc(&dy, 8 * n);
+  cudaMemcpy(dd, d.data(), 8 * n, cudaMemcpyHostToDevice);
+  rsqrt_probe<<<n / 256, 256>>>(dd, dy, n);
+  cudaMemcpy(y.data(), dy, 8 * n, cudaMemcpyDeviceToHost);
+  double worst = 0;
+  for (int i = 0; i < n; ++i) {
+    const long double ref = 1.0L / sqrtl((long double)d[i]);
+    worst = std::max(worst, (double)(fabsl((long double)y[i] - ref) / ref));
+  }
+  printf("rsqrt_newton max rel err %.3e (%.2f ulp)\n", worst, worst / 1.1102230246251565e-16);
+  cudaFree(dd);
+  cudaFree(dy);
+}
+
 int main() {
+  check_rsqrt();
   const int nb = 128;
   const int64_t ld = 128;
   std::vector<double> h(ld * nb);
@@ -37,11 +70,21 @@ int main() {
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
   printf("potrf_diag nb=%d: %.2f us/launch (%s)\n", nb, 1e3 * ms / reps, cudaGetErrorString(cudaGetLastError()));
+  cudaEventRecord(e0);
+  for (int it = 0; it < reps; ++it)
+    launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb},
+                kDiagNoW | kDiagUpperOnly);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("potrf_diag nb=%d (no W, upper only): %.2f us/launch\n", nb, 1e3 * ms / reps);
+  for (int it = 0; it < 2; ++it) launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
+  cudaDeviceSynchronize();
   long long t[64];
   cudaMemcpyFromSymbol(t, g_diag_trace, sizeof(t));
   const char* names[21] = {"load", "kb0 chol+Dinv", "kb0 panel", "kb0 trail", "kb1 chol+Dinv", "kb1 panel",
                            "kb1 trail", "kb2 chol+Dinv", "kb2 panel", "kb2 trail", "kb3 chol+Dinv",
-                           "kb3 panel", "kb3 trail", "W write", "D^-1 blocks", "L^-1 in place", "Winv write",
+                           "kb3 panel", "kb3 trail", "W write", "D^-1 blocks", "L^-1 doubling", "Winv write",
                            "", "", "", "start"};
   long long prev = t[20];
   for (int i = 0; i <= 16; ++i) {
@@ -50,8 +93,7 @@ int main() {
     prev = t[i];
   }
   printf("  total %lld cycles\n", t[16] - t[20]);
-  printf("  inverse: jb2 prod1 %lld prod2 %lld | jb1 prod1 %lld prod2 %lld | jb0 prod1 %lld prod2 %lld\n",
-         t[26] - t[14], t[25] - t[26], t[24] - t[25] - 0, t[23] - t[24], t[22] - t[23], t[21] - t[22]);
+  printf("  inverse: level32 %lld level64 %lld\n", t[22] - t[14], t[23] - t[22]);
   // check: W^T W == Z
   std::vector<double> w(ld * nb), wi(ld * nb);
   cudaMemcpy(w.data(), W, 8 * ld * nb, cudaMemcpyDeviceToHost);
