@@ -39,8 +39,11 @@ __global__ void axpby_identity_kernel(const double* X, int64_t ldx, double* Y, i
 // Y(i,j) = a * 0.5 * (X(i,j) + X(j,i)) + diag*[i==j].  Processes 32x32 tiles
 // pairwise through shared memory so both reads are coalesced; in-place safe
 // because each (tile, mirror tile) pair is owned by one block.
+// Y = a sym(X) + diag I and, when Y2 != nullptr, Y2 = a2 Y + diag2 I from the
+// same read (the EIG driver's A/|mu| and (1-s) A/|mu| - s I in one pass)
 __global__ void symmetrize_kernel(const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t n,
-                                  double a, double diag) {
+                                  double a, double diag, double* Y2, int64_t ldy2, double a2,
+                                  double diag2) {
   __shared__ double t1[32][33], t2[32][33];
   const int64_t nt = (n + 31) / 32;
   const int64_t npairs = nt * (nt + 1) / 2;
@@ -66,11 +69,13 @@ __global__ void symmetrize_kernel(const double* X, int64_t ldx, double* Y, int64
       if (i1 < n && j1 < n) {
         const double v = a * (0.5 * (t1[r][tx] + t2[tx][r])) + (i1 == j1 ? diag : 0.0);
         Y[i1 + j1 * ldy] = v;
+        if (Y2) Y2[i1 + j1 * ldy2] = a2 * v + (i1 == j1 ? diag2 : 0.0);
       }
       const int64_t i2 = tj * 32 + tx, j2 = ti * 32 + r;
       if (ti != tj && i2 < n && j2 < n) {
         const double v = a * (0.5 * (t2[r][tx] + t1[tx][r]));
         Y[i2 + j2 * ldy] = v;
+        if (Y2) Y2[i2 + j2 * ldy2] = a2 * v;
       }
     }
     __syncthreads();
@@ -217,7 +222,20 @@ void symmetrize_scale(Ctx& ctx, const DMat& X, double a, double diag, const DMat
   const int64_t nt = (X.rows + 31) / 32;
   const int64_t npairs = nt * (nt + 1) / 2;
   const int blocks = (int)std::min<int64_t>(npairs, 8LL * ctx.num_sms);
-  symmetrize_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, Y.ptr(), Y.ld, X.rows, a, diag);
+  symmetrize_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, Y.ptr(), Y.ld, X.rows, a, diag,
+                                                    nullptr, 0, 0.0, 0.0);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+}
+
+void symmetrize_scale2(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y, double a2,
+                       double diag2, const DMat& Y2) {
+  if (X.rows != X.cols) throw InvalidArgument("symmetrize: matrix not square");
+  const int64_t nt = (X.rows + 31) / 32;
+  const int64_t npairs = nt * (nt + 1) / 2;
+  const int blocks = (int)std::min<int64_t>(npairs, 8LL * ctx.num_sms);
+  symmetrize_kernel<<<blocks, 256, 0, ctx.stream>>>(X.ptr(), X.ld, Y.ptr(), Y.ld, X.rows, a, diag,
+                                                    Y2.ptr(), Y2.ld, a2, diag2);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count();
 }

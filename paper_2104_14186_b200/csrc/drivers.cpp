@@ -256,12 +256,13 @@ static bool is_symmetric(Ctx& ctx, const DMat& X) {
 }
 
 FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_t iters,
-                                     bool qr_first) {
+                                     bool qr_first, bool known_symmetric) {
   // polar.cpp:179-215
   if (!(ell0 > 0.0) || ell0 > 1.0)
     throw InvalidArgument("run_fixed_iterations: ell0 must be in (0, 1]");
   if (iters < 1) throw InvalidArgument("run_fixed_iterations: iters must be >= 1");
-  const bool symmetric = is_symmetric(ctx, X);
+  // (polar.cpp:186-195; the EIG driver's iterate is exactly symmetric by construction)
+  const bool symmetric = known_symmetric || is_symmetric(ctx, X);
   FixedIterResult r;
   r.ell = ell0;
   r.trace.push_back(ell0);
@@ -431,14 +432,15 @@ void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) 
 
 int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
                    double vhi, int64_t* sel0) {
-  // Jacobi (n <= 32) / tridiagonal + bisection + inverse iteration (faster and
-  // better orthogonality from n ~ 48 up: measured 0.87 vs 0.96 ms at n = 49,
-  // 2.2 vs 12 ms at n = 130); the QDWH spectral divide-and-conquer remains the
+  // Jacobi (n <= 16) / tridiagonal + bisection + inverse iteration (faster and
+  // better orthogonality above: measured with the one-CTA small tridiagonal path
+  // 0.32 vs 0.48 ms at n = 30, 0.42 ms at n = 49, 1.2 ms at n = 132, wall time
+  // through the C ABI); the QDWH spectral divide-and-conquer remains the
   // fallback for tight clusters.  Only the eigenvectors of the eigenvalues in
   // (vlo, vhi) are formed (the tridiagonal path skips the others entirely).
   static const bool force_dc = getenv("QDWHG_SYEV_DC") != nullptr;
   static const int jac_max =
-      getenv("QDWHG_JACOBI_MAX") ? std::min(atoi(getenv("QDWHG_JACOBI_MAX")), kJacobiMaxN) : 32;
+      getenv("QDWHG_JACOBI_MAX") ? std::min(atoi(getenv("QDWHG_JACOBI_MAX")), kJacobiMaxN) : 16;
   const int64_t n = S.rows;
   if (n > jac_max && !force_dc) {
     if (syev_tridiag(ctx, S, vals, Vout, vlo, vhi, sel0)) {
@@ -553,15 +555,16 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
   out.shift = s;
   out.tol = tol;
   out.randomized = randomize;
-  out.mu = lanczos_min_bound(ctx, A, 30);
+  out.mu = lanczos_min_bound(ctx, A, 30, &st);
   if (clk) clk->mark(0);
   if (out.mu >= 0.0) return out;  // partial.cpp:52
   const double scale = std::abs(out.mu);
   DMat As = ctx.arena->alloc(n, n);
-  symmetrize_scale(ctx, A, 1.0 / scale, 0.0, As);
   DMat X = ctx.arena->alloc(n, n);
-  axpby_identity(ctx, As, 1.0 - s, -s, X);
-  FixedIterResult it = run_fixed_iterations(ctx, X, s, iters, false);
+  // As = sym(A)/|mu| and X = (1-s) As - s I (partial.cpp:54-59) from one read of A
+  symmetrize_scale2(ctx, A, 1.0 / scale, 0.0, As, 1.0 - s, -s, X);
+  // X = (1-s) sym(A)/|mu| - s I is exactly symmetric (symmetrize_scale above)
+  FixedIterResult it = run_fixed_iterations(ctx, X, s, iters, false, true);
   out.trace = it.trace;
   out.iters_qr = it.iters_qr;
   out.iters_chol = it.iters_chol;

@@ -41,7 +41,7 @@ struct FixedIterResult {
 };
 // polar.cpp:179-215, in place on X.  qr_first: FixedVariant::QrFirst.
 FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_t iters,
-                                     bool qr_first);
+                                     bool qr_first, bool known_symmetric = false);
 
 struct PolarOut {
   double alpha = 0;

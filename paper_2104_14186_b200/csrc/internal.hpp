@@ -170,6 +170,9 @@ void fill(Ctx& ctx, const DMat& X, double v, double diag);
 void axpby_identity(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y);
 // Y = a * (X + X^T)/2 + diag*I  (square; Y must not alias X unless in place-safe mode)
 void symmetrize_scale(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y);
+// Y = a (X + X^T)/2 + diag I and Y2 = a2 Y + diag2 I in one pass (Y, Y2 distinct from X)
+void symmetrize_scale2(Ctx& ctx, const DMat& X, double a, double diag, const DMat& Y, double a2,
+                       double diag2, const DMat& Y2);
 void copy(Ctx& ctx, const DMat& X, const DMat& Y);
 // Y = X^T (Y must not alias X)
 void transpose(Ctx& ctx, const DMat& X, const DMat& Y);
@@ -234,8 +237,15 @@ void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
 int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
                    double vhi, int64_t* sel0);
 
+// Lowest eigenvalue of the symmetric tridiagonal (d, e) (host arrays, n <= 64)
+// and the last component of its unit eigenvector, on the device: warp
+// multisection on the Sturm count + inverse iteration (syevd.cu kernels).
+void tridiag_lowest(Ctx& ctx, const std::vector<double>& d, const std::vector<double>& e,
+                    double* theta, double* z_last);
+
 // ------------------------------------------------------------------ krylov.cu
 double two_norm_estimate(Ctx& ctx, const DMat& A);
-double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps);
+// pre: the caller's mat_stats(A, true) of the same A (skips the second pass)
+double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre = nullptr);
 
 }  // namespace qdwhg

@@ -330,11 +330,11 @@ double two_norm_estimate(Ctx& ctx, const DMat& A) {
   return 1.05 * est;
 }
 
-double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps) {
+double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre) {
   const int64_t n = A.rows;
   if (A.cols != n) throw InvalidArgument("lanczos_min_bound: matrix not square");
   if (steps < 1) throw InvalidArgument("lanczos_min_bound: steps must be >= 1");
-  const MatStats st = mat_stats(ctx, A, true);
+  const MatStats st = pre ? *pre : mat_stats(ctx, A, true);
   const double fro = std::sqrt(st.fro2);
   const double eps = 2.220446049250313e-16;
   if (st.asym > 1e3 * (double)n * eps * std::max(1.0, fro))
@@ -402,19 +402,12 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps) {
     beta.push_back(bj);
   }
   const int k = (int)alpha.size();
-  // tridiagonal T on device, Jacobi eigensolver (kernels.cpp:426-433)
-  std::vector<double> th((size_t)k * k, 0.0);
-  for (int i = 0; i < k; ++i) th[i + (size_t)i * k] = alpha[i];
-  for (int i = 0; i + 1 < k; ++i) th[i + (size_t)(i + 1) * k] = th[(i + 1) + (size_t)i * k] = beta[i];
-  DMat T = ctx.arena->alloc(k, k);
-  DMat TV = ctx.arena->alloc(k, k);
-  copy_from_host(ctx, th.data(), k, T);
-  std::vector<double> tvals;
-  syev_jacobi(ctx, T, tvals, TV);
-  double s_last = 0.0;
-  QDWHG_CUDA(cudaMemcpyAsync(&s_last, TV.ptr() + (k - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
-  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
-  double mu = tvals[0] - beta_last * std::abs(s_last);
+  // smallest eigenpair of the tridiagonal T (kernels.cpp:426-433 uses Jacobi on
+  // the dense T; T is tridiagonal, so Sturm multisection + inverse iteration on
+  // the device give the same theta_min and |s_last| in microseconds)
+  double theta = 0.0, s_last = 0.0;
+  tridiag_lowest(ctx, alpha, beta, &theta, &s_last);
+  double mu = theta - beta_last * std::abs(s_last);
   if (mu < 0.0) mu *= 1.1;
   ctx.arena->release_to(mark);
   return mu;

@@ -18,6 +18,7 @@
 //   5. back-transform Z_A = Q Z with the compact-WY blocks (Gram + larft + GEMMs).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -293,17 +294,13 @@ __global__ void bisect_kernel(const double* d, const double* e2, int n, double l
   if (lane == 0) w[k] = 0.5 * (lo + hi);
 }
 
-// Inverse iteration for eigenvalue w[k]: (T - w I) z = b with partial pivoting,
-// 3 solves, normalised.  Z is stored transposed: Zt[k + i*n] = z_k(i).
-// Factor storage (per thread, transposed likewise): u1 diag, u2 super, u3 super2, l, piv.
-__global__ void inviter_kernel(const double* d, const double* e, int n, const double* w, int k0,
-                               int cnt, double tnorm, double* Zt, double* U1, double* U2,
-                               double* U3, double* L, unsigned char* P) {
-  // eigenvector k0 + k (k < cnt); per-thread arrays are stored transposed with
-  // stride cnt: element i of thread k at [k + i*cnt] (coalesced across threads)
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cnt) return;
-  const double lam = w[k0 + k];
+// Inverse iteration for eigenvalue lam: (T - lam I) z = b with partial pivoting,
+// 3 solves, normalised.  Element i of this thread's vector / factor arrays is at
+// [i * zs] (Z) and [i * s] (u1 diag, u2 super, u3 super2, l, piv): strided so
+// consecutive threads touch consecutive words (global or shared memory).
+QDWHG_DEV void inviter_one(const double* d, const double* e, int n, double lam, double tnorm,
+                           double* Z, int zs, double* U1, double* U2, double* U3, double* L,
+                           unsigned char* P, int s) {
   const double eps = 2.220446049250313e-16;
   const double tiny = eps * tnorm;
   // ---- LU with partial pivoting of the tridiagonal (dlagtf shape)
@@ -313,7 +310,7 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
     const double cc = e[i];              // sub-diagonal below row i
     const double dn = d[i + 1] - lam;
     const double bn = (i + 2 < n) ? e[i + 1] : 0.0;
-    const size_t o = (size_t)k + (size_t)i * cnt;
+    const size_t o = (size_t)i * s;
     if (fabs(a) >= fabs(cc)) {
       // no swap: row i stays; multiplier l = cc / a
       const double piv = (a == 0.0) ? tiny : a;
@@ -338,52 +335,102 @@ __global__ void inviter_kernel(const double* d, const double* e, int n, const do
     }
   }
   {
-    const size_t o = (size_t)k + (size_t)(n - 1) * cnt;
+    const size_t o = (size_t)(n - 1) * s;
     U1[o] = (a == 0.0) ? tiny : a;
     U2[o] = 0.0;
     U3[o] = 0.0;
   }
   // ---- iterations: forward apply L (with pivots), back-solve U
   // start vector: ones (dstein uses random; ones is adequate after 3 solves)
-  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] = 1.0;
+  for (int i = 0; i < n; ++i) Z[(size_t)i * zs] = 1.0;
   for (int it = 0; it < 3; ++it) {
     if (it > 0) {
       // forward: apply the row swaps/multipliers to the rhs
       for (int i = 0; i < n - 1; ++i) {
-        const size_t o = (size_t)k + (size_t)i * cnt;
-        double zi = Zt[o], zn = Zt[o + cnt];
+        const size_t o = (size_t)i * s;
+        double zi = Z[(size_t)i * zs], zn = Z[(size_t)(i + 1) * zs];
         if (P[o]) {
           const double t = zi;
           zi = zn;
           zn = t;
         }
         zn -= L[o] * zi;
-        Zt[o] = zi;
-        Zt[o + cnt] = zn;
+        Z[(size_t)i * zs] = zi;
+        Z[(size_t)(i + 1) * zs] = zn;
       }
     }
     // back substitution U z = rhs, with scaling against overflow
     double z2 = 0.0, z1 = 0.0, nrm = 0.0;
     for (int i = n - 1; i >= 0; --i) {
-      const size_t o = (size_t)k + (size_t)i * cnt;
-      double v = Zt[o] - U2[o] * z1 - U3[o] * z2;
+      const size_t o = (size_t)i * s;
+      double v = Z[(size_t)i * zs] - U2[o] * z1 - U3[o] * z2;
       v /= U1[o];
-      Zt[o] = v;
+      Z[(size_t)i * zs] = v;
       z2 = z1;
       z1 = v;
       nrm = fmax(nrm, fabs(v));
     }
     // normalise (inf-norm first, then 2-norm at the end)
-    const double s = (nrm > 0.0) ? 1.0 / nrm : 1.0;
-    for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] *= s;
+    const double sc = (nrm > 0.0) ? 1.0 / nrm : 1.0;
+    for (int i = 0; i < n; ++i) Z[(size_t)i * zs] *= sc;
   }
   double s2 = 0.0;
   for (int i = 0; i < n; ++i) {
-    const double v = Zt[(size_t)k + (size_t)i * cnt];
+    const double v = Z[(size_t)i * zs];
     s2 += v * v;
   }
   const double inv = 1.0 / sqrt(s2);
-  for (int i = 0; i < n; ++i) Zt[(size_t)k + (size_t)i * cnt] *= inv;
+  for (int i = 0; i < n; ++i) Z[(size_t)i * zs] *= inv;
+}
+
+// Eigenvectors k0 .. k0+cnt-1, one thread each, arrays in global memory
+// (transposed, stride cnt): Zt[k + i*cnt] = z_k(i).
+__global__ void inviter_kernel(const double* d, const double* e, int n, const double* w, int k0,
+                               int cnt, double tnorm, double* Zt, double* U1, double* U2,
+                               double* U3, double* L, unsigned char* P) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  inviter_one(d, e, n, w[k0 + k], tnorm, Zt + k, cnt, U1 + k, U2 + k, U3 + k, L + k, P + k, cnt);
+}
+
+// Small tridiagonals (n <= kSmallTrd): 32 eigenvectors per CTA with the factor
+// and vector arrays in shared memory (an L1-latency recurrence instead of an
+// L2 round trip per step); Z (n x cnt, column-major) written directly.
+__global__ void __launch_bounds__(32)
+    inviter_small_kernel(const double* d, const double* e, int n, const double* w, int k0, int cnt,
+                         double tnorm, double* Z, int64_t ldz) {
+  extern __shared__ double ism[];
+  const int lane = threadIdx.x;
+  double* Zs = ism;                       // [n][33]
+  double* U1 = Zs + (size_t)n * 33;       // [n][32] each
+  double* U2 = U1 + (size_t)n * 32;
+  double* U3 = U2 + (size_t)n * 32;
+  double* Lm = U3 + (size_t)n * 32;
+  unsigned char* P = reinterpret_cast<unsigned char*>(Lm + (size_t)n * 32);
+  const int k = blockIdx.x * 32 + lane;
+  if (k < cnt)
+    inviter_one(d, e, n, w[k0 + k], tnorm, Zs + lane, 33, U1 + lane, U2 + lane, U3 + lane, Lm + lane,
+                P + lane, 32);
+  __syncwarp();
+  const int nv = min(32, cnt - blockIdx.x * 32);
+  for (int v = 0; v < nv; ++v)
+    for (int i = lane; i < n; i += 32) Z[i + (int64_t)(blockIdx.x * 32 + v) * ldz] = Zs[i * 33 + v];
+}
+
+size_t inviter_small_smem(int n) { return (size_t)n * (33 + 4 * 32) * sizeof(double) + (size_t)n * 32; }
+
+void inviter_small_launch(Ctx& ctx, const double* dd, const double* ee, int n, const double* wv, int k0,
+                          int cnt, double tnorm, double* Z, int64_t ldz) {
+  static bool attr = false;
+  if (!attr) {
+    QDWHG_CUDA(cudaFuncSetAttribute(inviter_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)inviter_small_smem(160)));
+    attr = true;
+  }
+  inviter_small_kernel<<<(cnt + 31) / 32, 32, inviter_small_smem(n), ctx.stream>>>(dd, ee, n, wv, k0, cnt,
+                                                                                  tnorm, Z, ldz);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
 }
 
 // Z(i, k) = Zt[k + i*cnt]   (i < n rows, k < cnt vectors)
@@ -406,6 +453,164 @@ __global__ void square_kernel(const double* e, int n, double* e2) {
     e2[i] = e[i] * e[i];
 }
 
+// ---------------------------------------------------------------- small blocks
+// Rayleigh-Ritz blocks up to kSmallTrd (cfg1/cfg2: ell ~ 50-130) in ONE CTA:
+// the whole matrix lives in shared memory, so a column costs three CTA barriers
+// instead of the cooperative panel's three grid barriers plus the per-panel
+// trailing GEMMs.  Unblocked dsytd2 (lower), same reflector convention as
+// sytrd_panel_kernel (beta = -sign(alpha) ||x||, tau = (beta - alpha)/beta,
+// v = [1; x(2:)/(alpha - beta)]).
+constexpr int kSmallTrd = 160;
+constexpr int kSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    sytd2_small_kernel(const double* S, int64_t lds, int n, double* d, double* e, double* tau,
+                       double* V, int64_t ldv) {
+  extern __shared__ double sm[];
+  const int LD = n | 1;              // odd stride: column reads by row groups are conflict-free
+  double* A = sm;                    // column-major A[c * LD + r], both triangles kept current
+  double* vs = A + (size_t)n * LD;   // reflector (n)
+  double* ps = vs + n + 1;           // p = tau A22 v (n)
+  double* sc = ps + n + 1;           // [0] tau, [1] p.v accumulator
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < n; c += (int)(blockDim.x / 32))
+    for (int r = c + lane; r < n; r += 32)  // lower triangle (all the kernel reads)
+      A[c * LD + r] = 0.5 * (S[r + (int64_t)c * lds] + S[c + (int64_t)r * lds]);
+  // V(:, j): zeros above row j+1 (every column written in full below)
+  for (int c = warp; c < n - 1; c += (int)(blockDim.x / 32))
+    for (int r = lane; r <= c; r += 32) V[r + (int64_t)c * ldv] = 0.0;
+  __syncthreads();
+  for (int i = 0; i + 1 < n; ++i) {
+    const int m = n - i - 1;  // rows i+1 .. n-1
+    const double* x = A + (size_t)i * LD + i + 1;
+    // ---- (a) reflector: one warp (m <= 159: <= 5 entries per lane)
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int r = 1 + lane; r < m; r += 32) s2 = fma(x[r], x[r], s2);
+      s2 = warp_sum(s2);
+      const double alpha = x[0];
+      double beta = alpha, taui = 0.0, scal = 0.0;
+      if (s2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+        taui = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int r = lane; r < m; r += 32) {
+        const double v = (r == 0) ? 1.0 : (s2 > 0.0 ? x[r] * scal : 0.0);
+        vs[r] = v;
+        V[(i + 1 + r) + (int64_t)i * ldv] = v;
+      }
+      if (lane == 0) {
+        d[i] = A[(size_t)i * LD + i];
+        e[i] = beta;
+        tau[i] = taui;
+        sc[0] = taui;
+      }
+    }
+    __syncthreads();
+    const double taui = sc[0];
+    if (taui != 0.0) {
+      // ---- (b) p = tau A22 v: 8 threads per row r of A22 read column r (A symmetric)
+      // (loop bound uniform per warp: the shuffles need all 32 lanes)
+      const int k = tid & 7;
+      for (int r0 = warp * 4; r0 < m; r0 += (int)(blockDim.x / 8)) {
+        const int r = r0 + ((tid >> 3) & 3);
+        // lower triangle only: A22(r, c) = row r left of the diagonal, column r below it
+        const double* A22 = A + (size_t)(i + 1) * LD + i + 1;
+        double acc = 0.0;
+        if (r < m)
+          for (int c = k; c < m; c += 8)
+            acc = fma(c < r ? A22[(size_t)c * LD + r] : A22[(size_t)r * LD + c], vs[c], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (k == 0 && r < m) ps[r] = taui * acc;
+      }
+      __syncthreads();
+      // ---- (c) A22 -= v w^T + w v^T,  w = p - (tau/2)(p.v) v; p.v summed by
+      // every warp redundantly (same order everywhere, no extra barrier)
+      double pv = 0.0;
+      for (int r = lane; r < m; r += 32) pv = fma(ps[r], vs[r], pv);
+      const double a2 = -0.5 * taui * warp_sum(pv);
+      // (lower triangle only; lane = row within a 32-row strip, warp = column)
+      for (int c = warp; c < m; c += (int)(blockDim.x / 32)) {
+        const double vc = vs[c], wc = ps[c] + a2 * vc;
+        double* col = A + (size_t)(i + 1 + c) * LD + i + 1;
+        for (int r = c + lane; r < m; r += 32) col[r] -= vs[r] * wc + (ps[r] + a2 * vs[r]) * vc;
+      }
+    }
+    __syncthreads();  // (also orders sc[0] reads before the next column's write)
+  }
+  if (tid == 0) d[n - 1] = A[(size_t)(n - 1) * LD + n - 1];
+}
+
+// C (n x cnt) <- H_0 H_1 ... H_{n-2} C, H_j = I - tau_j v_j v_j^T acting on rows
+// j+1.. (v_j = V(j+1:, j), unit first entry): the back-transform of the small
+// tridiagonalisation, one CTA, C staged in shared memory.
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    ormtr_small_kernel(const double* V, int64_t ldv, const double* tau, int n, double* C,
+                       int64_t ldc, int cnt) {
+  extern __shared__ double sm[];
+  const int LD = n | 1;
+  double* Cs = sm;                      // Cs[c * LD + r]
+  double* ws = Cs + (size_t)cnt * LD;   // v^T C (cnt)
+  double* vbuf = ws + cnt + 1;          // v ring: [3][n]
+  double* ts = vbuf + 3 * n;            // tau (n)
+  const int tid = threadIdx.x;
+  for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32))
+    for (int r = tid & 31; r < n; r += 32) Cs[c * LD + r] = C[r + (int64_t)c * ldc];
+  for (int r = tid; r < n - 1; r += blockDim.x) ts[r] = tau[r];
+  // v_j (rows j+1..) of the first two reflectors; later ones are prefetched into
+  // registers two steps ahead, so no step waits on a global load
+  for (int q = 0; q < 2 && n - 2 - q >= 0; ++q) {
+    const int j = n - 2 - q;
+    if (tid < n - j - 1) vbuf[q * n + tid] = V[(j + 1 + tid) + (int64_t)j * ldv];
+  }
+  __syncthreads();
+  for (int j = n - 2; j >= 0; --j) {
+    const int m = n - j - 1;
+    const int slot = (n - 2 - j) % 3;
+    double* vs = vbuf + slot * n;
+    double* vn = vbuf + ((slot + 2) % 3) * n;  // reflector j - 2
+    const double pre = (j > 1 && tid <= m + 1) ? V[(j - 1 + tid) + (int64_t)(j - 2) * ldv] : 0.0;
+    const double tj = ts[j];
+    // w_c = tau v^T C(j+1:, c): 8 threads per column
+    const int k = tid & 7;
+    for (int c0 = (tid >> 5) * 4; c0 < cnt; c0 += (int)(blockDim.x / 8)) {  // warp-uniform bound
+      const int c = c0 + ((tid >> 3) & 3);
+      const double* col = Cs + (size_t)c * LD + j + 1;
+      double acc = 0.0;
+      if (c < cnt)
+        for (int r = k; r < m; r += 8) acc = fma(vs[r], col[r], acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (k == 0 && c < cnt) ws[c] = tj * acc;
+    }
+    __syncthreads();
+    for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32)) {
+      double* col = Cs + (size_t)c * LD + j + 1;
+      const double wc = ws[c];
+      for (int r = tid & 31; r < m; r += 32) col[r] -= vs[r] * wc;
+    }
+    if (j > 1 && tid <= m + 1) vn[tid] = pre;
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32))
+    for (int r = tid & 31; r < n; r += 32) C[r + (int64_t)c * ldc] = Cs[c * LD + r];
+}
+
+int small_threads() {
+  static const int t = getenv("QDWHG_SMALL_THREADS") ? atoi(getenv("QDWHG_SMALL_THREADS")) : kSmallThreads;
+  return (t == 256 || t == 512 || t == 1024) ? t : kSmallThreads;
+}
+
+size_t sytd2_small_smem(int n) { return ((size_t)n * (n | 1) + 2 * (n + 1) + 2) * sizeof(double); }
+size_t ormtr_small_smem(int n, int cnt) {
+  return ((size_t)cnt * (n | 1) + (cnt + 1) + 4 * n) * sizeof(double);
+}
+
 }  // namespace
 
 void syev_dc_fallback(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
@@ -415,8 +620,9 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
                   double vhi, int64_t* sel0) {
   const int n = (int)S.rows;
   const Arena::Mark mark = ctx.arena->mark();
+  const bool small = n <= kSmallTrd;
   DMat A = ctx.arena->alloc(n, n);
-  copy(ctx, S, A);
+  if (!small) copy(ctx, S, A);
   const int nb = kTrdNB;
   const int npan = (n - 1 + nb - 1) / nb;  // columns 0 .. n-2 carry reflectors
   DMat Vfull = ctx.arena->alloc(n, std::max(npan * nb, 1));
@@ -431,17 +637,33 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
   QDWHG_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (npan * nb + 8), ctx.stream));
   QDWHG_CUDA(cudaMemsetAsync(ee, 0, sizeof(double) * (n + 8), ctx.stream));
-  QDWHG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (n + 2 * nb + 8), ctx.stream));  // SYMV atomics
-  fill(ctx, Vfull, 0.0, 0.0);
+  if (!small) {
+    QDWHG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (n + 2 * nb + 8), ctx.stream));  // SYMV atomics
+    fill(ctx, Vfull, 0.0, 0.0);
+  }
   static bool trd_attr = false;
   if (!trd_attr) {
     QDWHG_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)kTrdDynSmem));
     trd_attr = true;
   }
+  if (small) {
+    static bool small_attr = false;
+    if (!small_attr) {
+      QDWHG_CUDA(cudaFuncSetAttribute(sytd2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)sytd2_small_smem(kSmallTrd)));
+      QDWHG_CUDA(cudaFuncSetAttribute(ormtr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ormtr_small_smem(kSmallTrd, kSmallTrd)));
+      small_attr = true;
+    }
+    sytd2_small_kernel<<<1, small_threads(), sytd2_small_smem(n), ctx.stream>>>(S.ptr(), S.ld, n, dd, ee, tau,
+                                                                             Vfull.ptr(), Vfull.ld);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+  }
   // all SMs: the per-column SYMV streams the trailing matrix (HBM/L2 bound)
   const int grid = std::max(1, std::min(ctx.num_sms, (n + 31) / 32));
-  for (int p = 0; p < npan; ++p) {
+  for (int p = 0; p < (small ? 0 : npan); ++p) {
     const int j0 = p * nb;
     const int b = std::min(nb, n - 1 - j0);
     QDWHG_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * 64, ctx.stream));
@@ -464,7 +686,7 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     }
   }
   // last diagonal entry (and the one before if the last panel ended early)
-  {
+  if (!small) {
     // d[n-1] = A(n-1, n-1) after all updates (no reflector column touches it again)
     QDWHG_CUDA(cudaMemcpyAsync(dd + (n - 1), A.ptr() + (n - 1) + (int64_t)(n - 1) * A.ld,
                                sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
@@ -512,13 +734,18 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   double* U3 = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
   double* Lm = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * nc));
   unsigned char* Pv = static_cast<unsigned char*>(ctx.arena->alloc_bytes(nc));
-  inviter_kernel<<<(cnt + 63) / 64, 64, 0, ctx.stream>>>(dd, ee, n, wv, i0, cnt, tnorm, Zt, U1, U2, U3,
-                                                        Lm, Pv);
   DMat Z = ctx.arena->alloc(n, cnt);
-  transpose_kernel<<<dim3((cnt + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx.stream>>>(
-      Zt, n, cnt, Z.ptr(), Z.ld);
+  if (small) {
+    inviter_small_launch(ctx, dd, ee, n, wv, i0, cnt, tnorm, Z.ptr(), Z.ld);
+    ctx.count(2);
+  } else {
+    inviter_kernel<<<(cnt + 63) / 64, 64, 0, ctx.stream>>>(dd, ee, n, wv, i0, cnt, tnorm, Zt, U1, U2,
+                                                          U3, Lm, Pv);
+    transpose_kernel<<<dim3((cnt + 31) / 32, (n + 31) / 32), dim3(32, 8), 0, ctx.stream>>>(
+        Zt, n, cnt, Z.ptr(), Z.ld);
+    ctx.count(4);
+  }
   QDWHG_CUDA(cudaGetLastError());
-  ctx.count(4);
   // ---- Lowdin: E = Z^T Z - I;  Z <- Z (I - E/2 + 3/8 E^2)
   DMat E = ctx.arena->alloc(cnt, cnt);
   GemmExtra gr;
@@ -538,6 +765,14 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   // ---- back-transform: Vout = Q Z F, Q = H_0 ... H_{n-2}, blocks applied last to first
   const DMat Vsel = Vout.sub(0, 0, n, cnt);
   gemm(ctx, Op::N, Op::N, 1.0, Z, F, 0.0, Vsel);
+  if (small) {
+    ormtr_small_kernel<<<1, small_threads(), ormtr_small_smem(n, cnt), ctx.stream>>>(
+        Vfull.ptr(), Vfull.ld, tau, n, Vsel.ptr(), Vsel.ld, cnt);
+    QDWHG_CUDA(cudaGetLastError());
+    ctx.count();
+    ctx.arena->release_to(mark);
+    return true;
+  }
   DMat G = ctx.arena->alloc(nb, nb), Tb = ctx.arena->alloc(nb, nb);
   for (int p = npan - 1; p >= 0; --p) {
     const int j0 = p * nb;
@@ -559,6 +794,51 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   }
   ctx.arena->release_to(mark);
   return true;
+}
+
+void tridiag_lowest(Ctx& ctx, const std::vector<double>& d, const std::vector<double>& e,
+                    double* theta, double* z_last) {
+  const int n = (int)d.size();
+  if (n == 0) throw InvalidArgument("tridiag_lowest: empty");
+  if (n == 1) {
+    *theta = d[0];
+    *z_last = 1.0;
+    return;
+  }
+  double lo = 1e308, hi = -1e308, tnorm = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? std::abs(e[i - 1]) : 0.0) + (i + 1 < n ? std::abs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+    tnorm = std::max(tnorm, std::abs(d[i]) + r);
+  }
+  if (!(tnorm > 0.0)) tnorm = 1.0;
+  const double eps = 2.220446049250313e-16;
+  lo -= 2 * eps * tnorm + 1e-300;
+  hi += 2 * eps * tnorm + 1e-300;
+  const double pivmin = std::max(1e-300, eps * eps * tnorm * tnorm * 1e-10);
+  // one packed upload: [d | e | e^2], then w (1), z (n) and the LU scratch
+  std::vector<double> h((size_t)3 * n, 0.0);
+  for (int i = 0; i < n; ++i) h[i] = d[i];
+  for (int i = 0; i + 1 < n; ++i) {
+    h[n + i] = e[i];
+    h[2 * n + i] = e[i] * e[i];
+  }
+  const Arena::Mark mark = ctx.arena->mark();
+  double* dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (size_t)(5 * n + 8)));
+  double *dd = dev, *ee = dev + n, *e2 = dev + 2 * n, *wv = dev + 3 * n, *Zt = wv + 1;
+  QDWHG_CUDA(cudaMemcpyAsync(dev, h.data(), sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx.stream));
+  bisect_kernel<<<1, 32, 0, ctx.stream>>>(dd, e2, n, lo, hi, pivmin, 2 * eps * tnorm * 1e-3, wv);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+  inviter_small_launch(ctx, dd, ee, n, wv, 0, 1, tnorm, Zt, n);
+  double out[2];
+  QDWHG_CUDA(cudaMemcpyAsync(&out[0], wv, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaMemcpyAsync(&out[1], Zt + (n - 1), sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  ctx.arena->release_to(mark);
+  *theta = out[0];
+  *z_last = out[1];
 }
 
 }  // namespace qdwhg

@@ -115,6 +115,24 @@ def test_sym_eig_jacobi(n):
     assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
 
 
+@pytest.mark.parametrize("n", [17, 49, 132, 160, 161])
+@pytest.mark.parametrize("kind", ["spread", "clustered"])
+def test_sym_eig_small_tridiagonal(n, kind):
+    """One-CTA tridiagonalisation path (17..160) and the cooperative one just above,
+    with well-separated and tightly clustered spectra (inverse iteration + Lowdin)."""
+    if kind == "spread":
+        lam = np.linspace(-1.0, 1.0, n)
+    else:
+        lam = np.repeat(np.linspace(-1.0, 1.0, (n + 3) // 4), 4)[:n] + 1e-9 * np.arange(n)
+    q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 7 + n))
+    s = (q * lam) @ q.T
+    s = 0.5 * (s + s.T)
+    vals, v = qdwh.sym_eig_dense(s)
+    np.testing.assert_allclose(vals, np.sort(lam), rtol=0, atol=1e-13 * n)
+    assert np.linalg.norm(s @ v - v * vals) <= 1e-13 * np.linalg.norm(s) * n
+    assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
+
+
 @pytest.mark.parametrize("n", [300, 700])
 def test_sym_eig_divide_and_conquer(n):
     lam = np.linspace(-1.0, 2.0, n) + 0.001 * np.sin(np.arange(n))

@@ -19,6 +19,7 @@ X = (G / (G.norm() ** 0.5)).t().contiguous().t()
 Z = (G.T @ G / n + torch.eye(n, dtype=torch.float64, device=dev)).t().contiguous().t()
 
 
+Xs = ((G + G.T) / (2 * torch.linalg.matrix_norm(G, 2))).t().contiguous().t()
 Ysvd = None
 if what == "svd":
     m2 = int(sys.argv[4]) if len(sys.argv) > 4 else 8 * n
@@ -33,6 +34,8 @@ def call():
         return qdwh.svd_dense(Ysvd, handle=h)
     if what == "chol":
         return qdwh.qdwh_chol_step(X, 0.5, handle=h)
+    if what == "sym":  # one symmetric Cholesky-based step (the EIG path)
+        return qdwh.run_fixed_iterations(Xs, 0.2, 1, handle=h)
     if what == "qr":
         return qdwh.qr_factor(G, handle=h)
     return qdwh.cholesky_factor_inverse(Z, handle=h)
