@@ -216,10 +216,72 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 // (bit-identical to the owner's update: same inputs, same fma).  Then one
 // in-CTA combine and one cross-CTA reduction (cluster DSMEM or grid atomics),
 // i.e. two CTA barriers + one cluster/grid barrier per column.
+// T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise),
+// by recursive doubling instead of the column recurrence:
+//   T = [T11, -T11 (V1^T V2) T22; 0, T22],  V1^T V2 = G12,
+// block size s = 1, 2, 4, ... — 2 barriers per level, log2(b) levels.
+// One doubling level of larft with compile-time block size S: the k loops are
+// fully unrolled (zero terms by predicate) so every thread's shared loads are
+// in flight together instead of one load-FMA round trip per term.
+template <int S>
+QDWHG_DEV void larft_level(double (*Ts)[kBW + 1], double (*M)[kBW + 1], double (*Gs)[kBW + 1], int b,
+                           int t) {
+  if (S >= b) return;
+  // M(a+r, a+S+c) = sum_{k=r}^{S-1} T11(r, k) G(a+k, a+S+c)
+  for (int i = t; i < b * S; i += blockDim.x) {
+    const int r = i % S, rest = i / S;
+    const int pair = rest / S, c = rest % S;
+    const int a = pair * 2 * S;
+    if (a + S + c >= b) continue;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double v = (k >= r) ? Ts[a + r][a + k] * Gs[a + k][a + S + c] : 0.0;
+      if (k & 1) acc1 += v;
+      else acc0 += v;
+    }
+    M[a + r][a + S + c] = acc0 + acc1;
+  }
+  __syncthreads();
+  // T12(r, c) = -sum_{k=0}^{c} M(a+r, a+S+k) T22(k, c)
+  for (int i = t; i < b * S; i += blockDim.x) {
+    const int r = i % S, rest = i / S;
+    const int pair = rest / S, c = rest % S;
+    const int a = pair * 2 * S;
+    if (a + S + c >= b) continue;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double v = (k <= c) ? M[a + r][a + S + k] * Ts[a + S + k][a + S + c] : 0.0;
+      if (k & 1) acc1 += v;
+      else acc0 += v;
+    }
+    Ts[a + r][a + S + c] = -(acc0 + acc1);
+  }
+  __syncthreads();
+}
+
+// Fused panel tail (PanelTail): the compact-WY T of the panel is built inside
+// the column loop.  G(c, j) = v_c^T v_j for c < j rides in the otherwise unused
+// slots c < j of the per-column reduction vector (threads of finished columns
+// accumulate a_c . u over their rows during the same register pass), and CTA 0
+// extends T by the LAPACK dlarft column recurrence
+//   T(0:j, j) = -tau_j T(0:j, 0:j) G(0:j, j)
+// while the next reduction is in flight — no Gram GEMM, no larft launch.  The
+// kernel also zeroes V above the panel inside its outer block and (grid path)
+// leaves its barrier/accumulator buffers zeroed for the next launch.
+struct PanelTail {
+  double* T;          // b x b upper T (zeros below) of the panel, ld ldt
+  int64_t ldt;
+  double* vz;         // V rows above the panel that must be zero: zrows x b, ld ldv
+  int zrows;
+  unsigned* ticket;   // grid path: last-CTA election for the buffer cleanup
+};
+
 template <bool CLUSTER, int NRG, int RPT>
 __global__ void __launch_bounds__(64 * NRG, 1)
     geqr2_panel_reg_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
-                           int b, int rpc, double* acc, unsigned* bar) {
+                           int b, int rpc, double* acc, unsigned* bar, PanelTail tl) {
   constexpr int NT = kBW * NRG;
   constexpr int RB = NRG * RPT;  // row capacity per CTA (>= rpc)
   constexpr int RBP = RB + 1;
@@ -234,6 +296,11 @@ __global__ void __launch_bounds__(64 * NRG, 1)
   double* gbuf = tot + 2 * kBW;         // CLUSTER: [2 parity][16 ranks][2*kBW] pushed partials
   double* colsc = gbuf + 2 * 16 * 2 * kBW;  // [kBW] 1/v0 (0: no reflector) | [kBW] beta, per column
   uint64_t* mbar = reinterpret_cast<uint64_t*>(colsc + 2 * kBW);  // CLUSTER: [2] gather barriers
+  // CTA 0: G = V^T V (strict upper; tau_j kept on the diagonal) for the T of the tail
+  double(*Gs)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(mbar + 2);
+  // larft work arrays after the panel: the staging area when large enough, else
+  // appended after Gs
+  double* lwork = (kBW * (RB + 1) >= 2 * kBW * (kBW + 1)) ? stage : &Gs[kBW][0];
   const int tid = threadIdx.x;
   const int c = tid % kBW, rg = tid / kBW;
   const int rbeg = blockIdx.x * rpc;
@@ -267,7 +334,7 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     if (tid == 0) {
       const uint32_t bytes = (uint32_t)cg::this_cluster().num_blocks() * 2 * kBW * 8;
       mbar_arrive_expect_tx(&mbar[0], bytes);
-      if (b > 1) mbar_arrive_expect_tx(&mbar[1], bytes);
+      mbar_arrive_expect_tx(&mbar[1], bytes);  // reductions run for col = 0 .. b
     }
   }
   __syncthreads();
@@ -307,14 +374,14 @@ __global__ void __launch_bounds__(64 * NRG, 1)
         tot[tid] = s;
         // re-arm for column col + 2 by a thread that sent nothing (a sender's
         // release-arrive would wait for its own remote stores to land)
-        if (tid == kBW && col + 2 < b) mbar_arrive_expect_tx(&mbar[q], (uint32_t)nb_ * 2 * kBW * 8);
+        if (tid == kBW && col + 2 <= b) mbar_arrive_expect_tx(&mbar[q], (uint32_t)nb_ * 2 * kBW * 8);
       }
       __syncthreads();
     } else {
       double* buf = acc + (col % 3) * (2 * kBW);
       if (tid < 2 * kBW) {
         const int cc = tid % kBW;
-        if (cc < b && cc >= col && mine[tid] != 0.0) atomicAdd(&buf[tid], mine[tid]);
+        if (cc < b && mine[tid] != 0.0) atomicAdd(&buf[tid], mine[tid]);  // (cc < col: Gram slots)
       }
       side();
       grid_sync(bar, epoch);
@@ -376,46 +443,74 @@ __global__ void __launch_bounds__(64 * NRG, 1)
       colsc[jj] = reflect ? inv_v0 : 0.0;
       colsc[kBW + jj] = beta;
     }
-    if (blockIdx.x == 0 && tid == 0) tau_out[jj] = taup;
+    if (blockIdx.x == 0) {
+      if (tid == 0) {
+        tau_out[jj] = taup;
+        Gs[jj][jj] = taup;
+      }
+      // G(c, jj-1), c < jj-1, from the Gram slots of the reduction just completed
+      // (v_c = a_c / v0_c below its diagonal, a_c(jj-1) on row jj-1)
+      if (jj >= 2 && tid < jj - 1)
+        Gs[tid][jj - 1] = colsc[tid] * (tot[tid] + tot[kBW + tid] * colsc[jj - 1]);
+    }
     PANEL_MARK(9, jj);
     double top = 0.0, below = 0.0;
     const int kmask = jj + 1 - rbeg - rg;  // element t has row <= jj+1 iff NRG*t <= kmask
-    if ((tid % kBW) / 32 * 32 + 31 > jj) {  // warps with a column right of the pivot
-      if (kmask < 0) {
-        double bl[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains: FP64 latency, not throughput
+    // columns right of the pivot: H_jj update + partials of column jj+1 (rows > jj+1,
+    // top = row jj+1); finished columns c < jj (sc = 0, unchanged): Gram partials
+    // a_c . u over rows > jj, top = row jj
+    const bool gram = c < jj;
+    if ((tid % kBW) / 32 * 32 + 31 < jj) {
+      // warp of finished columns only: Gram partials, nothing to update
+      const double* U = reinterpret_cast<const double*>(UP);
+      double bl[4] = {0.0, 0.0, 0.0, 0.0};
+      const int lo = kmask - 1;
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) {
-          const int i = rg + NRG * t;
-          const double2 up = UP[i];
-          const double u = up.x;
-          const double pv = fma(-s1, u, up.y);
-          const double an = fma(-sc, u, a[t]);
-          a[t] = an;
-          bl[t & 3] = fma(pv, an, bl[t & 3]);
-        }
-        below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
-      } else {
-        double bl[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int t = 0; t < RPT; ++t) {
+        const int i = rg + NRG * t;
+        bl[t & 3] = (NRG * t > lo) ? fma(U[2 * i], a[t], bl[t & 3]) : bl[t & 3];
+      }
+      below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
+      if (lo >= 0 && lo % NRG == 0) {
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) {
-          const int i = rg + NRG * t;
-          const double2 up = UP[i];
-          const double u = (NRG * t == kmask - 1) ? v0 : up.x;  // row jj: u = v0 (v = 1)
-          const double pv = fma(-s1, u, up.y);
-          const double an = fma(-sc, u, a[t]);
-          a[t] = an;
-          bl[t & 3] = (NRG * t > kmask) ? fma(pv, an, bl[t & 3]) : bl[t & 3];
-        }
-        below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
-        if (kmask % NRG == 0) {
+        for (int t = 0; t < RPT; ++t)
+          if (NRG * t == lo) top = a[t];  // row jj
+      }
+    } else if (kmask < 0) {
+      double bl[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains: FP64 latency, not throughput
 #pragma unroll
-          for (int t = 0; t < RPT; ++t)
-            if (NRG * t == kmask) top = a[t];  // row jj+1
-        }
+      for (int t = 0; t < RPT; ++t) {
+        const int i = rg + NRG * t;
+        const double2 up = UP[i];
+        const double u = up.x;
+        const double pv = fma(-s1, u, up.y);
+        const double an = fma(-sc, u, a[t]);
+        a[t] = an;
+        bl[t & 3] = fma(gram ? u : pv, an, bl[t & 3]);
+      }
+      below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
+    } else {
+      double bl[4] = {0.0, 0.0, 0.0, 0.0};
+      const int lo = gram ? kmask - 1 : kmask;  // rows counted: NRG*t > lo
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const int i = rg + NRG * t;
+        const double2 up = UP[i];
+        const double u = (NRG * t == kmask - 1) ? v0 : up.x;  // row jj: u = v0 (v = 1)
+        const double pv = fma(-s1, u, up.y);
+        const double an = fma(-sc, u, a[t]);
+        a[t] = an;
+        bl[t & 3] = (NRG * t > lo) ? fma(gram ? up.x : pv, an, bl[t & 3]) : bl[t & 3];
+      }
+      below = (bl[0] + bl[1]) + (bl[2] + bl[3]);
+      if (lo >= 0 && lo % NRG == 0) {
+#pragma unroll
+        for (int t = 0; t < RPT; ++t)
+          if (NRG * t == lo) top = a[t];  // row jj+1 (gram: row jj)
       }
     }
     PANEL_MARK(10, jj);
-    if (!((jj + 1 < b) && c < b && c > jj)) top = below = 0.0;
+    if (!(c < b && (c > jj ? jj + 1 < b : gram))) top = below = 0.0;
     // snapshots of columns jj+1 (zero above its diagonal) and jj+2 (owners
     // only), written while the partial sums are in flight
     auto snapshots = [&] {
@@ -427,16 +522,18 @@ __global__ void __launch_bounds__(64 * NRG, 1)
         for (int t = 0; t < RPT; ++t) UPn[2 * (rg + NRG * t) + 1] = a[t];
       }
     };
-    if (jj + 1 < b) {
-      red[rg * 2 * kBW + c] = top;
-      red[rg * 2 * kBW + kBW + c] = below;
-      PANEL_MARK(11, jj);
-      __syncthreads();
-      PANEL_MARK(12, jj);
-      reduce(jj + 1, snapshots);
-      PANEL_MARK(13, jj);
-    }
+    red[rg * 2 * kBW + c] = top;
+    red[rg * 2 * kBW + kBW + c] = below;
+    PANEL_MARK(11, jj);
+    __syncthreads();
+    PANEL_MARK(12, jj);
+    // (jj + 1 == b: the last reduction carries only the Gram slots of column b-1)
+    reduce(jj + 1, snapshots);
+    PANEL_MARK(13, jj);
   }
+  // last G column (j = b-1) from the final reduction
+  if (blockIdx.x == 0 && tid < b - 1)
+    Gs[tid][b - 1] = colsc[tid] * (tot[tid] + tot[kBW + tid] * colsc[b - 1]);
   if (CLUSTER) cg::this_cluster().sync();  // peers may still write into our buffers
   __syncthreads();
   // ---- pivot columns: v = a / v0 below the diagonal, beta on it; then R (upper,
@@ -460,59 +557,56 @@ __global__ void __launch_bounds__(64 * NRG, 1)
       A[gr + (int64_t)cc * lda] = (gr <= cc) ? x : 0.0;
       V[gr + (int64_t)cc * ldv] = (gr < cc) ? 0.0 : (gr == cc ? 1.0 : x);
     }
+  // ---- T (LAPACK dlarft) of the panel by CTA 0: recursive doubling on G
+  if (blockIdx.x == 0) {
+    __syncthreads();  // staging reads of the write-out done (lwork may alias it)
+    double(*Ts)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(lwork);
+    double(*M)[kBW + 1] = reinterpret_cast<double(*)[kBW + 1]>(lwork + kBW * (kBW + 1));
+    for (int q = tid; q < kBW * kBW; q += NT) {
+      const int r = q % kBW, cc = q / kBW;
+      Ts[r][cc] = (r == cc && r < b) ? Gs[r][r] : 0.0;
+    }
+    __syncthreads();
+    larft_level<1>(Ts, M, Gs, b, tid);
+    larft_level<2>(Ts, M, Gs, b, tid);
+    larft_level<4>(Ts, M, Gs, b, tid);
+    larft_level<8>(Ts, M, Gs, b, tid);
+    larft_level<16>(Ts, M, Gs, b, tid);
+    larft_level<32>(Ts, M, Gs, b, tid);
+    for (int q = tid; q < b * b; q += NT) {
+      const int r = q % b, cc = q / b;
+      tl.T[r + (int64_t)cc * tl.ldt] = Ts[r][cc];
+    }
+  }
+  // V rows above the panel inside its outer block are zero (GEMMs read them)
+  for (int q = blockIdx.x * NT + tid; q < tl.zrows * b; q += gridDim.x * NT) {
+    const int r = q % tl.zrows, cc = q / tl.zrows;
+    tl.vz[r + (int64_t)cc * ldv] = 0.0;
+  }
+  if (!CLUSTER) {
+    // leave the barrier counter and accumulators zeroed for the next launch: the
+    // last CTA to get here knows every CTA has passed its final grid barrier
+    __shared__ bool last;
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(tl.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      for (int q = tid; q < 3 * 2 * kBW; q += NT) acc[q] = 0.0;
+      if (tid == 0) {
+        *bar = 0u;
+        *tl.ticket = 0u;
+      }
+    }
+  }
 }
 
 template <int NRG, int RPT>
 size_t panel_reg_smem() {
   constexpr int RB = NRG * RPT;
   return ((size_t)kBW * (RB + 1) + 4 * RB + NRG * 2 * kBW + 4 * kBW + 2 * kBW + 2 * 16 * 2 * kBW +
-          2 * kBW + 2) *
-         8;
-}
-
-// T (b x b upper) from G = V^T V and tau' (LAPACK dlarft, forward/columnwise),
-// by recursive doubling instead of the column recurrence:
-//   T = [T11, -T11 (V1^T V2) T22; 0, T22],  V1^T V2 = G12,
-// block size s = 1, 2, 4, ... — 2 barriers per level, log2(b) levels.
-// One doubling level of larft with compile-time block size S: the k loops are
-// fully unrolled (zero terms by predicate) so every thread's shared loads are
-// in flight together instead of one load-FMA round trip per term.
-template <int S>
-QDWHG_DEV void larft_level(double (*Ts)[kBW + 1], double (*M)[kBW + 1], double (*Gs)[kBW + 1], int b,
-                           int t) {
-  if (S >= b) return;
-  // M(a+r, a+S+c) = sum_{k=r}^{S-1} T11(r, k) G(a+k, a+S+c)
-  for (int i = t; i < b * S; i += blockDim.x) {
-    const int r = i % S, rest = i / S;
-    const int pair = rest / S, c = rest % S;
-    const int a = pair * 2 * S;
-    if (a + S + c >= b) continue;
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-      const double v = (k >= r) ? Ts[a + r][a + k] * Gs[a + k][a + S + c] : 0.0;
-      if (k & 1) acc1 += v;
-      else acc0 += v;
-    }
-    M[a + r][a + S + c] = acc0 + acc1;
-  }
-  __syncthreads();
-  // T12(r, c) = -sum_{k=0}^{c} M(a+r, a+S+k) T22(k, c)
-  for (int i = t; i < b * S; i += blockDim.x) {
-    const int r = i % S, rest = i / S;
-    const int pair = rest / S, c = rest % S;
-    const int a = pair * 2 * S;
-    if (a + S + c >= b) continue;
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < S; ++k) {
-      const double v = (k <= c) ? M[a + r][a + S + k] * Ts[a + S + k][a + S + c] : 0.0;
-      if (k & 1) acc1 += v;
-      else acc0 += v;
-    }
-    Ts[a + r][a + S + c] = -(acc0 + acc1);
-  }
-  __syncthreads();
+          2 * kBW + 2 + kBW * (kBW + 1) +
+          ((kBW * (RB + 1) >= 2 * kBW * (kBW + 1)) ? 0 : 2 * kBW * (kBW + 1))) *
+         8;  // (+ G and, unless the staging area holds them, the larft work arrays)
 }
 
 __global__ void larft_kernel(const double* G, int64_t ldg, const double* tau, double* T,
@@ -616,7 +710,8 @@ int reg_cluster_limit() {
 
 template <bool CL, int RPT, int NRG = 8>
 void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr, int64_t ldv,
-                      double* tau_dev, int mp, int b, int rpc, double* acc, unsigned* bar) {
+                      double* tau_dev, int mp, int b, int rpc, double* acc, unsigned* bar,
+                      PanelTail tl) {
   auto kern = geqr2_panel_reg_kernel<CL, NRG, RPT>;
   const size_t smem = panel_reg_smem<NRG, RPT>();
   static bool set = false;
@@ -638,11 +733,11 @@ void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr,
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
     cfg.numAttrs = 1;
-    QDWHG_CUDA(cudaLaunchKernelEx(&cfg, kern, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar));
+    QDWHG_CUDA(cudaLaunchKernelEx(&cfg, kern, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl));
   } else {
-    QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
-    QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
-    void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, &mp, &b, &rpc, &acc, &bar};
+    // acc / bar / ticket are zero on entry (geqrf zeroes them once; every grid
+    // launch leaves them zeroed)
+    void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, &mp, &b, &rpc, &acc, &bar, &tl};
     QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(nblk), dim3(64 * NRG), args, smem,
                                            ctx.stream));
   }
@@ -652,7 +747,7 @@ void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr,
 // Register-resident panel when the panel fits (cluster of <= 16 CTAs x 256
 // rows, or a cooperative grid of <= #SMs CTAs x 256 rows); false otherwise.
 bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
-                      unsigned* bar) {
+                      unsigned* bar, const PanelTail& tl) {
   static const bool disabled = getenv("QDWHG_PANEL_SMEM") != nullptr;
   if (disabled) return false;
   const int mp = (int)P.rows, b = (int)P.cols;
@@ -665,17 +760,17 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
   // cluster (deterministic DSMEM reduction, hardware barrier)
   if (ceil_div(mp, 8 * 4) <= csmax) {
     const int cs = ceil_div(mp, 8 * 4), rpc = ceil_div(mp, cs);
-    launch_panel_reg<true, 4>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<true, 4>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   if (ceil_div(mp, 8 * 8) <= csmax) {
     const int cs = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, cs);
-    launch_panel_reg<true, 8>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<true, 8>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   if (ceil_div(mp, 8 * 16) <= csmax) {
     const int cs = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, cs);
-    launch_panel_reg<true, 16>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<true, 16>(ctx, cs, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   // (a 16-CTA cluster of 256-row CTAs was slower than the grid path at 4096
@@ -688,37 +783,39 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
       ctx.panel_max_ctas > 0 ? std::min(ctx.panel_max_ctas, ctx.num_sms) : ctx.num_sms;
   if (ceil_div(mp, 8 * 8) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
-    launch_panel_reg<false, 8>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<false, 8>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   if (ceil_div(mp, 8 * 16) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
-    launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   if (ceil_div(mp, 8 * 32) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
-    launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+    launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
   if (max_ctas < ctx.num_sms) {  // taller than the cap allows: uncapped
     if (ceil_div(mp, 8 * 16) <= ctx.num_sms) {
       const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
-      launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+      launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
       return true;
     }
     if (ceil_div(mp, 8 * 32) <= ctx.num_sms) {
       const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
-      launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar);
+      launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
       return true;
     }
   }
   return false;
 }
 
-void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
-                  unsigned* bar) {
-  if (panel_factor_reg(ctx, P, Vp, tau_dev, acc, bar)) return;
+// Returns true when the panel's T (and the zeroed V rows above it) came out of
+// the fused register-panel kernel; false: the caller forms T (Gram + larft).
+bool panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, double* acc,
+                  unsigned* bar, const PanelTail& tl) {
+  if (panel_factor_reg(ctx, P, Vp, tau_dev, acc, bar, tl)) return true;
   // shared-memory panel kernel: panels taller than the register path covers
   int mp = (int)P.rows, b = (int)P.cols;
   static bool set = false;
@@ -755,7 +852,7 @@ void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
     QDWHG_CUDA(cudaLaunchKernelEx(&cfg, geqr2_panel_kernel<true>, Ap, lda, Vptr, ldv, tau_dev, mp, b,
                                   rpc, acc, bar));
     ctx.count();
-    return;
+    return false;
   }
   // grid path (tall panels): cooperative launch over up to all SMs
   const int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
@@ -767,6 +864,10 @@ void panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
   QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)geqr2_panel_kernel<false>, dim3(nblk),
                                          dim3(kPanelThreads), args, panel_smem(rpc), ctx.stream));
   ctx.count();
+  // the register kernels expect zeroed buffers on entry
+  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
+  return false;
 }
 
 }  // namespace
@@ -805,8 +906,9 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   w.T = ctx.arena->alloc(nbo, nout * nbo);
   fill(ctx, w.T, 0.0, 0.0);
   double* tau_dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 64)));
-  double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW));
-  unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
+  double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW + 256));
+  unsigned* bar = reinterpret_cast<unsigned*>(acc + 3 * 2 * kBW);  // [0] barrier, [32] ticket
+  QDWHG_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * 3 * 2 * kBW + 256, ctx.stream));
   DMat G = ctx.arena->alloc(nbo, nbo);
   static const bool no_la = getenv("QDWHG_QR_NO_LOOKAHEAD") != nullptr;
   const bool lookahead = !no_la && ctx.side != nullptr && n > 2 * nbo;
@@ -845,12 +947,19 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
       const int64_t j0 = jo + ji;
       const int64_t mp = m - j0;
       const DMat Vp = w.V.sub(j0, j0, mp, bi);
-      panel_factor(ctx, A.sub(j0, j0, mp, bi), Vp, tau_dev + j0, acc, bar);
-      if (j0 > 0) fill(ctx, w.V.sub(0, j0, j0, bi), 0.0, 0.0);  // V above the panel is zero
-      const DMat Gp = G.sub(0, 0, bi, bi);
-      gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
       const DMat Ti = To.sub(ji, ji, bi, bi);
-      larft_launch(ctx, Gp, tau_dev + j0, Ti);
+      PanelTail tl;
+      tl.T = Ti.ptr();
+      tl.ldt = Ti.ld;
+      tl.zrows = (int)ji;  // V rows jo .. j0-1 of the panel columns (read by the outer-block GEMMs)
+      tl.vz = w.V.sub(jo, j0, std::max<int64_t>(ji, 1), bi).ptr();
+      tl.ticket = bar + 32;
+      if (!panel_factor(ctx, A.sub(j0, j0, mp, bi), Vp, tau_dev + j0, acc, bar, tl)) {
+        if (j0 > 0) fill(ctx, w.V.sub(0, j0, j0, bi), 0.0, 0.0);  // V above the panel is zero
+        const DMat Gp = G.sub(0, 0, bi, bi);
+        gemm(ctx, Op::T, Op::N, 1.0, Vp, Vp, 0.0, Gp);
+        larft_launch(ctx, Gp, tau_dev + j0, Ti);
+      }
       blocks.push_back({ji, bi});
       const int64_t nc = bo - ji - bi;  // rest of the outer block
       if (nc > 0) {
