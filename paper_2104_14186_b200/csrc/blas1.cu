@@ -191,12 +191,9 @@ __global__ void mirror_kernel(double* X, int64_t ld, int64_t n) {
 }
 
 __global__ void zero_strict_lower_kernel(double* X, int64_t ld, int64_t m, int64_t n) {
-  const int64_t total = m * n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % m, j = idx / m;
-    if (i > j) X[i + j * ld] = 0.0;
-  }
+  // block per column (grid-stride), threads down the rows below the diagonal
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x)
+    for (int64_t i = j + 1 + threadIdx.x; i < m; i += blockDim.x) X[i + j * ld] = 0.0;
 }
 
 }  // namespace
@@ -382,8 +379,8 @@ void mirror_lower_to_upper(Ctx& ctx, const DMat& X) {
 }
 
 void zero_strict_lower(Ctx& ctx, const DMat& X) {
-  zero_strict_lower_kernel<<<grid_for(ctx, X.rows * X.cols, 256), 256, 0, ctx.stream>>>(
-      X.ptr(), X.ld, X.rows, X.cols);
+  zero_strict_lower_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(X.cols, 8LL * ctx.num_sms)), 256, 0,
+                             ctx.stream>>>(X.ptr(), X.ld, X.rows, X.cols);
   QDWHG_CUDA(cudaGetLastError());
   ctx.count();
 }

@@ -128,6 +128,9 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
     sx.split_k = 1;
     sx.force_bm = 128;
     on_side(ctx.ev_side, [&] {
+      // W^-1's strictly lower part (never written by the chain) zeroed off the
+      // critical path; the main stream reads it only after waiting on ev_side
+      zero_strict_lower(ctx, Winv);
       // Z22 lower in <= 64-tile pieces: two lower diagonal quarters + one full block
       const int64_t h1 = ((n2 / 2 + 127) / 128) * 128, h2 = n2 - h1;
       GemmExtra lo = sx;
@@ -166,7 +169,8 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
               }
             });
             y1_pending = true;
-          });
+          },
+          /*winv_lower_zeroed=*/true);
     } catch (...) {
       ctx.stream = main_stream;
       QDWHG_CUDA(cudaStreamSynchronize(ctx.side));

@@ -206,7 +206,7 @@ bool trtri_upper(Ctx& ctx, const DMat& R, const DMat& Rinv);
 // Top-level split of the fast variant with overlap hooks (see potrf.cu).
 void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
                       const std::function<void()>& z22_ready,
-                      const std::function<void()>& left_done);
+                      const std::function<void()>& left_done, bool winv_lower_zeroed = false);
 
 // ------------------------------------------------------------------ geqrf.cu
 struct QrWork {

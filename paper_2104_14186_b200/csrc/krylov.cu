@@ -150,38 +150,77 @@ __global__ void __launch_bounds__(kLzThreads, 1) lanczos_kernel(LanczosArgs a) {
     double* Qj = a.Q + (int64_t)j * a.ldq;
     if (j > 0)
       for (int i = tid; i < nown; i += kLzThreads) Qj[r0 + i] = qsrc[r0 + i] * qs;
-    // ---- w_i = (A q_j)_i for owned i: warp per column, 4 independent chains
-    double alpha_acc = 0.0;
+    // ---- w_i = (A q_j)_i for owned i, reading only the LOWER triangle of A (A is
+    // symmetric): the n^2/2 footprint stays L2-resident across the steps for
+    // n up to ~5000, and every element is read twice (column strip of its
+    // column owner, row strip of its row owner) — n * chunk reads per CTA.
+    //  (a) column strip: sum_{r >= i} A(r, i) q_r, warp per owned column i
     for (int ii = warp; ii < nown; ii += NW) {
-      const double* col = a.A + (int64_t)(r0 + ii) * a.lda;
+      const int i = r0 + ii;
+      const double* col = a.A + (int64_t)i * a.lda;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (vec2) {
         const double2* c2 = reinterpret_cast<const double2*>(col);
         const double2* q2 = reinterpret_cast<const double2*>(qsrc);
         const int n2 = n / 2;
-        int r = lane;
+        const int p0 = i >> 1;  // first pair holding row i (row i-1 masked when i is odd)
+        int r = p0 + lane;
         for (; r + 32 < n2; r += 64) {
           const double2 x = c2[r], y = c2[r + 32];
           const double2 u = q2[r], v = q2[r + 32];
-          s0 = fma(x.x, u.x, s0);
+          s0 = fma((2 * r >= i) ? x.x : 0.0, u.x, s0);
           s1 = fma(x.y, u.y, s1);
           s2 = fma(y.x, v.x, s2);
           s3 = fma(y.y, v.y, s3);
         }
         if (r < n2) {
           const double2 x = c2[r], u = q2[r];
-          s0 = fma(x.x, u.x, s0);
+          s0 = fma((2 * r >= i) ? x.x : 0.0, u.x, s0);
           s1 = fma(x.y, u.y, s1);
         }
       } else {
-        for (int r = lane; r < n; r += 32) s0 = fma(col[r], qsrc[r], s0);
+        for (int r = i + lane; r < n; r += 32) s0 = fma(col[r], qsrc[r], s0);
       }
-      const double wv = warp_sum((s0 + s1) + (s2 + s3)) * qs;
-      if (lane == 0) {
-        w_own[ii] = wv;
-        alpha_acc = fma(qsrc[r0 + ii] * qs, wv, alpha_acc);
-      }
+      const double wv = warp_sum((s0 + s1) + (s2 + s3));
+      //  (c) the diagonal block left of the diagonal: sum_{r0 <= c < i} A(i, c) q_c
+      double dc = 0.0;
+      for (int cc = r0 + lane; cc < i; cc += 32) dc = fma(a.A[i + (int64_t)cc * a.lda], qsrc[cc], dc);
+      dc = warp_sum(dc);
+      if (lane == 0) w_own[ii] = wv + dc;
     }
+    //  (b) row strip left of the diagonal block: sum_{c < r0} A(i, c) q_c, lanes
+    //      over the owned rows (coalesced column segments), warps over columns
+    //      in a fixed interleave, partials summed in warp order
+    {
+      double* rpart = red + 32;  // [NW][chunk]
+      for (int rb = 0; rb < nown; rb += 32) {
+        const int ii = rb + lane;
+        const bool own = ii < nown;
+        const double* rowp = a.A + (r0 + (own ? ii : 0));
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int cc = warp;
+        for (; cc + 3 * NW < r0; cc += 4 * NW) {
+          const double x0 = rowp[(int64_t)cc * a.lda], x1 = rowp[(int64_t)(cc + NW) * a.lda];
+          const double x2 = rowp[(int64_t)(cc + 2 * NW) * a.lda], x3 = rowp[(int64_t)(cc + 3 * NW) * a.lda];
+          s0 = fma(x0, qsrc[cc], s0);
+          s1 = fma(x1, qsrc[cc + NW], s1);
+          s2 = fma(x2, qsrc[cc + 2 * NW], s2);
+          s3 = fma(x3, qsrc[cc + 3 * NW], s3);
+        }
+        for (; cc < r0; cc += NW) s0 = fma(rowp[(int64_t)cc * a.lda], qsrc[cc], s0);
+        if (own) rpart[warp * chunk + ii] = (s0 + s1) + (s2 + s3);
+      }
+      __syncthreads();
+      for (int ii = tid; ii < nown; ii += kLzThreads) {
+        double sm = 0.0;
+        for (int k = 0; k < NW; ++k) sm += rpart[k * chunk + ii];
+        w_own[ii] = (w_own[ii] + sm) * qs;
+      }
+      __syncthreads();
+    }
+    double alpha_acc = 0.0;
+    for (int ii = tid; ii < nown; ii += kLzThreads) alpha_acc = fma(qsrc[r0 + ii] * qs, w_own[ii], alpha_acc);
+    alpha_acc = warp_sum(alpha_acc);
     if (lane == 0) red[warp] = alpha_acc;
     __syncthreads();
     if (tid == 0) {
@@ -358,7 +397,7 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre
   // one CTA per SM (co-resident for the grid barriers), at least 16 rows each
   const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, n / 16));
   const int chunk = (int)((n + G - 1) / G);
-  const size_t smem = (size_t)(chunk + 96) * 8;
+  const size_t smem = (size_t)(chunk + 96 + (kLzThreads / 32) * chunk) * 8;
   if (smem > 200 * 1024) throw InvalidArgument("lanczos_min_bound: matrix too large");
   static bool lz_attr = false;
   if (!lz_attr) {

@@ -512,17 +512,19 @@ void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int6
 // Z is overwritten (lower triangle workspace), Winv receives W^-1 (upper).
 void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
                       const std::function<void()>& z22_ready,
-                      const std::function<void()>& left_done) {
+                      const std::function<void()>& left_done, bool winv_lower_zeroed) {
   const int64_t n = Z.rows;
   const int nb = 128;
   if (n1 % nb || n1 <= 0 || n1 >= n) throw InvalidArgument("potrf_fast_split: bad split");
   QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);
-  fill(ctx, W, 0.0, 0.0);
-  fill(ctx, Winv, 0.0, 0.0);
+  // W: only its off-diagonal upper blocks W12 are used, each written before it is
+  // read (no fill).  W^-1: the chain writes every upper entry (upper-only leaves,
+  // W^-1_12 blocks); the strictly lower part must read as zero — zeroed here, or
+  // by the caller (on its side stream, overlapping the SYRK)
+  if (!winv_lower_zeroed) zero_strict_lower(ctx, Winv);
   const int64_t n2 = n - n1;
-  // W and W^-1 are pre-zeroed; W's diagonal blocks are never read
   const int leaf = kDiagUpperOnly | kDiagNoW;
   chol_inv_rec(ctx, Z, W, Winv, 0, n1, nb, leaf);
   left_done();
@@ -581,8 +583,10 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);
-  fill(ctx, W, 0.0, 0.0);
-  fill(ctx, Winv, 0.0, 0.0);
+  // (the fast path without W output reads only W12 blocks it wrote first)
+  if (stable || want_w) fill(ctx, W, 0.0, 0.0);
+  if (stable) fill(ctx, Winv, 0.0, 0.0);
+  else zero_strict_lower(ctx, Winv);  // upper part fully written by the chain
   if (!stable) {
     chol_inv_rec(ctx, Z, W, Winv, 0, n, nb, kDiagUpperOnly | (want_w ? 0 : kDiagNoW));
   } else {
