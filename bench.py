@@ -518,6 +518,17 @@ def main():
                             "measured": "CUDA events around each GEMM launch (on its own stream) in a "
                                         "second pass of the same steps (events in the value pass would "
                                         "block PDL); achieved = flops / union of the launch intervals"}
+        # DRAM bytes per GEMM launch from the committed `ncu --set full` capture of
+        # this config's solve (tools/ncu_gemm_traffic.py), when present
+        tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                          f"r01_gemm_traffic_cfg{args.config}.json")
+        if os.path.exists(tp):
+            tr = json.load(open(tp))
+            line["roofline"]["traffic"] = tr["traffic_bytes_per_launch_time_weighted"]
+            line["roofline"]["traffic_note"] = (
+                f"dram__bytes_read.sum + dram__bytes_write.sum per GEMM launch, time-weighted mean over "
+                f"{tr['launches']} launches of one solve captured with ncu --set full ({os.path.basename(tp)}); "
+                f"mean flops per launch {kst['gemm_flops'] / max(1, kst['gemm_timed_launches']):.3e}")
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(args.config)
         if cb:
