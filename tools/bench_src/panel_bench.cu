@@ -7,6 +7,7 @@
 #include "../../paper_2104_14186_b200/csrc/geqrf.cu"
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 using namespace qdwhg;
@@ -28,11 +29,15 @@ int main() {
     cudaMalloc(&A0, 8 * ld * b);
     cudaMalloc(&V, 8 * ld * b);
     cudaMalloc(&tau, 8 * 64);
-    cudaMalloc(&acc, 8 * 3 * 128);
-    cudaMalloc(&bar, 256);
+    cudaMalloc(&acc, 8 * 3 * 128 + 256);
+    cudaMemset(acc, 0, 8 * 3 * 128 + 256);
+    bar = reinterpret_cast<unsigned*>(acc + 3 * 128);
+    double* T;
+    cudaMalloc(&T, 8 * 64 * 64);
     cudaMalloc(&flag, 4);
     cudaMemcpy(A0, h.data(), 8 * ld * b, cudaMemcpyHostToDevice);
     Ctx ctx;
+    if (getenv("CAP")) ctx.panel_max_ctas = atoi(getenv("CAP"));
     ctx.dflag = flag;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -42,7 +47,13 @@ int main() {
     for (int it = 0; it < reps + 3; ++it) {
       cudaMemcpy(A, A0, 8 * ld * b, cudaMemcpyDeviceToDevice);
       cudaEventRecord(e0);
-      panel_factor(ctx, DMat{A, ld, 0, 0, mp, b}, DMat{V, ld, 0, 0, mp, b}, tau, acc, bar);
+      PanelTail tl;
+      tl.T = T;
+      tl.ldt = 64;
+      tl.vz = V;
+      tl.zrows = 0;
+      tl.ticket = bar + 32;
+      panel_factor(ctx, DMat{A, ld, 0, 0, mp, b}, DMat{V, ld, 0, 0, mp, b}, tau, acc, bar, tl);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -94,7 +105,7 @@ int main() {
     }
     for (int j = 0; j < b; ++j) et = std::max(et, std::abs(gt[j] - htau[j]));
     printf("  max|dR| %.2e (|R| %.1f)  max|dV| %.2e  max|dtau| %.2e\n", er, rmax, ev, et);
-    cudaFree(A); cudaFree(A0); cudaFree(V); cudaFree(tau); cudaFree(acc); cudaFree(bar); cudaFree(flag);
+    cudaFree(A); cudaFree(A0); cudaFree(V); cudaFree(tau); cudaFree(acc); cudaFree(T); cudaFree(flag);
   }
   return 0;
 }
