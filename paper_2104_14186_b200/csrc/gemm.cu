@@ -48,6 +48,12 @@ struct GemmParams {
   int a_bs0, a_bs1, b_bs0, b_bs1;
   int64_t d_bs, cin_bs;
   int nbatch;
+  // tail launch of a wave-balanced GEMM: tiles tile0 .. tile0 + gridDim.x - 1,
+  // split-K partials stored compactly per tile ([z][tile][BM x BN], ld = BM)
+  int tile0;
+  int ntl;       // tiles in this launch (0 = all)
+  int compact;
+  double flop_frac;  // share of the GEMM's algorithmic flops in this launch (profiling)
 };
 
 template <bool KMAJ>
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   int tm, tn;
-  tile_coords(p, blockIdx.x, tm, tn);
+  tile_coords(p, p.tile0 + blockIdx.x, tm, tn);
   const int m0 = tm * BM, n0 = tn * BN;
   int kb, ke;
   k_range<BM, BN>(p, m0, n0, kb, ke);
@@ -276,8 +282,11 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
   __syncthreads();
   constexpr int NW = WM * WN;
   const bool split = p.splits > 1;
-  double* D = split ? p.partial + (size_t)blockIdx.z * p.M * p.N : Dp;
-  const int64_t ldd = split ? p.M : p.ldd;
+  double* D = split ? (p.compact ? p.partial + ((int64_t)blockIdx.z * gridDim.x + blockIdx.x) * (BM * BN) -
+                                      m0 - (int64_t)n0 * BM
+                                : p.partial + (size_t)blockIdx.z * p.M * p.N)
+                    : Dp;
+  const int64_t ldd = split ? (p.compact ? BM : p.M) : p.ldd;
   const bool lower = !split && p.omode != (int)OutMode::Full;
   const bool mirror = !split && p.omode == (int)OutMode::LowerMirror;
   const bool vec = ((reinterpret_cast<uintptr_t>(D) & 15) == 0) && ((ldd & 1) == 0) &&
@@ -369,6 +378,31 @@ __global__ void splitk_reduce_kernel(const GemmParams p) {
     p.D[i + (size_t)j * p.ldd] = v;
     if (mirror && i != j) p.D[j + (size_t)i * p.ldd] = v;
   }
+}
+
+// Reduction of a compact split-K tail launch: block t sums the partials of
+// tile tile0 + t and applies the epilogue (alpha, beta Cin, diag, lower/mirror).
+template <int BM>
+__global__ void splitk_reduce_tiles_kernel(const GemmParams p, int ntail) {
+  const int t = blockIdx.x;
+  int tm, tn;
+  tile_coords(p, p.tile0 + t, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BM;
+  const bool lower = p.omode != (int)OutMode::Full;
+  const bool mirror = p.omode == (int)OutMode::LowerMirror;
+  griddep_wait();
+  for (int e = threadIdx.x; e < BM * BM; e += blockDim.x) {
+    const int i = m0 + e % BM, j = n0 + e / BM;
+    if (i >= p.M || j >= p.N || (lower && i < j)) continue;
+    double s = 0.0;
+    for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * ntail + t) * (BM * BM) + e];
+    double v = p.alpha * s;
+    if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
+    if (i == j) v += p.diag_add;
+    p.D[i + (size_t)j * p.ldd] = v;
+    if (mirror && i != j) p.D[j + (size_t)i * p.ldd] = v;
+  }
+  griddep_launch_dependents();
 }
 
 // ---------------------------------------------------------------- host side
@@ -472,7 +506,9 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
   const CUtensorMap ta = AK ? make_desc(A, 16, BM) : make_desc(A, 16, 16);
   const CUtensorMap tb = BK_ ? make_desc(B, 16, BN) : make_desc(B, 16, 16);
   int ntiles;
-  if (p.omode != (int)OutMode::Full)
+  if (p.ntl > 0)
+    ntiles = p.ntl;
+  else if (p.omode != (int)OutMode::Full)
     ntiles = p.tiles_n * (p.tiles_n + 1) / 2;
   else
     ntiles = p.tiles_m * p.tiles_n;
@@ -489,7 +525,7 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
     char tag[160];
     snprintf(tag, sizeof(tag), "BM=%d AK=%d BK=%d M=%d N=%d K=%d kmode=%d omode=%d splits=%d grid=%d",
              BM, (int)AK, (int)BK_, p.M, p.N, p.K, p.kmode, p.omode, p.splits, ntiles * p.splits);
-    ctx.prof_begin(algorithmic_flops(p), tag);
+    ctx.prof_begin(algorithmic_flops(p) * p.flop_frac, tag);
   }
   launch_pdl(ctx, kern, grid, dim3(threads), smem, ta, tb, p);
   if (ctx.profile) ctx.prof_end();
@@ -540,6 +576,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   }
 
   GemmParams p{};
+  p.flop_frac = 1.0;
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
@@ -608,6 +645,42 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
       }
     }
   }
+  // Wave balancing: when the chosen plan is unsplit and its last wave is
+  // partial, run the full waves as one launch and the tail tiles split-K over
+  // the whole machine (compact partials + per-tile reduction) — the tail costs
+  // ceil(tail*s / CTAs) * t/s instead of a whole wave t.  Full K range only
+  // (equal work per tile).
+  int tail_split = 1;
+  int64_t full_tiles = 0, tail_tiles = 0;
+  static const bool no_balance = getenv("QDWHG_GEMM_NO_BALANCE") != nullptr;
+  if (!no_balance && splits == 1 && nb_ == 1 && !tri && ex.split_k == 0) {
+    const int bm = BMt;
+    const int64_t tm = (M + bm - 1) / bm, tn = (N + bm - 1) / bm;
+    const int64_t tiles = (ex.out != OutMode::Full) ? tn * (tn + 1) / 2 : tm * tn;
+    const int per_sm = (bm == 32) ? 2 : 1;
+    const int64_t conc = (int64_t)ctx.num_sms * per_sm;
+    const int64_t full = (tiles / conc) * conc, tail = tiles - full;
+    const double eff = (bm == 128) ? 0.95 : (bm == 64) ? 0.75 : 0.45;
+    const double t_full = (double)bm * bm * keff / (sm_rate * eff / per_sm);
+    if (full > 0 && tail > 0) {
+      double plain = std::ceil((double)tiles / conc) * (t_full + 2e-6);
+      double bt = plain;
+      for (int sp : {2, 3, 4, 5, 6, 7, 8, 10, 12, 16}) {
+        if (ktiles / sp < 4) continue;
+        const double th = (double)(full / conc) * (t_full + 2e-6) +
+                          std::ceil((double)tail * sp / conc) * (t_full / sp + 2e-6) +
+                          (double)(sp + 2) * tail * bm * bm * 8.0 / 4e12 + 8e-6;
+        if (th < bt * 0.97) {
+          bt = th;
+          tail_split = sp;
+        }
+      }
+      if (tail_split > 1) {
+        full_tiles = full;
+        tail_tiles = tail;
+      }
+    }
+  }
   const bool big = BMt == 128, tiny = BMt == 32;
   p.tiles_m = (int)((M + BMt - 1) / BMt);
   p.tiles_n = (int)((N + BMt - 1) / BMt);
@@ -620,12 +693,43 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   const Arena::Mark mark = ctx.arena->mark();
   if (splits > 1) p.partial = static_cast<double*>(ctx.arena->alloc_bytes((size_t)splits * M * N * 8));
 
-  if (big)
-    dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, Ae, Be, p);
-  else if (tiny)
-    dispatch_layout<32, 32, 2, 2, 8>(ctx, ak, bkm, Ae, Be, p);
-  else
-    dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, Ae, Be, p);
+  auto dispatch = [&](GemmParams& q) {
+    if (big)
+      dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, Ae, Be, q);
+    else if (tiny)
+      dispatch_layout<32, 32, 2, 2, 8>(ctx, ak, bkm, Ae, Be, q);
+    else
+      dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, Ae, Be, q);
+  };
+  if (tail_split > 1) {
+    const double tot_tiles = (double)(full_tiles + tail_tiles);
+    GemmParams p1 = p;  // full waves, fused epilogue
+    p1.ntl = (int)full_tiles;
+    p1.flop_frac = full_tiles / tot_tiles;
+    dispatch(p1);
+    GemmParams p2 = p;  // tail tiles, split-K, compact partials
+    p2.tile0 = (int)full_tiles;
+    p2.ntl = (int)tail_tiles;
+    p2.splits = tail_split;
+    p2.compact = 1;
+    p2.flop_frac = tail_tiles / tot_tiles;
+    p2.partial = static_cast<double*>(
+        ctx.arena->alloc_bytes((size_t)tail_split * tail_tiles * BMt * BMt * 8));
+    dispatch(p2);
+    if (big)
+      launch_pdl(ctx, splitk_reduce_tiles_kernel<128>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
+                 (int)tail_tiles);
+    else if (tiny)
+      launch_pdl(ctx, splitk_reduce_tiles_kernel<32>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
+                 (int)tail_tiles);
+    else
+      launch_pdl(ctx, splitk_reduce_tiles_kernel<64>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
+                 (int)tail_tiles);
+    ctx.count();
+    ctx.arena->release_to(mark);
+    return;
+  }
+  dispatch(p);
 
   if (splits > 1) {
     const int64_t total = M * N;

@@ -27,6 +27,31 @@ def test_gemm_dmma(cuda, ta, tb, m, n, k):
     assert err <= 1e-13 * max(1.0, ref.abs().max().item()) * np.sqrt(k), err
 
 
+@pytest.mark.parametrize("m,n,k,out", [(2048, 2048, 1024, "full"), (2304, 2304, 768, "lower_mirror"),
+                                       (2432, 1920, 640, "full"), (1200, 1200, 2048, "lower")])
+def test_gemm_wave_balanced_tail(cuda, m, n, k, out):
+    """Shapes whose last 128-tile wave is partial: full waves + split-K tail with
+    compact partials and the per-tile reduction (alpha, beta Cin, diag, lower/mirror)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(m + n + k)
+    A = torch.randn((k, m), generator=g, dtype=torch.float64).to(cuda)
+    B = torch.randn((k, n), generator=g, dtype=torch.float64).to(cuda)
+    C0 = torch.randn((m, n), generator=g, dtype=torch.float64).to(cuda)
+    C = C0.t().contiguous().t()
+    qdwh.gemm(A.t().contiguous().t(), B.t().contiguous().t(), C, alpha=0.75, beta=0.25, trans_a=True,
+              out=out, diag_add=2.0 if out != "full" else 0.0)
+    ref = 0.75 * (A.T @ B) + 0.25 * C0
+    if out != "full":
+        ref = ref + 2.0 * torch.eye(m, dtype=torch.float64, device=cuda)
+        low = torch.tril(torch.ones(m, n, dtype=torch.bool, device=cuda))
+        if out == "lower_mirror":
+            ref = torch.where(low, ref, ref.T)
+        else:
+            ref = torch.where(low, ref, C0)
+    err = (C - ref).abs().max().item()
+    assert err <= 1e-13 * max(1.0, ref.abs().max().item()) * np.sqrt(k), err
+
+
 def test_qr_factor_matches_reference():
     g = golden("kernels")
     q, r = qdwh.qr_factor(g["a"])
