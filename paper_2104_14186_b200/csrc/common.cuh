@@ -154,6 +154,14 @@ QDWHG_DEV double fast_rcp(double x) {
   e = fma(-x, y, 1.0);
   return fma(y, e, y);
 }
+// 1/sqrt(x) to ~1 ulp: hardware estimate + two Newton steps (x > 0, finite)
+QDWHG_DEV double fast_rsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  r = r * fma(-h * r, r, 1.5);
+  return r * fma(-h * r, r, 1.5);
+}
 QDWHG_DEV double fast_sqrt(double x) {
   double r;
   asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(r) : "d"(x));

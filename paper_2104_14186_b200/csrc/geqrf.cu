@@ -425,20 +425,25 @@ __global__ void __launch_bounds__(64 * NRG, 1)
     double* UPn = snap + (par ^ 1) * 2 * RB;                               // next step's pairs
     const double x0 = tot[jj];
     const double sig2 = tot[kBW + jj];
-    const double nx2 = x0 * x0 + sig2;
+    const double nx2 = fma(x0, x0, sig2);
     const bool reflect = (jj < mp - 1) && nx2 > 0.0;
-    double beta = x0, v0 = 1.0, taup = 0.0, inv_v0 = 1.0;
+    // short dependent chain (FP64 latency is the column's critical path):
+    //   rn = 1/||x||, v0 = x0 - beta = x0 + sign(x0) ||x||, tau' = 1 + |x0| rn,
+    //   s_c = tau' (v^T a_c) / v0 = sign(x0) rn (a_c(j) + x_b^T a_c / v0)
+    double beta = x0, v0 = 1.0, taup = 0.0, inv_v0 = 1.0, srn = 0.0;
     if (reflect) {
-      const double normx = fast_sqrt(nx2);
-      beta = x0 >= 0.0 ? -normx : normx;
-      v0 = x0 - beta;
-      taup = (beta - x0) * fast_rcp(beta);
+      const double rn = fast_rsqrt(nx2);
+      const double normx = nx2 * rn;
+      v0 = x0 + copysign(normx, x0);
       inv_v0 = fast_rcp(v0);
+      beta = -copysign(normx, x0);
+      taup = fma(fabs(x0), rn, 1.0);
+      srn = copysign(rn, x0);
     }
     // w_c = tau' v^T a_c  (v = [1; x_below / v0]);  s_c = w_c / v0 scales u = v0 v
     double sc = 0.0, s1 = 0.0;
-    if (reflect && c > jj && c < b) sc = taup * (tot[c] + tot[kBW + c] * inv_v0) * inv_v0;
-    if (reflect && jj + 1 < b) s1 = taup * (tot[jj + 1] + tot[kBW + jj + 1] * inv_v0) * inv_v0;
+    if (reflect && c > jj && c < b) sc = srn * fma(tot[kBW + c], inv_v0, tot[c]);
+    if (reflect && jj + 1 < b) s1 = srn * fma(tot[kBW + jj + 1], inv_v0, tot[jj + 1]);
     if (tid == 0) {  // read after the last step's barriers
       colsc[jj] = reflect ? inv_v0 : 0.0;
       colsc[kBW + jj] = beta;
