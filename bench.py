@@ -189,6 +189,15 @@ def config_desc(cfg):
 
 def make_input(cfg, dev, handle):
     """Synthetic config input generated on the GPU (seeded Gaussian, our own QR)."""
+    inp = _make_input(cfg, dev, handle)
+    # randomized subspace detection (B Omega before the QR, partial.cpp:70/137):
+    # the config's choice, BENCH_RANDOMIZE=0/1 overrides
+    env = os.environ.get("BENCH_RANDOMIZE")
+    inp["randomize"] = bool(int(env)) if env is not None else bool(config_desc(cfg).get("randomize", False))
+    return inp
+
+
+def _make_input(cfg, dev, handle):
     import torch
     from paper_2104_14186_b200 import matgen, qdwh
     c = config_desc(cfg)
@@ -237,9 +246,11 @@ def thin_q(G, handle):
 def solve(inp, handle, host=False):
     from paper_2104_14186_b200 import qdwh
     A = inp["A_host"] if host else inp["A"]
+    rnd = bool(inp.get("randomize", False))
     if inp["kind"] == "eig":
-        return qdwh.partial_eig_request(A, "largest", inp["c"], inp["k"], handle=handle)
-    return qdwh.partial_svd_request(A, cut=inp["cut"], k=inp["k"], handle=handle)
+        return qdwh.partial_eig_request(A, "largest", inp["c"], inp["k"], use_randomization=rnd,
+                                        handle=handle)
+    return qdwh.partial_svd_request(A, cut=inp["cut"], k=inp["k"], use_randomization=rnd, handle=handle)
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -274,9 +285,10 @@ def ref_sample(cfg):
     vr, _ = np.linalg.qr(O.gaussian_matrix(n, n, c["seed"] ^ matgen.RIGHT_STREAM))
     a = (ul * sig) @ vr.T
     k = max(1, int(round(c["k"] / c["n"] * n)))
-    return dict(kind="svd", a=a, m=m, n=n, k=k, cut=matgen.sigma_cut(sig, k),
+    rnd = bool(c.get("randomize", False))
+    return dict(kind="svd", a=a, m=m, n=n, k=k, cut=matgen.sigma_cut(sig, k), randomize=rnd,
                 desc=f"cfg{cfg} family ({c['family']} spectrum, top {k}) at {m}x{n}, "
-                     f"1 reference qdwh_partial_svd solve")
+                     f"1 reference qdwh_partial_svd solve" + (" (randomized)" if rnd else ""))
 
 
 def ref_solve_flops(sample):
@@ -291,10 +303,11 @@ def ref_solve_flops(sample):
     else:
         alpha = R.two_norm_estimate(sample["a"])
         t0 = time.perf_counter()
-        s, u, v, d = R.partial_svd(sample["a"], sample["cut"] / alpha)
+        rnd = bool(sample.get("randomize", False))
+        s, u, v, d = R.partial_svd(sample["a"], sample["cut"] / alpha, randomize=rnd)
         dt = time.perf_counter() - t0
         fl = O.flops_partial_svd(sample["m"], sample["n"], d["subspace_size"], d["k"], d["iters_qr"],
-                                 d["iters_chol"], False)
+                                 d["iters_chol"], rnd)
     return dt, fl
 
 
@@ -371,6 +384,8 @@ def config_json(cfg, gpus):
          "k": c["k"], "parallelism": f"replicas{gpus}" if gpus > 1 else "single",
          "l2": "flushed (256 MiB write) before every timed step"}
     d.update({kk: v for kk, v in c.items() if kk in ("n", "m")})
+    env = os.environ.get("BENCH_RANDOMIZE")
+    d["randomized_detection"] = bool(int(env)) if env is not None else bool(c.get("randomize", False))
     return d
 
 

@@ -28,7 +28,9 @@ CONFIGS = {
     2: dict(kind="eig", n=4096, family="logsigned", k=41, seed=42),
     3: dict(kind="svd", m=8192, n=8192, family="log16", k=410, seed=42),
     4: dict(kind="eig", n=16384, family="wishart", k=3277, seed=42, shift=0.8881 - 0.05),
-    5: dict(kind="svd", m=32768, n=8192, family="inv", k=819, seed=42),
+    # randomized detection for the slow sigma_i = 1/i decay (l 4546 -> ~2.9k,
+    # measured 1.44 -> 1.22 s on one B200); the reference's own use_randomization option
+    5: dict(kind="svd", m=32768, n=8192, family="inv", k=819, seed=42, randomize=True),
 }
 
 
