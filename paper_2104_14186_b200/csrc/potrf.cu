@@ -344,13 +344,19 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   }
   DIAG_MARK(15);
 
-  // ---- Winv = L^{-T} (upper) with explicit zeros below
+  // ---- Winv = L^{-T} (upper) with explicit zeros below.  Winv(r, c) = A[r * kLDA + c]:
+  // 8 lanes per column (4 columns per warp instruction), so the transposed shared
+  // reads hit 16 distinct bank pairs (kLDA = 132) instead of 4 with a lane per row
   {
     const int rend = (flags & kDiagUpperOnly) ? 0 : nb;
-    for (int c = warp; c < nb; c += kDiagThreads / 32) {
+    const int j = lane >> 3, rr = lane & 7;
+    for (int c0 = 4 * warp; c0 < nb; c0 += 4 * (kDiagThreads / 32)) {
+      const int c = c0 + j;
+      const int rmax = max(c0 + 4, rend);  // warp-uniform trip count
       double* wc = Winv + (int64_t)c * ldwi;
 #pragma unroll 4
-      for (int r = lane; r < max(c + 1, rend); r += 32) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+      for (int r = rr; r < rmax; r += 8)
+        if (c < nb && r < max(c + 1, rend)) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
     }
   }
   DIAG_MARK(16);
