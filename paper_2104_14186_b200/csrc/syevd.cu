@@ -626,7 +626,7 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   const int nb = kTrdNB;
   const int npan = (n - 1 + nb - 1) / nb;  // columns 0 .. n-2 carry reflectors
   DMat Vfull = ctx.arena->alloc(n, std::max(npan * nb, 1));
-  DMat Vp = ctx.arena->alloc(n, nb), Wp = ctx.arena->alloc(n, nb);
+  DMat Wp = ctx.arena->alloc(n, nb);
   double* dd = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
   double* ee = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 8)));
   double* tau = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (npan * nb + 8)));
@@ -637,10 +637,9 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   unsigned* bar = static_cast<unsigned*>(ctx.arena->alloc_bytes(256));
   QDWHG_CUDA(cudaMemsetAsync(tau, 0, sizeof(double) * (npan * nb + 8), ctx.stream));
   QDWHG_CUDA(cudaMemsetAsync(ee, 0, sizeof(double) * (n + 8), ctx.stream));
-  if (!small) {
+  if (!small)  // (Vfull needs no fill: every panel writes its V columns in full)
     QDWHG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (n + 2 * nb + 8), ctx.stream));  // SYMV atomics
-    fill(ctx, Vfull, 0.0, 0.0);
-  }
+  if (Wp.ld != Vfull.ld) throw CudaError("syev_tridiag: panel V/W leading dimensions differ");
   static bool trd_attr = false;
   if (!trd_attr) {
     QDWHG_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -668,16 +667,17 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
     const int b = std::min(nb, n - 1 - j0);
     QDWHG_CUDA(cudaMemsetAsync(red, 0, sizeof(double) * 64, ctx.stream));
     QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
-    TrdArgs args{A.ptr(), A.ld, Vp.ptr(), Wp.ptr(), Vp.ld, dd, ee, tau, y, ypart, red, bar, n, j0, b};
+    // the panel's reflectors go straight into their columns of Vfull
+    const DMat Vpan = Vfull.sub(0, j0, n, nb);
+    TrdArgs args{A.ptr(), A.ld, Vpan.ptr(), Wp.ptr(), Vfull.ld, dd, ee, tau, y, ypart, red, bar, n, j0, b};
     void* kargs[] = {&args};
     QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)sytrd_panel_kernel, dim3(grid), dim3(kTrdThreads),
                                            kargs, kTrdDynSmem, ctx.stream));
     ctx.count();
-    copy(ctx, Vp.sub(0, 0, n, b), Vfull.sub(0, j0, n, b));
     const int r0 = j0 + b;
     const int rest = n - r0;
     if (rest > 0) {
-      const DMat Vr = Vp.sub(r0, 0, rest, b), Wr = Wp.sub(r0, 0, rest, b);
+      const DMat Vr = Vpan.sub(r0, 0, rest, b), Wr = Wp.sub(r0, 0, rest, b);
       const DMat At = A.sub(r0, r0, rest, rest);
       GemmExtra lo;  // the panel kernel reads only the lower triangle of A
       lo.out = OutMode::Lower;
