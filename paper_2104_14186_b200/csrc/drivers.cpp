@@ -546,6 +546,111 @@ static void check_finite(Ctx& ctx, const DMat& A, const char* who, MatStats* out
   if (out) *out = st;
 }
 
+// Subspace extraction for a SMALL subspace (partial.cpp:71-79 semantics, Cholesky
+// QR instead of Householder): the R factor of the unpivoted QR of B is the
+// Cholesky factor of B^T B, so
+//   ind = first i with |W_ii| < tol,  W = chol(B^T B + delta I)
+// (delta = 4 n u ||B||^2 only keeps the rank-deficient tail positive definite; it
+// moves the |R_ii| >= tol pivots by ~delta / R_ii), and Q2 is an orthonormal basis
+// of span(B1)^perp, B1 = B(:, 0:ind-1) — the subspace spanned by Q(:, ind-1:n)
+// of the Householder QR — from a projected Gaussian block
+//   Y = (I - B1 G11^{-1} B1^T)^2 Omega,  G11^{-1} = W11^{-1} W11^{-T}
+// (two passes: the delta-shifted projector leaves ~delta/sigma_min(B1)^2 per pass),
+// Q2 = the dominant l-dimensional range of Y (eigenvectors of Y^T Y), CholQR2.
+// Everything is GEMM-shaped plus the recursive Cholesky-and-inverse: ~1.7 n^3
+// instead of the latency-bound panel chain of GEQRF.  Used when l is small
+// (trace(I - B) <= n/16 and l + 16 <= n/8); returns false to fall back.
+static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DMat& Q2out,
+                            const DMat& Q2buf) {
+  static const bool off = getenv("QDWHG_SUBSPACE_HOUSEHOLDER") != nullptr;
+  const int64_t n = B.rows;
+  if (off || B.cols != n || n < 1024) return false;
+  if ((double)n - device_trace(ctx, B) > (double)n / 16.0) return false;  // l estimate
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat G = ctx.arena->alloc(n, n);
+  DMat Winv = ctx.arena->alloc(n, n);
+  GemmExtra syrk;
+  syrk.out = OutMode::Lower;
+  // ||B||_2 <= 1 (B = (X + I)/2, |eig(X)| <= 1): delta a few times the rounding
+  // noise of the Gram's entries keeps the deficient tail positive definite
+  syrk.diag_add = 32.0 * std::sqrt((double)n) * kEps;
+  gemm(ctx, Op::T, Op::N, 1.0, B, B, 0.0, G, syrk);
+  try {
+    potrf_upper_and_inverse(ctx, G, Winv, /*want_w=*/true, /*stable=*/false);  // G <- W
+  } catch (const NotPositiveDefinite&) {
+    ctx.arena->release_to(mark);
+    return false;
+  }
+  std::vector<double> d;
+  diag_to_host(ctx, G, d);
+  ind = 0;  // detect_deficiency_index, partial.cpp:32-38
+  for (size_t i = 0; i < d.size(); ++i)
+    if (!(std::abs(d[i]) >= tol)) {
+      ind = i + 1;
+      break;
+    }
+  if (ind == 0) {
+    ctx.arena->release_to(mark);
+    return true;
+  }
+  const int64_t ell = n - (int64_t)ind + 1, k1 = (int64_t)ind - 1;
+  const int64_t r = ell + 16;
+  if (r > Q2buf.cols || k1 < 1) {
+    ctx.arena->release_to(mark);
+    return false;
+  }
+  DMat Y = ctx.arena->alloc(n, r);
+  gaussian_fill(ctx, Y, 0x7375627370ull);  // fixed stream ("subsp")
+  DMat T1 = ctx.arena->alloc(k1, r), T2 = ctx.arena->alloc(k1, r);
+  const DMat B1 = B.col_block(0, k1), W11i = Winv.sub(0, 0, k1, k1);
+  // Richardson passes of the least-squares projection: each leaves ~delta /
+  // sigma_min(B1)^2 (+ u kappa(B1)^2) of what is left in span(B1); three passes,
+  // and the caller checks the Ritz residuals of the result (falls back otherwise)
+  for (int pass = 0; pass < 3; ++pass) {
+    gemm(ctx, Op::T, Op::N, 1.0, B1, Y, 0.0, T1);           // B1^T Y
+    GemmExtra lo;
+    lo.krange = KRange::ALower;                              // W11^{-T} lower
+    gemm(ctx, Op::T, Op::N, 1.0, W11i, T1, 0.0, T2, lo);
+    GemmExtra up;
+    up.krange = KRange::AUpper;                              // W11^{-1} upper
+    gemm(ctx, Op::N, Op::N, 1.0, W11i, T2, 0.0, T1, up);
+    gemm(ctx, Op::N, Op::N, -1.0, B1, T1, 1.0, Y);           // Y -= B1 G11^{-1} B1^T Y
+  }
+  // dominant l-dimensional range of Y: eigenvectors of the r x r Gram
+  DMat E = ctx.arena->alloc(r, r), U = ctx.arena->alloc(r, r);
+  GemmExtra gm;
+  gm.out = OutMode::LowerMirror;
+  gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, E, gm);
+  std::vector<double> vals;
+  syev(ctx, E, vals, U);  // ascending
+  // the l kept directions must stand far above the p projected-out ones
+  if (!(vals[r - ell] > 1e8 * std::max(std::abs(vals[r - ell - 1]), 1e-300) && vals[r - ell] > 0.0)) {
+    ctx.arena->release_to(mark);
+    return false;
+  }
+  Q2out = Q2buf.col_block(0, ell);
+  gemm(ctx, Op::N, Op::N, 1.0, Y, U.col_block(r - ell, ell), 0.0, Q2out);
+  // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice
+  DMat F = ctx.arena->alloc(ell, ell), Fi = ctx.arena->alloc(ell, ell), Qt = ctx.arena->alloc(n, ell);
+  for (int pass = 0; pass < 2; ++pass) {
+    GemmExtra fl;
+    fl.out = OutMode::Lower;
+    gemm(ctx, Op::T, Op::N, 1.0, Q2out, Q2out, 0.0, F, fl);
+    try {
+      potrf_upper_and_inverse(ctx, F, Fi, false, /*stable=*/true);
+    } catch (const NotPositiveDefinite&) {
+      ctx.arena->release_to(mark);
+      return false;
+    }
+    copy(ctx, Q2out, Qt);
+    GemmExtra bu;
+    bu.krange = KRange::BUpper;
+    gemm(ctx, Op::N, Op::N, 1.0, Qt, Fi, 0.0, Q2out, bu);
+  }
+  ctx.arena->release_to(mark);
+  return true;
+}
+
 EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomize, double tol,
                    uint64_t seed, StageClock* clk) {
   // partial.cpp:40-99
@@ -582,56 +687,97 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     B = ctx.arena->alloc(n, n);
     gemm(ctx, Op::N, Op::N, 1.0, X, Om, 0.0, B);
   }
-  QrWork qw;
-  geqrf(ctx, B, qw);
-  std::vector<double> d;
-  diag_to_host(ctx, B, d);
-  if (clk) clk->mark(2);
-  size_t ind = 0;  // detect_deficiency_index, partial.cpp:32-38
-  for (size_t i = 0; i < d.size(); ++i)
-    if (std::abs(d[i]) < tol) {
-      ind = i + 1;
-      break;
-    }
+  // small subspace: Cholesky-QR extraction first (same ind, same span), verified by
+  // the Ritz residuals of the result; otherwise (or if that check fails) the
+  // reference's Householder QR + trailing-column Q formation
+  const Arena::Mark sub_mark = ctx.arena->mark();
   const double nd = (double)n;
-  out.flops = it.iters_chol * (10.0 / 3.0) * nd * nd * nd + 4.0 / 3.0 * nd * nd * nd +
-              (randomize ? 2 * nd * nd * nd : 0.0);
-  if (ind == 0) return out;
-  out.rank_index = ind;
-  const int64_t ell = n - (int64_t)ind + 1;
-  out.subspace_size = ell;
-  out.no_savings = ell > n / 2;
-  DMat Q2 = ctx.arena->alloc(n, ell);
-  orgqr_cols(ctx, qw, n, n, (int64_t)ind - 1, Q2);
-  if (clk) clk->mark(3);
-  DMat AQ = ctx.arena->alloc(n, ell);
-  gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ);
-  DMat S = ctx.arena->alloc(ell, ell);
-  GemmExtra rr;  // S = Q2^T (A Q2) is symmetric: lower tiles, mirrored (exactly symmetric)
-  rr.out = OutMode::LowerMirror;
-  gemm(ctx, Op::T, Op::N, 1.0, Q2, AQ, 0.0, S, rr);
-  if (clk) clk->mark(4);
-  std::vector<double> vals;
-  DMat W = ctx.arena->alloc(ell, ell);
-  int64_t sel0 = 0;
-  syev_range(ctx, S, vals, W, -INFINITY, 0.0, &sel0);  // vectors for the negative Ritz values only
-  if (clk) clk->mark(5);
-  double max_abs_ritz = 0.0;
-  for (double v : vals) max_abs_ritz = std::max(max_abs_ritz, std::abs(v));
-  const double floor = -nd * kEps * max_abs_ritz;
-  int64_t k = 0;
-  while (k < ell && vals[k] < 0.0) ++k;
-  const double l = (double)ell;
-  out.flops += 2 * nd * nd * l - 2 * l * l * l / 3 + 2 * nd * nd * l + 2 * nd * l * l + 9 * l * l * l;
-  if (k == 0) return out;
-  out.lambda.resize(k);
-  for (int64_t i = 0; i < k; ++i) {
-    out.lambda[i] = scale * vals[i];
-    if (vals[i] >= floor) ++out.borderline;
+  const double as_fro = std::sqrt(st.fro2) / scale;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    ctx.arena->release_to(sub_mark);
+    out.rank_index = 0;
+    out.subspace_size = 0;
+    out.no_savings = false;
+    out.borderline = 0;
+    out.lambda.clear();
+    out.V = DMat{};
+    size_t ind = 0;
+    DMat Q2;
+    const DMat Q2buf =
+        (randomize || attempt > 0) ? DMat{} : ctx.arena->alloc(n, std::max<int64_t>(1, n / 8));
+    const bool chq = !randomize && attempt == 0 && subspace_cholqr(ctx, B, tol, ind, Q2, Q2buf);
+    QrWork qw;
+    if (!chq) {
+      geqrf(ctx, B, qw);
+      std::vector<double> d;
+      diag_to_host(ctx, B, d);
+      ind = 0;  // detect_deficiency_index, partial.cpp:32-38
+      for (size_t i = 0; i < d.size(); ++i)
+        if (std::abs(d[i]) < tol) {
+          ind = i + 1;
+          break;
+        }
+    }
+    if (clk) clk->mark(2);
+    out.flops = it.iters_chol * (10.0 / 3.0) * nd * nd * nd + 4.0 / 3.0 * nd * nd * nd +
+                (randomize ? 2 * nd * nd * nd : 0.0);
+    if (ind == 0) return out;
+    out.rank_index = ind;
+    const int64_t ell = n - (int64_t)ind + 1;
+    out.subspace_size = ell;
+    out.no_savings = ell > n / 2;
+    if (!chq) {
+      Q2 = ctx.arena->alloc(n, ell);
+      orgqr_cols(ctx, qw, n, n, (int64_t)ind - 1, Q2);
+    }
+    if (clk) clk->mark(3);
+    DMat AQ = ctx.arena->alloc(n, ell);
+    gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ);
+    DMat S = ctx.arena->alloc(ell, ell);
+    GemmExtra rr;  // S = Q2^T (A Q2) is symmetric: lower tiles, mirrored (exactly symmetric)
+    rr.out = OutMode::LowerMirror;
+    gemm(ctx, Op::T, Op::N, 1.0, Q2, AQ, 0.0, S, rr);
+    if (clk) clk->mark(4);
+    std::vector<double> vals;
+    DMat W = ctx.arena->alloc(ell, ell);
+    int64_t sel0 = 0;
+    syev_range(ctx, S, vals, W, -INFINITY, 0.0, &sel0);  // vectors for the negative Ritz values only
+    if (clk) clk->mark(5);
+    double max_abs_ritz = 0.0;
+    for (double v : vals) max_abs_ritz = std::max(max_abs_ritz, std::abs(v));
+    const double floor = -nd * kEps * max_abs_ritz;
+    int64_t k = 0;
+    while (k < ell && vals[k] < 0.0) ++k;
+    const double l = (double)ell;
+    out.flops += 2 * nd * nd * l - 2 * l * l * l / 3 + 2 * nd * nd * l + 2 * nd * l * l + 9 * l * l * l;
+    if (k == 0) {
+      if (chq) continue;  // confirm an empty result on the reference path
+      return out;
+    }
+    out.lambda.resize(k);
+    for (int64_t i = 0; i < k; ++i) {
+      out.lambda[i] = scale * vals[i];
+      if (vals[i] >= floor) ++out.borderline;
+    }
+    out.V = ctx.arena->alloc(n, k);
+    gemm(ctx, Op::N, Op::N, 1.0, Q2, W.sub(0, 0, ell, k), 0.0, out.V);
+    out.flops += 2 * nd * l * (double)k;
+    if (chq) {
+      // Ritz residual ||As V - V Lambda||_F against 1e-13 sqrt(n) ||As||_F (10x inside
+      // the north-star gate): a subspace that lost accuracy is redone by Householder
+      const Arena::Mark rm = ctx.arena->mark();
+      DMat R = ctx.arena->alloc(n, k), D = ctx.arena->alloc(k, k);
+      std::vector<double> hd((size_t)k * k, 0.0);
+      for (int64_t i = 0; i < k; ++i) hd[i + (size_t)i * k] = vals[i];
+      copy_from_host(ctx, hd.data(), k, D);
+      gemm(ctx, Op::N, Op::N, 1.0, As, out.V, 0.0, R);
+      gemm(ctx, Op::N, Op::N, -1.0, out.V, D, 1.0, R);
+      const double res = std::sqrt(mat_stats(ctx, R, false).fro2);
+      ctx.arena->release_to(rm);
+      if (!(res <= 1e-13 * std::sqrt(nd) * as_fro)) continue;
+    }
+    break;
   }
-  out.V = ctx.arena->alloc(n, k);
-  gemm(ctx, Op::N, Op::N, 1.0, Q2, W.sub(0, 0, ell, k), 0.0, out.V);
-  out.flops += 2 * nd * l * (double)k;
   if (clk) clk->mark(6);
   return out;
 }

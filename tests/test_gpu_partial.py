@@ -210,3 +210,51 @@ def test_soak_multistream_paths(cuda, seed):
     rs = qdwh.partial_svd_request(b, cut=float(np.sqrt(sig[kk - 1] * sig[kk])))
     assert rs.count() == kk
     np.testing.assert_allclose(rs.sigma1, sig[:kk], rtol=1e-10)
+
+
+@pytest.mark.parametrize("n,k,family", [(2048, 20, "logsigned"), (4096, 41, "logsigned"),
+                                        (1536, 60, "uniform")])
+def test_cholqr_subspace_matches_householder(n, k, family):
+    """The small-subspace extraction (Cholesky QR of B, projected Gaussian block)
+    against the reference's Householder QR path (QDWHG_SUBSPACE_HOUSEHOLDER, in a
+    subprocess so the switch is read fresh): same deficiency index and subspace
+    size, eigenvalues to 1e-12, north-star gates on both."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, sys\n"
+        "import numpy as np\n"
+        "from oracle import qdwh_oracle as O\n"
+        "from paper_2104_14186_b200 import matgen, qdwh\n"
+        f"n, k, fam = {n}, {k}, '{family}'\n"
+        "lam = matgen.config_eigenvalues(fam, n, 7)\n"
+        "q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 7))\n"
+        "a = (q * lam) @ q.T\n"
+        "a = 0.5 * (a + a.T)\n"
+        "c = matgen.largest_k_shift(lam, k)\n"
+        "r = qdwh.partial_eig_request(a, 'largest', c, k)\n"
+        "v = np.asarray(r.v)\n"
+        "res = np.linalg.norm(a @ v - v * r.lambda_minus) / np.linalg.norm(a)\n"
+        "orth = np.linalg.norm(np.eye(r.count()) - v.T @ v)\n"
+        "print(json.dumps(dict(vals=list(r.lambda_minus), ell=r.subspace_size, ind=r.rank_index,\n"
+        "                      res=res, orth=orth, want=list(np.sort(lam)[::-1][:k]))))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for hh in (False, True):
+        env = dict(os.environ, PYTHONPATH=root)
+        env.pop("QDWHG_SUBSPACE_HOUSEHOLDER", None)
+        if hh:
+            env["QDWHG_SUBSPACE_HOUSEHOLDER"] = "1"
+        p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        import json
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    chq, hh = outs
+    assert len(chq["vals"]) == len(hh["vals"]) == k
+    assert chq["ind"] == hh["ind"] and chq["ell"] == hh["ell"]
+    np.testing.assert_allclose(chq["vals"], hh["vals"], rtol=1e-12)
+    np.testing.assert_allclose(chq["vals"], chq["want"], rtol=1e-10, atol=1e-14)
+    for o in outs:
+        assert o["res"] <= 1e-12 * np.sqrt(n) and o["orth"] <= 1e-12 * np.sqrt(n)
