@@ -576,16 +576,17 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   syrk.diag_add = 32.0 * std::sqrt((double)n) * kEps;
   gemm(ctx, Op::T, Op::N, 1.0, B, B, 0.0, G, syrk);
   try {
-    potrf_upper_and_inverse(ctx, G, Winv, /*want_w=*/true, /*stable=*/false);  // G <- W
+    potrf_upper_and_inverse(ctx, G, Winv, /*want_w=*/false, /*stable=*/false);
   } catch (const NotPositiveDefinite&) {
     ctx.arena->release_to(mark);
     return false;
   }
+  // |R_ii| = W_ii = 1 / (W^{-1})_ii (triangular inverse: no need to write W out)
   std::vector<double> d;
-  diag_to_host(ctx, G, d);
+  diag_to_host(ctx, Winv, d);
   ind = 0;  // detect_deficiency_index, partial.cpp:32-38
   for (size_t i = 0; i < d.size(); ++i)
-    if (!(std::abs(d[i]) >= tol)) {
+    if (!(1.0 / std::abs(d[i]) >= tol)) {
       ind = i + 1;
       break;
     }
@@ -621,15 +622,19 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   GemmExtra gm;
   gm.out = OutMode::LowerMirror;
   gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, E, gm);
+  // the l kept eigenvalues are O(r) (a projected Gaussian Wishart block), the p
+  // projected-out ones at rounding level: vectors only above a threshold in the
+  // gap (the rounding-level cluster would defeat inverse iteration's Lowdin check)
   std::vector<double> vals;
-  syev(ctx, E, vals, U);  // ascending
-  // the l kept directions must stand far above the p projected-out ones
-  if (!(vals[r - ell] > 1e8 * std::max(std::abs(vals[r - ell - 1]), 1e-300) && vals[r - ell] > 0.0)) {
+  const double tr = device_trace(ctx, E);
+  int64_t sel0 = 0;
+  const int64_t cnt = syev_range(ctx, E, vals, U, 1e-8 * tr / (double)ell, INFINITY, &sel0);
+  if (cnt != ell || !(vals[r - ell] > 1e8 * std::max(std::abs(vals[r - ell - 1]), 1e-300))) {
     ctx.arena->release_to(mark);
     return false;
   }
   Q2out = Q2buf.col_block(0, ell);
-  gemm(ctx, Op::N, Op::N, 1.0, Y, U.col_block(r - ell, ell), 0.0, Q2out);
+  gemm(ctx, Op::N, Op::N, 1.0, Y, U.col_block(0, ell), 0.0, Q2out);
   // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice
   DMat F = ctx.arena->alloc(ell, ell), Fi = ctx.arena->alloc(ell, ell), Qt = ctx.arena->alloc(n, ell);
   for (int pass = 0; pass < 2; ++pass) {
