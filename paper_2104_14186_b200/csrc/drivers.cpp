@@ -607,7 +607,8 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   // Richardson passes of the least-squares projection: each leaves ~delta /
   // sigma_min(B1)^2 (+ u kappa(B1)^2) of what is left in span(B1); three passes,
   // and the caller checks the Ritz residuals of the result (falls back otherwise)
-  for (int pass = 0; pass < 3; ++pass) {
+  static const int npass = getenv("QDWHG_SUBSPACE_PASSES") ? std::max(1, atoi(getenv("QDWHG_SUBSPACE_PASSES"))) : 3;
+  for (int pass = 0; pass < npass; ++pass) {
     gemm(ctx, Op::T, Op::N, 1.0, B1, Y, 0.0, T1);           // B1^T Y
     GemmExtra lo;
     lo.krange = KRange::ALower;                              // W11^{-T} lower
