@@ -637,6 +637,9 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
       const double waves = std::ceil(units / ((double)ctx.num_sms * per_sm));
       const double t_unit = (double)bm * bm * (keff / sp) / (sm_rate * eff / per_sm) + 2e-6;
       double t = waves * t_unit;
+      // triangular K ranges: the heaviest tiles carry the full K, and with few
+      // waves they set the time (a one-wave TRMM runs as long as its K = n tile)
+      if (tri) t = std::max(t, (double)bm * bm * ((double)K / sp) / (sm_rate * eff / per_sm) + 2e-6);
       if (sp > 1) t += (double)(sp + 1) * M * N * 8.0 / 4e12 + 3e-6;
       if (t < best * 0.97) {  // prefer the earlier (larger-tile, fewer-split) candidate on ties
         best = t;
