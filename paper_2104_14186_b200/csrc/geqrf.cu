@@ -1041,7 +1041,9 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
         // cap only for mid-size matrices (measured: helps at 4096^2, hurts at
         // 8192^2, 16384^2 and 32768 x 4546, where the side work dominates and
         // the grid panels need most SMs anyway)
-        const int64_t cap_tiles = (m <= 6144 && n <= 6144) ? 64 : (int64_t)1 << 40;
+        static const int64_t cap_env = getenv("QDWHG_QR_SIDE_CAP") ? atoll(getenv("QDWHG_QR_SIDE_CAP")) : 0;
+        const int64_t cap_tiles =
+            cap_env > 0 ? cap_env : ((m <= 6144 && n <= 6144) ? 64 : (int64_t)1 << 40);
         const int64_t cw1 = std::max<int64_t>(128, (cap_tiles / ((bo + 127) / 128)) * 128);
         const int64_t cw2 = std::max<int64_t>(128, (cap_tiles / ((mo + 127) / 128)) * 128);
         const DMat C = A.sub(jo, jo + bo + bn, mo, nr);
