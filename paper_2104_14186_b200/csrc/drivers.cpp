@@ -595,7 +595,9 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     return true;
   }
   const int64_t ell = n - (int64_t)ind + 1, k1 = (int64_t)ind - 1;
-  const int64_t r = ell + 16;
+  // >= 8 oversampling columns, rounded up to a multiple of 64 so the skinny
+  // projection GEMMs fill whole 64-wide tiles
+  const int64_t r = ((ell + 8 + 63) / 64) * 64;
   if (r > Q2buf.cols || k1 < 1) {
     ctx.arena->release_to(mark);
     return false;

@@ -29,7 +29,16 @@ if what == "svd":
     Ysvd = ((q1[:, :n] * sig[None, :]) @ q2.T).t().contiguous().t()
 
 
+inp = None
+if what == "solve":  # one cfg2 solve (bench input)
+    import bench
+    inp = bench.make_input(2, dev, h)
+
+
 def call():
+    if what == "solve":
+        import bench
+        return bench.solve(inp, h)
     if what == "svd":
         return qdwh.svd_dense(Ysvd, handle=h)
     if what == "chol":
