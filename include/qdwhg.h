@@ -233,6 +233,18 @@ qdwhg_status qdwhg_gemm_ex(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, in
  * Host or device pointers. */
 qdwhg_status qdwhg_cholesky_inverse(qdwhg_handle* h, int64_t n, double* Z, int64_t ldz,
                                     double* Winv, int64_t ldwi);
+/* W^{-1} only (upper, explicit zeros below) of Z = W^T W by the recursive
+ * Cholesky-and-inverse that multiplies by explicit inverses of half blocks (errors
+ * ~ u*kappa(Z)): for well-conditioned Z such as the QDWH Cholesky step's
+ * I + c X^T X (kappa <= 1 + c; polar.cpp:85-93).  Z is not modified. */
+qdwhg_status qdwhg_cholesky_inverse_fast(qdwhg_handle* h, int64_t n, const double* Z, int64_t ldz,
+                                         double* Winv, int64_t ldwi);
+/* Subspace extraction of Alg. 1/2 (partial.cpp:71-79 / 138-146): unpivoted Householder
+ * QR of the n x n B, *ind = first 1-based i with |R_ii| < tol (0: none), *ell = n - ind + 1,
+ * and Q2 = Q(:, ind-1:n) (n x ell) formed from the trailing reflectors only.  B is read
+ * (host or device).  CAPACITY when ell > ell_cap. */
+qdwhg_status qdwhg_subspace_q2(qdwhg_handle* h, int64_t n, double* B, int64_t ldb, double tol,
+                               int64_t* ind, int64_t* ell, double* Q2, int64_t ldq, int64_t ell_cap);
 /* Counter-based N(0,1) matrix on the device (kernels.cpp:441-447 scheme, device libm). */
 qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64_t seed, double* A,
                                    int64_t lda);

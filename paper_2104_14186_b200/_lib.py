@@ -99,6 +99,8 @@ SIGNATURES = {
     "qdwhg_gemm_ex": [_P, _I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _I32,
                       _I32, _D],
     "qdwhg_cholesky_inverse": [_P, _I64, _P, _I64, _P, _I64],
+    "qdwhg_cholesky_inverse_fast": [_P, _I64, _P, _I64, _P, _I64],
+    "qdwhg_subspace_q2": [_P, _I64, _P, _I64, _D, _P, _P, _P, _I64, _I64],
     "qdwhg_gaussian_matrix": [_P, _I64, _I64, _U64, _P, _I64],
     "qdwhg_halley_weights": [_D, _P],
     "qdwhg_iterations_to_converge": [_D, _D, _I64, _P],

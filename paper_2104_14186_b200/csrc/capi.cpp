@@ -765,6 +765,50 @@ qdwhg_status qdwhg_cholesky_inverse(qdwhg_handle* h, int64_t n, double* Z, int64
   });
 }
 
+qdwhg_status qdwhg_cholesky_inverse_fast(qdwhg_handle* h, int64_t n, const double* Z, int64_t ldz,
+                                         double* Winv, int64_t ldwi) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !Z || !Winv) throw InvalidArgument("cholesky_inverse_fast: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Zd = stage_in(ctx, Z, n, n, ldz, nullptr);  // workspace copy: Z is not modified
+    DMat Wi = ctx.arena->alloc(n, n);
+    potrf_upper_and_inverse(ctx, Zd, Wi, /*want_w=*/false, /*stable=*/false);
+    stage_out(ctx, Wi, Winv, ldwi);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_subspace_q2(qdwhg_handle* h, int64_t n, double* B, int64_t ldb, double tol,
+                               int64_t* ind, int64_t* ell, double* Q2, int64_t ldq, int64_t ell_cap) {
+  if (!h || !ind || !ell) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !B) throw InvalidArgument("subspace_q2: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Bd = stage_in(ctx, B, n, n, ldb, nullptr);
+    // partial.cpp:71-79: Householder QR of B, ind = first |R_ii| < tol, Q2 = Q(:, ind-1:n)
+    QrWork qw;
+    geqrf(ctx, Bd, qw);
+    std::vector<double> d;
+    diag_to_host(ctx, Bd, d);
+    size_t i0 = 0;
+    for (size_t i = 0; i < d.size(); ++i)
+      if (std::abs(d[i]) < tol) {
+        i0 = i + 1;
+        break;
+      }
+    *ind = (int64_t)i0;
+    *ell = i0 ? n - (int64_t)i0 + 1 : 0;
+    if (i0 == 0) return;
+    if (*ell > ell_cap) throw CapacityError("subspace_q2: subspace larger than ell_cap");
+    if (!Q2) throw InvalidArgument("subspace_q2: no output buffer");
+    DMat Qd = ctx.arena->alloc(n, *ell);
+    orgqr_cols(ctx, qw, n, n, (int64_t)i0 - 1, Qd);
+    stage_out(ctx, Qd, Q2, ldq);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
 qdwhg_status qdwhg_gemm_ex(qdwhg_handle* h, int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
                            int64_t k, double alpha, const double* A, int64_t lda, const double* B,
                            int64_t ldb, double beta, double* C, int64_t ldc, int32_t krange,

@@ -114,13 +114,17 @@ def halley(ell):
     return qdwh.halley_weights(ell)
 
 
-def _chol_step_rows(be, comm, X_r, w):
-    """One Cholesky-based QDWH step on row-distributed X (polar.cpp:82-128)."""
+def _chol_step_rows(be, comm, X_r, w, symmetric=False):
+    """One Cholesky-based QDWH step on row-distributed X (polar.cpp:82-128).
+    symmetric (EIG path): X Z^{-1} with the replicated Z^{-1} = W^{-1} W^{-T} (one
+    LAUUM + one local GEMM: 4/3 n^3 instead of the two TRMMs' 5/3 n^3)."""
     G = be.gram(X_r)                       # X_r^T X_r
     comm.allreduce(G)                      # sum over ranks
     Z = be.shift_scale(G, w.c, 1.0)        # I + c * sym(G)
     Winv = be.chol_inv(Z)                  # replicated, throws NotPositiveDefinite
     bc = w.b / w.c
+    if symmetric:
+        return be.zinv_update(X_r, Winv, bc, w.a - bc)
     return be.trmm_update(X_r, Winv, bc, w.a - bc)
 
 
@@ -142,7 +146,7 @@ def dist_partial_eig(be, comm, A_r, n: int, s: float = 0.2, iters: int = 3, tol:
     res.ell_trace = [ell]
     for _ in range(iters):
         w = halley(ell)
-        X_r = _chol_step_rows(be, comm, X_r, w)
+        X_r = _chol_step_rows(be, comm, X_r, w, symmetric=True)
         X_full = comm.allgather_rows(X_r, n)             # symmetrize (polar.cpp:210)
         X_r = be.sym_rows(X_full, r0, r1)
         res.iters_chol += 1
@@ -362,7 +366,19 @@ class GpuBackend:
         return self._cm(Z)
 
     def chol_inv(self, Z):
-        return self.q.cholesky_inverse(self._cm(Z), handle=self.h)
+        # kappa(Z) <= 1 + c in the QDWH step: the recursive Cholesky-and-inverse
+        return self.q.cholesky_inverse_fast(self._cm(Z), handle=self.h)
+
+    def zinv_update(self, X, Winv, bc, coef):
+        """(b/c) X + (a - b/c) X Z^{-1}, Z^{-1} = W^{-1} W^{-T} (LAUUM: lower tiles,
+        K from the tile row, mirrored)."""
+        n = Winv.shape[0]
+        Winv = self._cm(Winv)
+        WiT = self._cm(Winv.T)
+        Zi = self.empty(n, n, like=X)
+        self.q.gemm(Winv, WiT, Zi, krange="a_upper", out="lower_mirror", handle=self.h)
+        Xo = self._cm(X.clone())
+        return self.q.gemm(self._cm(X), Zi, Xo, alpha=coef, beta=bc, handle=self.h)
 
     def trmm_update(self, X, Winv, bc, coef):
         Y = self.empty(X.shape[0], X.shape[1], like=X)
@@ -384,13 +400,9 @@ class GpuBackend:
         return self.q.lanczos_min_bound(self._cm(A), handle=self.h)
 
     def qr_q2(self, B, tol):
-        Q, R = self.q.qr_factor(self._cm(B), handle=self.h)
-        d = np.abs(np.diagonal(R.detach().cpu().numpy()))
-        hits = np.nonzero(d < tol)[0]
-        if hits.size == 0:
-            return 0, None
-        ind = int(hits[0]) + 1
-        return ind, self._cm(Q[:, ind - 1:])
+        # partial.cpp:71-79 on the device: trailing-column Q formation only
+        ind, Q2 = self.q.subspace_q2(self._cm(B), tol, handle=self.h)
+        return ind, (self._cm(Q2) if Q2 is not None else None)
 
     def syev(self, S):
         vals, V = self.q.sym_eig_dense(self._cm(S), handle=self.h)

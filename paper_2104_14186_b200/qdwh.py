@@ -621,6 +621,35 @@ def cholesky_inverse(z, *, handle: Optional[Handle] = None):
     return cholesky_factor_inverse(z, handle=handle)[1]
 
 
+def cholesky_inverse_fast(z, *, handle: Optional[Handle] = None):
+    """W^{-1} (upper) of a WELL-CONDITIONED Z = W^T W (the QDWH step's I + c X^T X) by
+    the recursive Cholesky-and-inverse; z (lower triangle read) is not modified."""
+    h = handle or default_handle()
+    Z = _Mat(z)
+    n = Z.shape[0]
+    Wi = _empty_like_kind(Z, n, n)
+    wp, ldw = _ptr_ld(Wi)
+    h.check(h.lib.qdwhg_cholesky_inverse_fast(h.h, n, Z.ptr, Z.ld, wp, ldw))
+    return Wi
+
+
+def subspace_q2(b, tol: float = 0.01, *, handle: Optional[Handle] = None):
+    """partial.cpp:71-79 — (ind, Q2): ind = first 1-based i with |R_ii| < tol of the
+    unpivoted QR of b (0 if none), Q2 = Q(:, ind-1:n) (None if ind == 0)."""
+    h = handle or default_handle()
+    B = _Mat(b)
+    n = B.shape[0]
+    Q2 = _empty_like_kind(B, n, n)
+    qp, ldq = _ptr_ld(Q2)
+    ind = ctypes.c_int64(0)
+    ell = ctypes.c_int64(0)
+    h.check(h.lib.qdwhg_subspace_q2(h.h, n, B.ptr, B.ld, float(tol), ctypes.byref(ind),
+                                    ctypes.byref(ell), qp, ldq, n))
+    if ind.value == 0:
+        return 0, None
+    return int(ind.value), Q2[:, :ell.value]
+
+
 def gaussian_matrix_device(m: int, n: int, seed: int, *, device=None,
                            handle: Optional[Handle] = None):
     """Counter-based N(0,1) matrix generated on the GPU (kernels.cpp:441-447 scheme)."""

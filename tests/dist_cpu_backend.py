@@ -41,6 +41,9 @@ class CpuBackend:
     def trmm_update(self, X, Winv, bc, coef):
         return bc * X + coef * ((X @ Winv) @ Winv.T)
 
+    def zinv_update(self, X, Winv, bc, coef):
+        return bc * X + coef * (X @ (Winv @ Winv.T))
+
     def sym_rows(self, A_full, r0, r1):
         return 0.5 * (A_full[r0:r1, :] + A_full[:, r0:r1].T)
 

@@ -290,3 +290,30 @@ def test_qr_outer_block_sizes(nbo):
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_cholesky_inverse_fast_and_subspace_q2(cuda):
+    """The two device building blocks of the distributed driver: the recursive
+    Cholesky-and-inverse on a well-conditioned Z, and the partial.cpp:71-79 subspace
+    extraction (ind, Q2) against the oracle's full QR."""
+    import torch
+    n = 700
+    x = O.gaussian_matrix(n, n, 17) / np.sqrt(n)
+    z = np.eye(n) + 3.0 * (x.T @ x)
+    zi = qdwh.cholesky_inverse_fast(torch.from_numpy(np.asfortranarray(z)).to(cuda)).cpu().numpy()
+    assert np.linalg.norm(zi.T @ z @ zi - np.eye(n)) <= 1e-12 * n
+    assert np.allclose(np.tril(zi, -1), 0.0)
+    # a rank-deficient "(X + I)/2"-like matrix: projector onto a 640-dim subspace
+    q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 18))
+    lam = np.concatenate([np.ones(640), np.zeros(n - 640)])
+    b = (q * lam) @ q.T
+    ind, q2 = qdwh.subspace_q2(torch.from_numpy(np.asfortranarray(b)).to(cuda), 0.01)
+    qo, ro = O.qr_factor(b)
+    ind_o = O.detect_deficiency_index(ro, 0.01)
+    assert ind == ind_o
+    q2 = q2.cpu().numpy()
+    ref = qo[:, ind - 1:]
+    assert q2.shape == ref.shape
+    assert np.linalg.norm(q2.T @ q2 - np.eye(q2.shape[1])) <= 1e-12 * n
+    # same subspace: the projectors agree
+    assert np.linalg.norm(q2 @ q2.T - ref @ ref.T) <= 1e-10
