@@ -270,22 +270,48 @@ FixedIterResult run_fixed_iterations(Ctx& ctx, const DMat& X, double ell0, size_
   FixedIterResult r;
   r.ell = ell0;
   r.trace.push_back(ell0);
-  for (size_t k = 0; k < iters; ++k) {
-    const WeightStep w = halley_weights(r.ell);
-    if (qr_first && k == 0) {
-      qdwh_qr_step(ctx, X, w, X);
-      ++r.iters_qr;
-    } else {
-      qdwh_chol_step(ctx, X, w, X, symmetric);  // symmetric output by construction
-      ++r.iters_chol;
+  // Fixed trip count, no fallback (polar.cpp:206-207): one pivot check after the
+  // last step instead of a host round trip per step; symmetric Cholesky steps
+  // ping-pong between X and a second buffer (their mirrored epilogue cannot write
+  // in place)
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat cur = X;
+  DMat spare;
+  const bool pingpong = symmetric && X.rows == X.cols && !qr_first;
+  if (pingpong) spare = ctx.arena->alloc(X.rows, X.cols);
+  QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
+  ctx.defer_pivot_check = true;
+  try {
+    for (size_t k = 0; k < iters; ++k) {
+      const WeightStep w = halley_weights(r.ell);
+      if (qr_first && k == 0) {
+        qdwh_qr_step(ctx, cur, w, cur);
+        ++r.iters_qr;
+        if (symmetric) symmetrize_scale(ctx, cur, 1.0, 0.0, cur);
+      } else if (pingpong) {
+        const DMat nxt = (cur.base == X.base) ? spare : X;
+        qdwh_chol_step(ctx, cur, w, nxt, true);  // symmetric output by construction
+        cur = nxt;
+        ++r.iters_chol;
+      } else {
+        qdwh_chol_step(ctx, cur, w, cur, symmetric);
+        ++r.iters_chol;
+      }
       r.ell = w.ell_out;
       r.trace.push_back(r.ell);
-      continue;
     }
-    if (symmetric) symmetrize_scale(ctx, X, 1.0, 0.0, X);
-    r.ell = w.ell_out;
-    r.trace.push_back(r.ell);
+  } catch (...) {
+    ctx.defer_pivot_check = false;
+    ctx.arena->release_to(mark);
+    throw;
   }
+  ctx.defer_pivot_check = false;
+  if (cur.base != X.base) copy(ctx, cur, X);
+  ctx.arena->release_to(mark);
+  int hflag = 0;
+  QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (hflag) throw NotPositiveDefinite("cholesky: pivot is not positive");
   return r;
 }
 

@@ -107,6 +107,9 @@ struct Ctx {
   Arena* arena = nullptr;
   int num_sms = 148;
   int panel_max_ctas = 0;  // GEQRF grid-panel CTA cap while a side stream runs (0 = none)
+  // run_fixed_iterations: the factorisations leave the sticky pivot flag for ONE
+  // check after the last step (no host round trip per Cholesky step)
+  bool defer_pivot_check = false;
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
   double* hscratch = nullptr;   // pinned host mirror of dscratch
   int* dflag = nullptr;         // device status flag

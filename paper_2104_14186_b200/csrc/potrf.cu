@@ -522,7 +522,7 @@ void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
   const int64_t n = Z.rows;
   const int nb = 128;
   if (n1 % nb || n1 <= 0 || n1 >= n) throw InvalidArgument("potrf_fast_split: bad split");
-  QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
+  if (!ctx.defer_pivot_check) QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);
   // W: only its off-diagonal upper blocks W12 are used, each written before it is
@@ -550,10 +550,11 @@ void potrf_fast_split(Ctx& ctx, const DMat& Z, const DMat& Winv, int64_t n1,
   GemmExtra e4;
   e4.krange = KRange::AUpper;  // W11^-1 upper
   gemm(ctx, Op::N, Op::N, -1.0, Winv.sub(0, 0, n1, n1), T, 0.0, Winv.sub(0, n1, n1, n2), e4);
+  ctx.arena->release_to(mark);
+  if (ctx.defer_pivot_check) return;
   int hflag = 0;
   QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
-  ctx.arena->release_to(mark);
   if (hflag) throw NotPositiveDefinite("cholesky: pivot is not positive");
 }
 
@@ -586,7 +587,8 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   if (Z.cols != n) throw InvalidArgument("cholesky: matrix not square");
   static const int nb_env = getenv("QDWHG_POTRF_NB") ? atoi(getenv("QDWHG_POTRF_NB")) : 0;
   const int nb = (nb_env == 32 || nb_env == 64 || nb_env == 96 || nb_env == 128) ? nb_env : 128;
-  QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
+  const bool defer = ctx.defer_pivot_check && !stable && !want_w;
+  if (!defer) QDWHG_CUDA(cudaMemsetAsync(ctx.dflag, 0, sizeof(int), ctx.stream));
   const Arena::Mark mark = ctx.arena->mark();
   DMat W = ctx.arena->alloc(n, n);
   // (the fast path without W output reads only W12 blocks it wrote first)
@@ -618,6 +620,10 @@ void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool wan
   }
   // one pivot check for the whole factorisation (a failed pivot poisons what
   // follows with NaN, which is discarded: the call throws)
+  if (defer) {
+    ctx.arena->release_to(mark);
+    return;
+  }
   int hflag = 0;
   QDWHG_CUDA(cudaMemcpyAsync(&hflag, ctx.dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));

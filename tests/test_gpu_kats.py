@@ -73,6 +73,24 @@ def test_chol_step_fails_over_and_qr_step_survives():
     assert threw
 
 
+def test_fixed_iterations_propagate_cholesky_failure():
+    # polar.cpp:206-207: a fixed-iteration run never falls back — NotPositiveDefinite
+    # from a Cholesky step propagates (the library checks the pivot flag once, after
+    # the last step: the same exception, no per-step host round trip)
+    witnesses = 0
+    for ell in (1e-15, 1.5e-15, 2e-15, 3e-15, 5e-15, 7e-15):
+        for rows in (2, 3, 4, 5):
+            x = np.ones((rows, 2))
+            try:
+                qdwh.qdwh_chol_step(x, ell)
+                continue
+            except qdwh.NotPositiveDefinite:
+                witnesses += 1
+            with pytest.raises(qdwh.NotPositiveDefinite):
+                qdwh.run_fixed_iterations(x, ell, 2, "CholeskyOnly")
+    assert witnesses > 0
+
+
 # ----------------------------------------------------------------- polar
 def test_polar_recognizes_spd_and_orthogonal():
     # test_polar.cpp:159-178
