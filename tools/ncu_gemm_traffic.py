@@ -22,8 +22,8 @@ def val(r, name):
         return None
     v = float(r[i].replace(",", ""))
     u = units[i]
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
-             "msecond": 1e3}.get(u, 1.0)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3,
+             "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(u, 1.0)
     return v * scale
 
 
