@@ -804,7 +804,8 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
       std::vector<double> hd((size_t)k * k, 0.0);
       for (int64_t i = 0; i < k; ++i) hd[i + (size_t)i * k] = vals[i];
       copy_from_host(ctx, hd.data(), k, D);
-      gemm(ctx, Op::N, Op::N, 1.0, As, out.V, 0.0, R);
+      // As V = (As Q2) W_k: the n x l product is already there (AQ), no n^2 k GEMM
+      gemm(ctx, Op::N, Op::N, 1.0, AQ, W.sub(0, 0, ell, k), 0.0, R);
       gemm(ctx, Op::N, Op::N, -1.0, out.V, D, 1.0, R);
       const double res = std::sqrt(mat_stats(ctx, R, false).fro2);
       ctx.arena->release_to(rm);
