@@ -664,9 +664,11 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   }
   Q2out = Q2buf.col_block(0, ell);
   gemm(ctx, Op::N, Op::N, 1.0, Y, U.col_block(0, ell), 0.0, Q2out);
-  // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice
+  // CholQR: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2).  Y U already has orthogonal columns
+  // (U: eigenvectors of Y^T Y, kappa(Y U) = sqrt(mu_max / mu_min) = O(10)), so one
+  // pass reaches rounding-level orthogonality
   DMat F = ctx.arena->alloc(ell, ell), Fi = ctx.arena->alloc(ell, ell), Qt = ctx.arena->alloc(n, ell);
-  for (int pass = 0; pass < 2; ++pass) {
+  for (int pass = 0; pass < 1; ++pass) {
     GemmExtra fl;
     fl.out = OutMode::Lower;
     gemm(ctx, Op::T, Op::N, 1.0, Q2out, Q2out, 0.0, F, fl);
