@@ -26,7 +26,9 @@ namespace {
 // Normalised start vector of the reference's counter generator (host glibc
 // log/cos: ~0.3 ms at n = 4096), cached per (n, seed) — it is the same vector on
 // every call of a given size.
-const std::vector<double>& start_vector(int64_t n, uint64_t seed) {
+// (returned by value: a copy of n doubles is nothing next to the generation, and
+// no caller holds a reference into the cache while another thread evicts it)
+std::vector<double> start_vector(int64_t n, uint64_t seed) {
   static std::mutex mu;
   static std::map<std::pair<int64_t, uint64_t>, std::vector<double>> cache;
   std::lock_guard<std::mutex> lock(mu);
@@ -37,8 +39,9 @@ const std::vector<double>& start_vector(int64_t n, uint64_t seed) {
   for (double x : v) s += x * x;
   const double nv = std::sqrt(s);
   for (double& x : v) x /= nv;
-  if (cache.size() > 64) cache.clear();
-  return cache.emplace(std::make_pair(n, seed), std::move(v)).first->second;
+  if (cache.size() >= 64) cache.clear();
+  cache.emplace(std::make_pair(n, seed), v);
+  return v;
 }
 
 // z_j = sum_i A(i,j) x_i  (one warp per column; coalesced down the column)
@@ -344,7 +347,7 @@ double two_norm_estimate(Ctx& ctx, const DMat& A) {
   if (st.fro2 == 0.0) throw InvalidArgument("two_norm_estimate: zero matrix");
   const Arena::Mark mark = ctx.arena->mark();
   Krylov K(ctx);
-  const std::vector<double>& v0 = start_vector(n, 0x6e6f726d32ull);  // kernels.cpp:336
+  const std::vector<double> v0 = start_vector(n, 0x6e6f726d32ull);  // kernels.cpp:336
   double* v = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
   double* y = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * m));
   double* z = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * n));
@@ -396,7 +399,7 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre
   if (m > 63) throw InvalidArgument("lanczos_min_bound: at most 63 steps supported");
   const Arena::Mark mark = ctx.arena->mark();
   DMat Q = ctx.arena->alloc(n, m + 1);
-  const std::vector<double>& q0 = start_vector(n, 0x6c616e637aull);  // kernels.cpp:379
+  const std::vector<double> q0 = start_vector(n, 0x6c616e637aull);  // kernels.cpp:379
   QDWHG_CUDA(cudaMemcpyAsync(Q.ptr(), q0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx.stream));
   // All steps run in one cooperative kernel without host round trips; a
   // breakdown (beta <= tol) is detected afterwards and the recurrence
