@@ -60,7 +60,7 @@ def test_qr_factor_matches_reference():
     assert np.all(np.tril(r, -1) == 0.0)
 
 
-@pytest.mark.parametrize("m,n", [(200, 130), (513, 512), (1000, 64), (70, 70), (2048, 1000)])
+@pytest.mark.parametrize("m,n", [(200, 130), (513, 512), (1000, 64), (70, 70), (2048, 1000), (5000, 100)])
 def test_qr_factor_identities(m, n):
     a = O.gaussian_matrix(m, n, 7 + m + n)
     q, r = qdwh.qr_factor(a)
