@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
 
   // ---------------- epilogue: accumulators -> smem tile -> coalesced column writes
   __syncthreads();  // every warp is past the mainloop: the stage buffers are free
+  // PDL: the next kernel may be scheduled now (once every CTA of this grid got
+  // here); it still waits in griddep_wait() for this grid's completion and memory
+  // flush, so only its launch and prologue overlap this epilogue
+  griddep_launch_dependents();
   constexpr int LDC = BM + 2;  // conflict-free 8-byte writes per half-warp
   double* Cs = sA;
 #pragma unroll
@@ -357,7 +361,6 @@ __global__ void __launch_bounds__(WM * WN * 32, 1)
       }
     }
   }
-  griddep_launch_dependents();
 }
 
 // Split-K reduction + epilogue: D = alpha * sum_z P_z + beta * Cin (+diag), with

@@ -344,6 +344,8 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   }
   DIAG_MARK(15);
 
+  // PDL: the dependent GEMM's launch and prologue overlap the write-out below
+  griddep_launch_dependents();
   // ---- Winv = L^{-T} (upper) with explicit zeros below.  Winv(r, c) = A[r * kLDA + c]:
   // 8 lanes per column (4 columns per warp instruction), so the transposed shared
   // reads hit 16 distinct bank pairs (kLDA = 132) instead of 4 with a lane per row
