@@ -369,6 +369,7 @@ __global__ void splitk_reduce_kernel(const GemmParams p) {
   const int64_t total = (int64_t)p.M * p.N;
   const bool lower = p.omode != (int)OutMode::Full;
   const bool mirror = p.omode == (int)OutMode::LowerMirror;
+  griddep_wait();  // PDL launch: the partials of the GEMM just before
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(idx % p.M), j = (int)(idx / p.M);
@@ -381,6 +382,7 @@ __global__ void splitk_reduce_kernel(const GemmParams p) {
     p.D[i + (size_t)j * p.ldd] = v;
     if (mirror && i != j) p.D[j + (size_t)i * p.ldd] = v;
   }
+  griddep_launch_dependents();
 }
 
 // Reduction of a compact split-K tail launch: block t sums the partials of
@@ -740,8 +742,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
   if (splits > 1) {
     const int64_t total = M * N;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * ctx.num_sms);
-    splitk_reduce_kernel<<<blocks, 256, 0, ctx.stream>>>(p);
-    QDWHG_CUDA(cudaGetLastError());
+    launch_pdl(ctx, splitk_reduce_kernel, dim3(blocks), dim3(256), 0, p);
     ctx.count();
   }
   ctx.arena->release_to(mark);
