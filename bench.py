@@ -235,49 +235,19 @@ def make_input(cfg, dev, handle):
 
 
 def _make_input(cfg, dev, handle):
-    import torch
-    from paper_2104_14186_b200 import matgen, qdwh
-    c = config_desc(cfg)
-    if c["kind"] == "eig":
-        n = c["n"]
-        if c["family"] == "wishart":
-            G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=handle)
-            A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
-            qdwh.gemm(G, G, A, alpha=1.0 / n, trans_a=True, handle=handle)
-            A -= torch.eye(n, dtype=torch.float64, device=dev)
-            A = 0.5 * (A + A.t())
-            A = A.t().contiguous().t()
-            return dict(A=A, c=c["shift"], k=c["k"], truth=None, kind="eig")
-        lam = matgen.config_eigenvalues(c["family"], n, c["seed"])
-        G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=handle)
-        Q, _ = qdwh.qr_factor(G, handle=handle)
-        QL = (Q * torch.from_numpy(lam).to(dev)[None, :]).t().contiguous().t()
-        A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
-        qdwh.gemm(QL, Q, A, trans_b=True, handle=handle)
-        A = (0.5 * (A + A.t())).t().contiguous().t()
-        k = c["k"]
-        cs = matgen.largest_k_shift(lam, k)
-        return dict(A=A, c=cs, k=k, truth=np.sort(lam)[::-1][:k], kind="eig")
-    m, n = c["m"], c["n"]
-    sig = matgen.config_singular_values(c["family"], n)
-    Gl = qdwh.gaussian_matrix_device(m, n, c["seed"] ^ matgen.LEFT_STREAM, device=dev, handle=handle)
-    U, _ = qdwh.qr_factor(Gl, handle=handle) if m == n else (None, None)
-    if m != n:
-        # thin Q of the tall Gaussian: first n columns of the QR's Q
-        U = thin_q(Gl, handle)
-    Gr = qdwh.gaussian_matrix_device(n, n, c["seed"] ^ matgen.RIGHT_STREAM, device=dev, handle=handle)
-    V, _ = qdwh.qr_factor(Gr, handle=handle)
-    US = (U[:, :n] * torch.from_numpy(sig).to(dev)[None, :]).t().contiguous().t()
-    A = torch.empty((n, m), dtype=torch.float64, device=dev).t()
-    qdwh.gemm(US, V, A, trans_b=True, handle=handle)
-    k = c["k"]
-    return dict(A=A, cut=matgen.sigma_cut(sig, k), k=k, truth=np.sort(sig)[::-1][:k], kind="svd")
+    """Deterministic device generation (matgen.device_input: seeded device Gaussian,
+    our QR in QDWHG_FLAG_DETERMINISTIC mode) — the same bytes as the full-size
+    parity fixtures (tests/golden/fullsize/cfgN.npz, keyed by SHA-256)."""
+    from paper_2104_14186_b200 import matgen
+    return matgen.device_input(cfg, dev)
 
 
-def thin_q(G, handle):
-    from paper_2104_14186_b200 import qdwh
-    Q, _ = qdwh.qr_factor(G, handle=handle)
-    return Q[:, :G.shape[1]]
+def fullsize_fixture(cfg):
+    p = os.path.join(ROOT, "tests", "golden", "fullsize", f"cfg{cfg}.npz")
+    if not os.path.exists(p):
+        return None
+    z = np.load(p)
+    return {k: z[k] for k in z.files}
 
 
 def solve(inp, handle, host=False):
@@ -406,11 +376,17 @@ def run_reference_arm(args, rank):
     line = dict(base, value=value, unit="TFLOP/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * float(np.mean(times)),
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
-                data="synthetic", config=config_json(args.config, args.gpus),
+                data="synthetic",
+                config=dict(config_json(args.config, args.gpus), same_input=False,
+                            sample_n=sample.get("n"), sample_m=sample.get("m", sample.get("n")),
+                            sample_k=sample.get("k"),
+                            sample=f"{sample['desc']} — a bounded sample of the workload "
+                                   f"family; the rate (TFLOP/s) is comparable, the time is not"),
                 cpu_baseline={"value": value, "unit": "TFLOP/s", "cores": cores,
                               "kind": "reference",
                               "sample": f"{cores} concurrent single-threaded reference solves per "
-                                        f"step, each: {sample['desc']}"},
+                                        f"step, each: {sample['desc']}",
+                              "same_input_reference": same_input_reference(args.config)},
                 e2e={"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                      "d2h_bytes_per_step": 0},
                 host_cpu=cpu_model())
@@ -531,8 +507,11 @@ def main():
     else:
         d2h = k * 8 + (inp["A"].shape[0] + inp["A"].shape[1]) * k * 8
 
-    # ---- correctness of what was timed (device residual / orthogonality, planted truth)
+    # ---- correctness of what was timed (device residual / orthogonality, planted
+    # truth, and the CPU oracle's values on the same input bytes — fixture keyed by
+    # the input's SHA-256, tests/golden/fullsize)
     check = verify(inp, res)
+    check.update(oracle_check(args.config, inp, res))
 
     # ---- aggregate over ranks (max time, summed work)
     tot_t, tot_f = float(sum(times)), float(sum(flops))
@@ -593,10 +572,53 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         cb = cpu_baseline(args.config)
         if cb:
+            sir = same_input_reference(args.config)
+            if sir:
+                sir["time_ratio_vs_gpu_value"] = sir["seconds"] / (tot_t / args.steps)
+                sir["time_ratio_vs_gpu_e2e"] = sir["seconds"] / (e_t / e2e_steps)
+                cb["same_input_reference"] = sir
             line["cpu_baseline"] = cb
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def oracle_check(cfg, inp, res):
+    from paper_2104_14186_b200 import matgen
+    fx = fullsize_fixture(cfg)
+    a = matgen.host_copy(inp["A"])
+    sha = matgen.input_sha256(a)
+    del a
+    out = {"input_sha256": sha}
+    if fx is None or str(fx["sha256"]) != sha:
+        out["oracle_match"] = "no fixture for these input bytes"
+        return out
+    if inp["kind"] == "eig":
+        got = np.sort(np.asarray(res.lambda_minus))[::-1]
+    else:
+        got = np.asarray(res.sigma1)
+    want = fx["values"]
+    out["oracle_k"] = int(len(want))
+    if len(got) != len(want):
+        out["oracle_match"] = f"k differs: {len(got)} vs oracle {len(want)}"
+        return out
+    out["max_rel_err_vs_oracle"] = float(np.max(np.abs(got - want) / np.abs(want)))
+    out["oracle_match"] = bool(out["max_rel_err_vs_oracle"] <= 1e-10)
+    out["oracle_source"] = ("tests/golden/fullsize/cfg%d.npz: pinned numpy oracle on the same bytes"
+                            % cfg) + (" + the reference itself" if "ref_values" in fx else "")
+    return out
+
+
+def same_input_reference(cfg):
+    """The reference's own single-threaded time-to-solution on this config's exact
+    input bytes, measured once on a B200 box's host (tests/golden/make_fullsize.py
+    --ref) and cached with the input hash."""
+    fx = fullsize_fixture(cfg)
+    if fx is None or "reference" not in fx:
+        return None
+    meta = json.loads(str(fx["reference"]))
+    return {"seconds": meta["seconds"], "threads": 1, "input_sha256": str(fx["sha256"]),
+            "host_cpu": str(fx["host_cpu"]), "source": f"tests/golden/fullsize/cfg{cfg}.npz"}
 
 
 def verify(inp, res):

@@ -61,8 +61,13 @@ typedef struct qdwhg_options {
   int32_t device;        /* CUDA ordinal; -1 = current device */
   int32_t reserved0;
   uint64_t arena_bytes;  /* 0 = grow on demand */
-  uint64_t flags;        /* reserved, 0 */
+  uint64_t flags;        /* QDWHG_FLAG_* bits, 0 = defaults */
 } qdwhg_options;
+
+/* Bitwise run-to-run reproducible results: the cross-CTA reductions of the tall
+ * QR panels sum per-CTA partials in a fixed order instead of FP64 atomics
+ * (slower panels on matrices with more than 2048 rows). */
+#define QDWHG_FLAG_DETERMINISTIC 1u
 
 #define QDWHG_MAX_TRACE 64
 #define QDWHG_NUM_STAGES 8
@@ -169,6 +174,8 @@ typedef struct qdwhg_kernel_stats {
   double gemm_busy_seconds;     /* union of the launch intervals (concurrent launches counted once) */
 } qdwhg_kernel_stats;
 qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable);
+/* Toggle QDWHG_FLAG_DETERMINISTIC on an existing handle. */
+qdwhg_status qdwhg_set_deterministic(qdwhg_handle* h, int32_t enable);
 qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out);
 
 /* ---- drivers ------------------------------------------------------------ */

@@ -223,7 +223,9 @@ def require_symmetric(a: np.ndarray, who: str):
 
 def symmetrize(a: np.ndarray) -> np.ndarray:
     """matrix.cpp:99-105"""
-    return 0.5 * (a + a.T)
+    out = a + a.T
+    out *= 0.5
+    return out
 
 
 # ---------------------------------------------------------------- kernels
@@ -268,6 +270,33 @@ def qr_factor(a: np.ndarray):
     return q, r
 
 
+def qr_trailing_q(a: np.ndarray, c0: int):
+    """(Q(:, c0:m), |diag R|-ready R) of the Householder QR of square-or-tall a —
+    the columns of kernels.cpp:105-112's full Q that partial.cpp:79/146 keep
+    (Q2 = Q(:, ind-1:n)), formed by applying the reflectors to the trailing
+    identity columns (LAPACK dgeqrf + dormqr, same reflectors and convention as
+    np.linalg.qr, so the same Q columns up to rounding) instead of forming all of
+    Q.  Returns (r, form) with form(c0) -> Q(:, c0:m)."""
+    import scipy.linalg.lapack as L
+    require_finite(a, "qr_factor")
+    m, n = a.shape
+    qr, tau, work, info = L.dgeqrf(np.asfortranarray(a))
+    if info != 0:
+        raise RuntimeError(f"dgeqrf info={info}")
+    r = np.triu(qr[:n, :]) if m >= n else np.triu(qr)
+
+    def form(c0: int) -> np.ndarray:
+        e = np.zeros((m, m - c0), order="F")
+        e[c0:, :] = np.eye(m - c0)
+        lw = L.dormqr("L", "N", qr, tau, e, -1)[1]
+        out, _, info2 = L.dormqr("L", "N", qr, tau, e, max(int(lw[0].real), 1), overwrite_c=1)
+        if info2 != 0:
+            raise RuntimeError(f"dormqr info={info2}")
+        return out
+
+    return r, form
+
+
 def qr_factor_thin(a: np.ndarray, ncols: int):
     """kernels.cpp:114-122"""
     require_finite(a, "qr_factor")
@@ -282,10 +311,11 @@ def cholesky(z: np.ndarray) -> np.ndarray:
     require_finite(z, "cholesky")
     if z.shape[0] != z.shape[1]:
         raise ValueError("cholesky: matrix not square")
-    try:
-        return np.linalg.cholesky(z).T.copy()
-    except np.linalg.LinAlgError as e:  # pivot <= 0
-        raise NotPositiveDefinite(str(e)) from None
+    import scipy.linalg.lapack as L
+    w, info = L.dpotrf(np.asfortranarray(z), lower=0, clean=1)
+    if info != 0:  # pivot <= 0 (kernels.cpp:136-138)
+        raise NotPositiveDefinite(f"cholesky: pivot {info} is not positive")
+    return w
 
 
 def sym_eig_dense(s: np.ndarray):
@@ -395,11 +425,17 @@ def qdwh_chol_step(x: np.ndarray, w: WeightStep) -> np.ndarray:
     """polar.cpp:82-128 — Z = I + c sym(X^T X), W = chol(Z), X+ = (b/c)X + (a-b/c) X W^-1 W^-T."""
     require_finite(x, "qdwh_chol_step")
     import scipy.linalg as sla
+    import scipy.linalg.blas as B
     n = x.shape[1]
-    z = symmetrize(x.T @ x) * w.c + np.eye(n)
+    # Z = I + c sym(X^T X): the Gram is symmetric by construction (DSYRK's upper
+    # triangle, mirrored), so sym() is the identity on it
+    z = B.dsyrk(w.c, np.asfortranarray(x), trans=1, lower=0)
+    z = np.triu(z) + np.triu(z, 1).T
+    z[np.diag_indices(n)] += 1.0
     wu = cholesky(z)
-    y = sla.solve_triangular(wu, x.T, trans="T", lower=False).T      # Y W = X
-    g = sla.solve_triangular(wu, y.T, trans="N", lower=False).T      # G W^T = Y
+    # Y W = X  ->  Y = X W^-1 ;  G W^T = Y  ->  G = Y W^-T   (right-side DTRSMs)
+    y = B.dtrsm(1.0, wu, np.array(x, order="F", copy=True), side=1, lower=0, trans_a=0)
+    g = B.dtrsm(1.0, wu, y, side=1, lower=0, trans_a=1, overwrite_b=1)
     bc = w.b / w.c
     return bc * x + (w.a - bc) * g
 
@@ -534,7 +570,7 @@ def qdwh_partial_eig(a: np.ndarray, plan: ShiftPlan, use_randomization: bool = F
     b = it.x * 0.5 + 0.5 * np.eye(n)
     if use_randomization:
         b = b @ gaussian_matrix(n, n, seed)
-    q, r = qr_factor(b)
+    r, form_q = qr_trailing_q(b, 0)
     ind = detect_deficiency_index(r, tol)
     if ind is None:
         return res
@@ -542,7 +578,7 @@ def qdwh_partial_eig(a: np.ndarray, plan: ShiftPlan, use_randomization: bool = F
     ell = n - ind + 1
     res.subspace_size = ell
     res.no_savings = ell > n // 2
-    q2 = q[:, ind - 1: ind - 1 + ell]
+    q2 = form_q(ind - 1)[:, :ell]
     reduced = symmetrize(q2.T @ (a_scaled @ q2))
     vals, vecs = sym_eig_dense(reduced)
     max_abs_ritz = float(np.max(np.abs(vals))) if vals.size else 0.0
@@ -604,7 +640,7 @@ def qdwh_partial_svd(a: np.ndarray, s: float, tol: float = 0.01,
     mm = np.eye(n) - symmetrize(x.T @ x)
     if use_randomization:
         mm = mm @ gaussian_matrix(n, n, seed)
-    q, r = qr_factor(mm)
+    r, form_q = qr_trailing_q(mm, 0)
     ind = detect_deficiency_index(r, tol)
     if ind is None:
         return res
@@ -612,7 +648,7 @@ def qdwh_partial_svd(a: np.ndarray, s: float, tol: float = 0.01,
     ell = n - ind + 1
     res.subspace_size = ell
     res.no_savings = ell > n // 2
-    q2 = q[:, ind - 1: ind - 1 + ell]
+    q2 = form_q(ind - 1)[:, :ell]
     u, sig, v = svd_dense(a @ q2)
     cutoff = s * res.alpha
     k = 0

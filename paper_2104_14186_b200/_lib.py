@@ -79,6 +79,7 @@ SIGNATURES = {
     "qdwhg_synchronize": [_P],
     "qdwhg_set_stream": [_P, _P],
     "qdwhg_profile": [_P, _I32],
+    "qdwhg_set_deterministic": [_P, _I32],
     "qdwhg_get_kernel_stats": [_P, _P],
     "qdwhg_partial_eig": [_P, _I64, _P, _I64, _I64, _I32, _D, _U64, _P, _P, _I64, _I64, _P],
     "qdwhg_partial_eig_request": [_P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P],

@@ -10,7 +10,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 
 #include "../../include/qdwhg.h"
 #include "drivers.hpp"
@@ -18,6 +22,31 @@
 namespace qdwhg {
 
 // ---------------------------------------------------------------- arena
+void func_attr(const void* kern, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int, int>> done;
+  int dev = 0;
+  QDWHG_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_tuple(dev, kern, (int)attr, value);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return;
+  QDWHG_CUDA(cudaFuncSetAttribute(kern, attr, value));
+  done.insert(key);
+}
+
+int per_device_cached(int slot, int (*probe)()) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, int> cache;
+  int dev = 0;
+  QDWHG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, slot});
+  if (it != cache.end()) return it->second;
+  const int v = probe();
+  cache[{dev, slot}] = v;
+  return v;
+}
+
 Arena::~Arena() {
   for (auto& c : chunks_) cudaFree(c.base);
 }
@@ -294,6 +323,7 @@ qdwhg_status qdwhg_create(qdwhg_handle** out, const qdwhg_options* opts) {
     QDWHG_CUDA(cudaMallocHost(&h->ctx.hscratch, 1 << 16));
     QDWHG_CUDA(cudaMalloc(&h->ctx.dflag, 256));
     if (opts && opts->arena_bytes) h->arena.reserve(opts->arena_bytes);
+    h->ctx.deterministic = opts && (opts->flags & QDWHG_FLAG_DETERMINISTIC);
   });
   if (st != QDWHG_OK) {
     delete h;
@@ -340,6 +370,12 @@ qdwhg_status qdwhg_set_stream(qdwhg_handle* h, void* stream) {
     QDWHG_CUDA(cudaStreamSynchronize(h->ctx.stream));
     h->ctx.stream = stream ? static_cast<cudaStream_t>(stream) : h->stream;
   });
+}
+
+qdwhg_status qdwhg_set_deterministic(qdwhg_handle* h, int32_t enable) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  h->ctx.deterministic = enable != 0;
+  return QDWHG_OK;
 }
 
 qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable) {

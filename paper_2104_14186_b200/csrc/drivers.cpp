@@ -127,10 +127,12 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
     GemmExtra sx;
     sx.split_k = 1;
     sx.force_bm = 128;
+    // W^-1's strictly lower part is never written by the chain's leaves
+    // (kDiagUpperOnly) but is read as zeros by the main-stream GEMMs of the left
+    // half of the recursion (W11^-T, W^-1 operands): zeroed on the main stream,
+    // before anything reads it (the arena hands back stale data otherwise)
+    zero_strict_lower(ctx, Winv);
     on_side(ctx.ev_side, [&] {
-      // W^-1's strictly lower part (never written by the chain) zeroed off the
-      // critical path; the main stream reads it only after waiting on ev_side
-      zero_strict_lower(ctx, Winv);
       // Z22 lower in <= 64-tile pieces: two lower diagonal quarters + one full block
       const int64_t h1 = ((n2 / 2 + 127) / 128) * 128, h2 = n2 - h1;
       GemmExtra lo = sx;
@@ -591,6 +593,10 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   static const bool off = getenv("QDWHG_SUBSPACE_HOUSEHOLDER") != nullptr;
   const int64_t n = B.rows;
   if (off || B.cols != n || n < 1024) return false;
+  // the delta shift below floors every |W_ii| at ~sqrt(delta): a tol that close
+  // to it cannot be resolved by this path (the reference's Householder R can)
+  const double delta = 32.0 * std::sqrt((double)n) * kEps;
+  if (!(tol > 10.0 * std::sqrt(delta))) return false;
   if ((double)n - device_trace(ctx, B) > (double)n / 16.0) return false;  // l estimate
   const Arena::Mark mark = ctx.arena->mark();
   DMat G = ctx.arena->alloc(n, n);
@@ -599,7 +605,7 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   syrk.out = OutMode::Lower;
   // ||B||_2 <= 1 (B = (X + I)/2, |eig(X)| <= 1): delta a few times the rounding
   // noise of the Gram's entries keeps the deficient tail positive definite
-  syrk.diag_add = 32.0 * std::sqrt((double)n) * kEps;
+  syrk.diag_add = delta;
   gemm(ctx, Op::T, Op::N, 1.0, B, B, 0.0, G, syrk);
   try {
     potrf_upper_and_inverse(ctx, G, Winv, /*want_w=*/false, /*stable=*/false);
@@ -617,8 +623,9 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
       break;
     }
   if (ind == 0) {
+    // no deficient pivot: confirmed on the reference's Householder path (as for k == 0)
     ctx.arena->release_to(mark);
-    return true;
+    return false;
   }
   const int64_t ell = n - (int64_t)ind + 1, k1 = (int64_t)ind - 1;
   // >= 8 oversampling columns, rounded up to a multiple of 64 so the skinny

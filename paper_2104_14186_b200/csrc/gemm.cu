@@ -503,11 +503,7 @@ void launch_cfg(Ctx& ctx, const DMat& A, const DMat& B, GemmParams& p) {
   constexpr int threads = WM * WN * 32;
   constexpr size_t smem = 1024 + (size_t)STAGES * (BM + BN) * BK * 8 + 2 * STAGES * 8;
   auto kern = gemm_dmma_kernel<BM, BN, WM, WN, STAGES, AK, BK_>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const CUtensorMap ta = AK ? make_desc(A, 16, BM) : make_desc(A, 16, 16);
   const CUtensorMap tb = BK_ ? make_desc(B, 16, BN) : make_desc(B, 16, 16);
   int ntiles;

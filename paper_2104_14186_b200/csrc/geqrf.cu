@@ -36,6 +36,13 @@ __device__ long long g_panel_trace[16];
 
 constexpr int kPanelThreads = 256;
 constexpr int kBW = 64;  // max panel width (one thread column per panel column)
+// Deterministic grid-path reduction (the shared-memory grid panel always, the
+// register panel when Ctx::deterministic): per-CTA slots
+// [2 parity][kMaxGridCtas][2*kBW] after the atomic accumulators, summed in CTA
+// order by every CTA after the grid barrier — bitwise reproducible run to run.
+constexpr int kMaxGridCtas = 160;
+constexpr size_t kAccDoubles = 3 * 2 * kBW;  // atomic accumulators (zero between launches)
+constexpr size_t kSlotDoubles = (size_t)2 * kMaxGridCtas * 2 * kBW;
 
 
 // Partial sums for pivot column `col` over this CTA's rows:
@@ -68,6 +75,29 @@ QDWHG_DEV void panel_partials(const double* S, int RP, int nr, int rbeg, int b, 
   __syncthreads();
 }
 
+// tot[s] = sum of slots[g][s] over CTAs g = 0..G-1 in a fixed order (strided
+// groups of nthreads / (2 kBW) threads, then the groups in order): every CTA
+// computes the same bits.  `scratch` holds nthreads doubles of shared memory.
+__device__ __forceinline__ void slot_sum(const double* slots, int G, double* scratch, double* tot,
+                                         int nthreads) {
+  const int tid = threadIdx.x;
+  const int np = nthreads / (2 * kBW);
+  const int s = tid % (2 * kBW), part = tid / (2 * kBW);
+  if (part < np) {
+    double acc0 = 0.0;
+    const double* p = slots + (size_t)part * 2 * kBW + s;
+#pragma unroll 4
+    for (int g = part; g < G; g += np, p += (size_t)np * 2 * kBW) acc0 += __ldcg(p);
+    scratch[part * 2 * kBW + s] = acc0;
+  }
+  __syncthreads();
+  if (tid < 2 * kBW) {
+    double t = 0.0;
+    for (int q = 0; q < np; ++q) t += scratch[q * 2 * kBW + tid];
+    tot[tid] = t;
+  }
+}
+
 // Unblocked Householder QR of an mp x b panel (b <= 64) whose rows are spread
 // over the CTAs of the launch, each CTA keeping its rows in shared memory.
 // Per column ONE cross-CTA reduction of [x0, sigma^2, a_jj,c, x^T a_c] gives the
@@ -75,8 +105,8 @@ QDWHG_DEV void panel_partials(const double* S, int RP, int nr, int rbeg, int b, 
 //   CLUSTER = true : one thread-block cluster (<= 16 CTAs): partial vectors are
 //                    read from the peers' shared memory (DSMEM) in fixed order
 //                    (deterministic) behind one hardware cluster barrier;
-//   CLUSTER = false: any number of co-resident CTAs (cooperative launch): FP64
-//                    atomics into a rotating global buffer + a grid barrier.
+//   CLUSTER = false: any number of co-resident CTAs (cooperative launch): per-CTA
+//                    slots + a grid barrier, summed in CTA order (deterministic).
 template <bool CLUSTER>
 __global__ void __launch_bounds__(kPanelThreads, 1)
     geqr2_panel_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
@@ -122,19 +152,19 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
       }
       __syncthreads();
     } else {
-      double* buf = acc + (col % 3) * (2 * kBW);
+      // slot per CTA, double-buffered by parity: a CTA writes column col+2's
+      // slot only after the barrier of col+1, which every CTA reaches after
+      // reading column col's slots
+      double* buf = acc + kAccDoubles + (size_t)(col & 1) * kMaxGridCtas * (2 * kBW);
       if (threadIdx.x < 2 * kBW) {
         const int cc = threadIdx.x % kBW;
-        if (cc < b && cc >= col && mine[threadIdx.x] != 0.0) atomicAdd(&buf[threadIdx.x], mine[threadIdx.x]);
+        __stcg(&buf[(size_t)blockIdx.x * 2 * kBW + threadIdx.x],
+               (cc < b && cc >= col) ? mine[threadIdx.x] : 0.0);
       }
       PANEL_MARK(5, col);
       grid_sync(bar, epoch);
       PANEL_MARK(6, col);
-      if (threadIdx.x < 2 * kBW) tot[threadIdx.x] = __ldcg(&buf[threadIdx.x]);
-      if (blockIdx.x == 0) {  // buffer col+2 was last read before this barrier
-        double* z = acc + ((col + 2) % 3) * (2 * kBW);
-        if (threadIdx.x < 2 * kBW) z[threadIdx.x] = 0.0;
-      }
+      slot_sum(buf, (int)gridDim.x, red, tot, kPanelThreads);
       __syncthreads();
     }
     PANEL_MARK(7, col);
@@ -278,7 +308,7 @@ struct PanelTail {
   unsigned* ticket;   // grid path: last-CTA election for the buffer cleanup
 };
 
-template <bool CLUSTER, int NRG, int RPT>
+template <bool CLUSTER, int NRG, int RPT, bool DET>
 __global__ void __launch_bounds__(64 * NRG, 1)
     geqr2_panel_reg_kernel(double* A, int64_t lda, double* V, int64_t ldv, double* tau_out, int mp,
                            int b, int rpc, double* acc, unsigned* bar, PanelTail tl) {
@@ -378,6 +408,16 @@ __global__ void __launch_bounds__(64 * NRG, 1)
       }
       __syncthreads();
     } else {
+      if constexpr (DET) {
+        // per-CTA slots, parity double-buffered (see geqr2_panel_kernel)
+        double* buf = acc + kAccDoubles + (size_t)(col & 1) * kMaxGridCtas * (2 * kBW);
+        if (tid < 2 * kBW) __stcg(&buf[(size_t)blockIdx.x * 2 * kBW + tid], mine[tid]);
+        side();
+        grid_sync(bar, epoch);
+        slot_sum(buf, (int)gridDim.x, red, tot, NT);
+        __syncthreads();
+        return;
+      }
       double* buf = acc + (col % 3) * (2 * kBW);
       if (tid < 2 * kBW) {
         const int cc = tid % kBW;
@@ -659,9 +699,8 @@ constexpr size_t kPanelSmemMax = 220 * 1024;
 
 // Largest cluster the device allows for the panel (16 non-portable, else 8).
 int cluster_size_limit() {
-  static int cs = -1;
-  if (cs < 0) {
-    cs = 8;
+  return per_device_cached(0, [] {
+    int cs = 8;
     if (cudaFuncSetAttribute(geqr2_panel_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
                              1) == cudaSuccess) {
       cudaLaunchConfig_t cfg = {};
@@ -680,16 +719,15 @@ int cluster_size_limit() {
         cs = 16;
     }
     cudaGetLastError();
-  }
-  return cs;
+    return cs;
+  });
 }
 
 // Largest cluster the register-resident panel kernel can use (16 non-portable, else 8).
 int reg_cluster_limit() {
-  static int cs = -1;
-  if (cs < 0) {
-    cs = 8;
-    auto kern = geqr2_panel_reg_kernel<true, 8, 32>;
+  return per_device_cached(1, [] {
+    int cs = 8;
+    auto kern = geqr2_panel_reg_kernel<true, 8, 32, false>;
     const size_t smem = panel_reg_smem<8, 32>();
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
@@ -709,22 +747,18 @@ int reg_cluster_limit() {
       if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) cs = 16;
     }
     cudaGetLastError();
-  }
-  return cs;
+    return cs;
+  });
 }
 
-template <bool CL, int RPT, int NRG = 8>
-void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr, int64_t ldv,
+template <bool CL, int RPT, bool DET = false, int NRG = 8>
+void launch_panel_reg_t(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr, int64_t ldv,
                       double* tau_dev, int mp, int b, int rpc, double* acc, unsigned* bar,
                       PanelTail tl) {
-  auto kern = geqr2_panel_reg_kernel<CL, NRG, RPT>;
+  auto kern = geqr2_panel_reg_kernel<CL, NRG, RPT, DET>;
   const size_t smem = panel_reg_smem<NRG, RPT>();
-  static bool set = false;
-  if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (CL) QDWHG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    set = true;
-  }
+  func_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (CL) func_attr(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (CL) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblk);
@@ -747,6 +781,16 @@ void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr,
                                            ctx.stream));
   }
   ctx.count();
+}
+
+template <bool CL, int RPT>
+void launch_panel_reg(Ctx& ctx, int nblk, double* Ap, int64_t lda, double* Vptr, int64_t ldv,
+                      double* tau_dev, int mp, int b, int rpc, double* acc, unsigned* bar,
+                      PanelTail tl) {
+  if (!CL && ctx.deterministic)
+    launch_panel_reg_t<CL, RPT, true>(ctx, nblk, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
+  else
+    launch_panel_reg_t<CL, RPT, false>(ctx, nblk, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
 }
 
 // Register-resident panel when the panel fits (cluster of <= 16 CTAs x 256
@@ -784,8 +828,8 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
   // cooperative grid (FP64 atomics + grid barrier); while a look-ahead side
   // stream runs, the grid is capped (ctx.panel_max_ctas) so the panel does not
   // need the whole machine at once
-  const int max_ctas =
-      ctx.panel_max_ctas > 0 ? std::min(ctx.panel_max_ctas, ctx.num_sms) : ctx.num_sms;
+  const int sms = std::min(ctx.num_sms, kMaxGridCtas);  // slot capacity of the grid reduction
+  const int max_ctas = ctx.panel_max_ctas > 0 ? std::min(ctx.panel_max_ctas, sms) : sms;
   if (ceil_div(mp, 8 * 8) <= max_ctas) {
     const int nb = ceil_div(mp, 8 * 8), rpc = ceil_div(mp, nb);
     launch_panel_reg<false, 8>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
@@ -801,13 +845,13 @@ bool panel_factor_reg(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, 
     launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
     return true;
   }
-  if (max_ctas < ctx.num_sms) {  // taller than the cap allows: uncapped
-    if (ceil_div(mp, 8 * 16) <= ctx.num_sms) {
+  if (max_ctas < sms) {  // taller than the cap allows: uncapped
+    if (ceil_div(mp, 8 * 16) <= sms) {
       const int nb = ceil_div(mp, 8 * 16), rpc = ceil_div(mp, nb);
       launch_panel_reg<false, 16>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
       return true;
     }
-    if (ceil_div(mp, 8 * 32) <= ctx.num_sms) {
+    if (ceil_div(mp, 8 * 32) <= sms) {
       const int nb = ceil_div(mp, 8 * 32), rpc = ceil_div(mp, nb);
       launch_panel_reg<false, 32>(ctx, nb, Ap, lda, Vptr, ldv, tau_dev, mp, b, rpc, acc, bar, tl);
       return true;
@@ -823,14 +867,8 @@ bool panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
   if (panel_factor_reg(ctx, P, Vp, tau_dev, acc, bar, tl)) return true;
   // shared-memory panel kernel: panels taller than the register path covers
   int mp = (int)P.rows, b = (int)P.cols;
-  static bool set = false;
-  if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel<false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax));
-    QDWHG_CUDA(cudaFuncSetAttribute(geqr2_panel_kernel<true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax));
-    set = true;
-  }
+  func_attr(geqr2_panel_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax);
+  func_attr(geqr2_panel_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPanelSmemMax);
   double* Ap = P.ptr();
   int64_t lda = P.ld;
   double* Vptr = Vp.ptr();
@@ -860,17 +898,16 @@ bool panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
     return false;
   }
   // grid path (tall panels): cooperative launch over up to all SMs
-  const int nblk = std::max(1, std::min(ctx.num_sms, (mp + 63) / 64));
+  const int nblk = std::max(1, std::min(std::min(ctx.num_sms, kMaxGridCtas), (mp + 63) / 64));
   rpc = (mp + nblk - 1) / nblk;
   if (panel_smem(rpc) > kPanelSmemMax) throw InvalidArgument("geqrf: panel too tall for shared memory");
-  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
   QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
   void* args[] = {&Ap, &lda, &Vptr, &ldv, &tau_dev, &mp, &b, &rpc, &acc, &bar};
   QDWHG_CUDA(cudaLaunchCooperativeKernel((void*)geqr2_panel_kernel<false>, dim3(nblk),
                                          dim3(kPanelThreads), args, panel_smem(rpc), ctx.stream));
   ctx.count();
-  // the register kernels expect zeroed buffers on entry
-  QDWHG_CUDA(cudaMemsetAsync(acc, 0, 3 * 2 * kBW * sizeof(double), ctx.stream));
+  // the register kernels expect a zeroed barrier counter on entry (the atomic
+  // accumulators were not touched: this kernel reduces through the slots)
   QDWHG_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), ctx.stream));
   return false;
 }
@@ -879,12 +916,7 @@ bool panel_factor(Ctx& ctx, const DMat& P, const DMat& Vp, double* tau_dev, doub
 
 // T (b x b, b <= 64) of a compact-WY block from its Gram G = V^T V and taus.
 void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T) {
-  static bool larft_attr = false;
-  if (!larft_attr) {
-    QDWHG_CUDA(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    3 * kBW * (kBW + 1) * 8));
-    larft_attr = true;
-  }
+  func_attr(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kBW * (kBW + 1) * 8);
   launch_pdl(ctx, larft_kernel, dim3(1), dim3(512), (size_t)(3 * kBW * (kBW + 1) * 8), G.ptr(), G.ld,
              tau_dev, T.ptr(), T.ld, (int)G.rows);
   ctx.count();
@@ -911,9 +943,11 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   w.T = ctx.arena->alloc(nbo, nout * nbo);
   fill(ctx, w.T, 0.0, 0.0);
   double* tau_dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 64)));
-  double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 3 * 2 * kBW + 256));
-  unsigned* bar = reinterpret_cast<unsigned*>(acc + 3 * 2 * kBW);  // [0] barrier, [32] ticket
-  QDWHG_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * 3 * 2 * kBW + 256, ctx.stream));
+  // [atomic accumulators | deterministic slots | barrier, ticket]
+  double* acc = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (kAccDoubles + kSlotDoubles) + 256));
+  unsigned* bar = reinterpret_cast<unsigned*>(acc + kAccDoubles + kSlotDoubles);  // [0] barrier, [32] ticket
+  QDWHG_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * kAccDoubles, ctx.stream));
+  QDWHG_CUDA(cudaMemsetAsync(bar, 0, 256, ctx.stream));
   DMat G = ctx.arena->alloc(nbo, nbo);
   static const bool no_la = getenv("QDWHG_QR_NO_LOOKAHEAD") != nullptr;
   const bool lookahead = !no_la && ctx.side != nullptr && n > 2 * nbo;

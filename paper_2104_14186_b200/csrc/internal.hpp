@@ -92,6 +92,18 @@ class Arena {
   size_t high_ = 0;
 };
 
+// Kernel attributes are per device: set once per (device, kernel, attribute,
+// value) under a mutex, so a second handle on another GPU (or another thread)
+// gets its own setting.
+void func_attr(const void* kern, cudaFuncAttribute attr, int value);
+template <typename... KArgs>
+void func_attr(void (*kern)(KArgs...), cudaFuncAttribute attr, int value) {
+  func_attr(reinterpret_cast<const void*>(kern), attr, value);
+}
+
+// Per-device cached probe result (slot < 8): probe() runs once per device.
+int per_device_cached(int slot, int (*probe)());
+
 enum class Op { N, T };
 // Which part of the K range can contribute for an output tile (triangular
 // operands store explicit zeros; skipping them is the TRMM saving).
@@ -110,6 +122,9 @@ struct Ctx {
   // run_fixed_iterations: the factorisations leave the sticky pivot flag for ONE
   // check after the last step (no host round trip per Cholesky step)
   bool defer_pivot_check = false;
+  // bitwise reproducible mode: grid-path QR panels reduce through per-CTA slots
+  // in a fixed order instead of FP64 atomics (qdwhg_set_deterministic)
+  bool deterministic = false;
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
   double* hscratch = nullptr;   // pinned host mirror of dscratch
   int* dflag = nullptr;         // device status flag

@@ -410,11 +410,7 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre
   const int chunk = (int)((n + G - 1) / G);
   const size_t smem = (size_t)(chunk + 96 + (kLzThreads / 32) * chunk) * 8;
   if (smem > 200 * 1024) throw InvalidArgument("lanczos_min_bound: matrix too large");
-  static bool lz_attr = false;
-  if (!lz_attr) {
-    QDWHG_CUDA(cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    lz_attr = true;
-  }
+  func_attr(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   double* wbuf = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * n));
   double* slots = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * G * 64));
   double* bslots = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * 2 * G));

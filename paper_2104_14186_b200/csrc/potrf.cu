@@ -366,12 +366,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
 
 void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, int flags = 0) {
   const size_t smem = (size_t)(128 * kLDA + 64 * kLDT + 128) * 8;
-  static bool set = false;
-  if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-    set = true;
-  }
+  func_attr(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(ctx, potrf_diag_kernel, dim3(1), dim3(kDiagThreads), smem, Zkk.ptr(), Zkk.ld, Wkk.ptr(),
              Wkk.ld, Wikk.ptr(), Wikk.ld, (int)Zkk.rows, ctx.dflag, flags);
   ctx.count();
@@ -460,12 +455,7 @@ __global__ void __launch_bounds__(64) panel_trsm_kernel(const double* Wkk, int64
 void launch_panel_trsm(Ctx& ctx, const DMat& Wkk, const DMat& Zr, const DMat& X) {
   const int b = (int)Wkk.rows, ncols = (int)Zr.rows;
   const size_t smem = ((size_t)b * (b + 1) + (size_t)b * 65) * 8;
-  static bool set = false;
-  if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)((128 * 129 + 128 * 65) * 8)));
-    set = true;
-  }
+  func_attr(panel_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((128 * 129 + 128 * 65) * 8));
   panel_trsm_kernel<<<(ncols + 63) / 64, 64, smem, ctx.stream>>>(Wkk.ptr(), Wkk.ld, Zr.ptr(), Zr.ld,
                                                                 X.ptr(), X.ld, b, ncols);
   QDWHG_CUDA(cudaGetLastError());

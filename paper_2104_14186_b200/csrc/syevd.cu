@@ -421,12 +421,7 @@ size_t inviter_small_smem(int n) { return (size_t)n * (33 + 4 * 32) * sizeof(dou
 
 void inviter_small_launch(Ctx& ctx, const double* dd, const double* ee, int n, const double* wv, int k0,
                           int cnt, double tnorm, double* Z, int64_t ldz) {
-  static bool attr = false;
-  if (!attr) {
-    QDWHG_CUDA(cudaFuncSetAttribute(inviter_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)inviter_small_smem(160)));
-    attr = true;
-  }
+  func_attr(inviter_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inviter_small_smem(160));
   inviter_small_kernel<<<(cnt + 31) / 32, 32, inviter_small_smem(n), ctx.stream>>>(dd, ee, n, wv, k0, cnt,
                                                                                   tnorm, Z, ldz);
   QDWHG_CUDA(cudaGetLastError());
@@ -640,21 +635,11 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   if (!small)  // (Vfull needs no fill: every panel writes its V columns in full)
     QDWHG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * (n + 2 * nb + 8), ctx.stream));  // SYMV atomics
   if (Wp.ld != Vfull.ld) throw CudaError("syev_tridiag: panel V/W leading dimensions differ");
-  static bool trd_attr = false;
-  if (!trd_attr) {
-    QDWHG_CUDA(cudaFuncSetAttribute(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kTrdDynSmem));
-    trd_attr = true;
-  }
+  func_attr(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrdDynSmem);
   if (small) {
-    static bool small_attr = false;
-    if (!small_attr) {
-      QDWHG_CUDA(cudaFuncSetAttribute(sytd2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)sytd2_small_smem(kSmallTrd)));
-      QDWHG_CUDA(cudaFuncSetAttribute(ormtr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)ormtr_small_smem(kSmallTrd, kSmallTrd)));
-      small_attr = true;
-    }
+    func_attr(sytd2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sytd2_small_smem(kSmallTrd));
+    func_attr(ormtr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+              (int)ormtr_small_smem(kSmallTrd, kSmallTrd));
     sytd2_small_kernel<<<1, small_threads(), sytd2_small_smem(n), ctx.stream>>>(S.ptr(), S.ld, n, dd, ee, tau,
                                                                              Vfull.ptr(), Vfull.ld);
     QDWHG_CUDA(cudaGetLastError());

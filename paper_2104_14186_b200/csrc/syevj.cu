@@ -167,14 +167,9 @@ void syev_jacobi(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat&
   const int n = (int)S.rows;
   if (n > kJacobiMax) throw InvalidArgument("syev_jacobi: n exceeds the single-CTA limit");
   const size_t smem = ((size_t)n * (n + 1) + 2 * (kJacobiMax / 2 + 1)) * 8 + 2 * (kJacobiMax / 2 + 1) * 4;
-  static bool set = false;
-  if (!set) {
-    QDWHG_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(((size_t)kJacobiMax * (kJacobiMax + 1) +
-                                           2 * (kJacobiMax / 2 + 1)) * 8 +
-                                          2 * (kJacobiMax / 2 + 1) * 4)));
-    set = true;
-  }
+  func_attr(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            (int)(((size_t)kJacobiMax * (kJacobiMax + 1) + 2 * (kJacobiMax / 2 + 1)) * 8 +
+                  2 * (kJacobiMax / 2 + 1) * 4));
   const Arena::Mark mark = ctx.arena->mark();
   DMat Vt = ctx.arena->alloc(n, n);
   double* ev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 1)));

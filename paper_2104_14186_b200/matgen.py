@@ -98,3 +98,64 @@ def sigma_cut(sig: np.ndarray, k: int) -> float:
 def cut_fraction_s(sig: np.ndarray, k: int, alpha: float) -> float:
     """Relative threshold s = sigma*/alpha for the reference's sigma > s*alpha rule."""
     return sigma_cut(sig, k) / alpha
+
+
+# ------------------------------------------------------------------ device inputs
+def device_input(cfg: int, dev, handle=None) -> dict:
+    """The config's input generated on the GPU through libqdwhg (seeded device
+    Gaussian, our own Householder QR for the orthogonal factors, DMMA GEMMs).
+    The generating handle runs in deterministic mode (QDWHG_FLAG_DETERMINISTIC:
+    fixed-order panel reductions), so the bytes — and input_sha256() — are the
+    same on every run and every B200; the full-size parity fixtures
+    (tests/golden/fullsize/) are keyed by that hash."""
+    import torch
+    from . import qdwh
+    c = dict(CONFIGS[cfg])
+    h = handle if handle is not None else qdwh.Handle(device=dev.index or 0, deterministic=True)
+    if c["kind"] == "eig":
+        n = c["n"]
+        if c["family"] == "wishart":
+            G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=h)
+            A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+            qdwh.gemm(G, G, A, alpha=1.0 / n, trans_a=True, handle=h)
+            del G
+            A -= torch.eye(n, dtype=torch.float64, device=dev)
+            A = (0.5 * (A + A.t())).t().contiguous().t()
+            return dict(A=A, c=c["shift"], k=c["k"], truth=None, kind="eig", cfg=cfg)
+        lam = config_eigenvalues(c["family"], n, c["seed"])
+        G = qdwh.gaussian_matrix_device(n, n, c["seed"], device=dev, handle=h)
+        Q, _ = qdwh.qr_factor(G, handle=h)
+        del G
+        QL = (Q * torch.from_numpy(lam).to(dev)[None, :]).t().contiguous().t()
+        A = torch.empty((n, n), dtype=torch.float64, device=dev).t()
+        qdwh.gemm(QL, Q, A, trans_b=True, handle=h)
+        A = (0.5 * (A + A.t())).t().contiguous().t()
+        k = c["k"]
+        return dict(A=A, c=largest_k_shift(lam, k), k=k, truth=np.sort(lam)[::-1][:k], kind="eig",
+                    cfg=cfg)
+    m, n = c["m"], c["n"]
+    sig = config_singular_values(c["family"], n)
+    Gl = qdwh.gaussian_matrix_device(m, n, c["seed"] ^ LEFT_STREAM, device=dev, handle=h)
+    U = qdwh.qr_factor(Gl, handle=h)[0][:, :n]  # thin Q (first n columns)
+    del Gl
+    Gr = qdwh.gaussian_matrix_device(n, n, c["seed"] ^ RIGHT_STREAM, device=dev, handle=h)
+    V, _ = qdwh.qr_factor(Gr, handle=h)
+    del Gr
+    US = (U * torch.from_numpy(sig).to(dev)[None, :]).t().contiguous().t()
+    del U
+    A = torch.empty((n, m), dtype=torch.float64, device=dev).t()
+    qdwh.gemm(US, V, A, trans_b=True, handle=h)
+    k = c["k"]
+    return dict(A=A, cut=sigma_cut(sig, k), k=k, truth=np.sort(sig)[::-1][:k], kind="svd", cfg=cfg,
+                randomize=bool(c.get("randomize", False)))
+
+
+def host_copy(A) -> np.ndarray:
+    """Column-major host copy (numpy, Fortran order) of a device matrix."""
+    return np.asfortranarray(A.cpu().numpy())
+
+
+def input_sha256(a_host: np.ndarray) -> str:
+    """SHA-256 of the column-major FP64 bytes (the QDWH-file payload order)."""
+    import hashlib
+    return hashlib.sha256(np.asfortranarray(a_host).tobytes(order="F")).hexdigest()

@@ -51,10 +51,10 @@ _STATUS = {1: ValueError, 2: NotPositiveDefinite, 3: NotConverged, 4: CapacityEr
 class Handle:
     """One qdwhg handle (device, stream, workspace arena)."""
 
-    def __init__(self, device: int = -1, arena_bytes: int = 0):
+    def __init__(self, device: int = -1, arena_bytes: int = 0, deterministic: bool = False):
         self.lib = _lib.load()
         self.h = ctypes.c_void_p()
-        opts = _lib.Options(device, 0, arena_bytes, 0)
+        opts = _lib.Options(device, 0, arena_bytes, 1 if deterministic else 0)
         rc = self.lib.qdwhg_create(ctypes.byref(self.h), ctypes.byref(opts))
         if rc != 0:
             raise _STATUS.get(rc, RuntimeError)(f"qdwhg_create failed ({rc})")
@@ -80,6 +80,11 @@ class Handle:
     def own_stream(self):
         """Back to the handle's own (non-blocking) stream."""
         self.check(self.lib.qdwhg_set_stream(self.h, None))
+
+    def set_deterministic(self, enable: bool = True):
+        """Bitwise reproducible mode (QDWHG_FLAG_DETERMINISTIC): tall QR panels
+        reduce across CTAs in a fixed order instead of with FP64 atomics."""
+        self.check(self.lib.qdwhg_set_deterministic(self.h, int(bool(enable))))
 
     def profile(self, enable: bool = True):
         """Bracket every DMMA GEMM launch with CUDA events (live kernel timing)."""

@@ -12,7 +12,7 @@ from paper_2104_14186_b200 import matgen, qdwh
 pytestmark = pytest.mark.gpu
 
 EIG_CASES = ["eig_diag", "eig_spd", "eig_gen256", "eig_gen96_two_step", "eig_gen128_randomized",
-             "eig_cfg1_n256", "eig_cfg2_n384"]
+             "eig_cfg1_n256", "eig_cfg2_n384", "eig_cfg4_wishart_n512", "eig_cfg4_wishart_n1024"]
 SVD_CASES = ["svd_diag", "svd_identity", "svd_gen256", "svd_gen128_qrfirst",
              "svd_gen128_randomized", "svd_cfg3_n256", "svd_cfg5_tall"]
 

@@ -99,7 +99,7 @@ def test_polar_against_reference(name):
 
 
 EIG_CASES = ["eig_diag", "eig_spd", "eig_gen256", "eig_gen96_two_step", "eig_gen128_randomized",
-             "eig_cfg1_n256", "eig_cfg2_n384"]
+             "eig_cfg1_n256", "eig_cfg2_n384", "eig_cfg4_wishart_n512", "eig_cfg4_wishart_n1024"]
 SVD_CASES = ["svd_diag", "svd_identity", "svd_gen256", "svd_gen128_qrfirst",
              "svd_gen128_randomized", "svd_cfg3_n256", "svd_cfg5_tall"]
 
@@ -112,8 +112,9 @@ def test_partial_eig_against_reference(name):
     assert r.count() == len(g["lam"])
     if r.count():
         np.testing.assert_allclose(r.lambda_minus, g["lam"], rtol=1e-10)
-        # same invariant subspace as the reference's V
-        assert np.linalg.norm(r.v @ (r.v.T @ g["v"]) - g["v"]) < 1e-10 * np.sqrt(len(g["lam"]))
+        # same invariant subspace as the reference's V (stored for n <= 512)
+        if g["v"].size:
+            assert np.linalg.norm(r.v @ (r.v.T @ g["v"]) - g["v"]) < 1e-10 * np.sqrt(len(g["lam"]))
     assert abs(r.mu - float(g["mu"])) <= 1e-10 * abs(float(g["mu"]))
     assert r.subspace_size == int(g["subspace_size"])
     assert r.rank_index == int(g["rank_index"])
