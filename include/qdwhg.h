@@ -256,6 +256,36 @@ qdwhg_status qdwhg_subspace_q2(qdwhg_handle* h, int64_t n, double* B, int64_t ld
 qdwhg_status qdwhg_gaussian_matrix(qdwhg_handle* h, int64_t m, int64_t n, uint64_t seed, double* A,
                                    int64_t lda);
 
+/* ---- distributed driver: P x Q grid, 2D block-cyclic nb x nb tiles ------
+ * (PAPER.md:671-686 data layout, Alg. 3).  One rank per GPU,
+ * SPMD: every rank makes the same calls with its own handle.  Communication is
+ * NCCL (panel / diagonal-block broadcasts in the grid's row / column / world
+ * teams, short all-reductions, tile exchanges for transposes and gathers);
+ * libnccl is loaded at run time.  Ranks emulated as threads of one process use
+ * a loopback world instead (tests).  Matrices passed to load / solve are FULL
+ * m x n (host or device; each rank reads only its own tiles).  Results: lambda /
+ * sigma and info on every rank, V / U on rank 0 only (others may pass NULL).
+ * The QR-based first step of partial SVD (s < 1e-3) is single-GPU only. */
+typedef struct qdwhg_dist qdwhg_dist;
+qdwhg_status qdwhg_dist_unique_id(void* id128); /* ncclGetUniqueId (rank 0 shares it) */
+qdwhg_status qdwhg_dist_create_nccl(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                    int32_t rank, const void* id128);
+qdwhg_status qdwhg_dist_world_create(void** world, int32_t nranks);
+qdwhg_status qdwhg_dist_world_destroy(void* world);
+qdwhg_status qdwhg_dist_create_loopback(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                        int32_t rank, void* world);
+qdwhg_status qdwhg_dist_destroy(qdwhg_dist* d);
+qdwhg_status qdwhg_dist_get_stats(const qdwhg_dist* d, uint64_t* collectives, uint64_t* local_gemms);
+/* Keep the rank's tiles of A resident (solves with A == NULL reuse them). */
+qdwhg_status qdwhg_dist_load(qdwhg_dist* d, int64_t m, int64_t n, const double* A, int64_t lda);
+qdwhg_status qdwhg_dist_partial_eig_request(qdwhg_dist* d, int64_t n, const double* A, int64_t lda,
+                                            const qdwhg_eig_request* req, double* lambda, double* V,
+                                            int64_t ldv, int64_t k_cap, qdwhg_eig_info* info);
+qdwhg_status qdwhg_dist_partial_svd_request(qdwhg_dist* d, int64_t m, int64_t n, const double* A, int64_t lda,
+                                            const qdwhg_svd_request* req, double* sigma, double* U,
+                                            int64_t ldu, double* V, int64_t ldv, int64_t k_cap,
+                                            qdwhg_svd_info* info);
+
 /* ---- host scalars (bit-identical to the reference: same libm calls) ---- */
 qdwhg_status qdwhg_halley_weights(double ell, double out5[5]); /* a, b, c, ell_in, ell_out */
 qdwhg_status qdwhg_iterations_to_converge(double ell0, double eps, int64_t max_iters,

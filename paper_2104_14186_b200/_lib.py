@@ -103,6 +103,16 @@ SIGNATURES = {
     "qdwhg_cholesky_inverse_fast": [_P, _I64, _P, _I64, _P, _I64],
     "qdwhg_subspace_q2": [_P, _I64, _P, _I64, _D, _P, _P, _P, _I64, _I64],
     "qdwhg_gaussian_matrix": [_P, _I64, _I64, _U64, _P, _I64],
+    "qdwhg_dist_unique_id": [_P],
+    "qdwhg_dist_create_nccl": [_P, _P, _I32, _I32, _I32, _I32, _P],
+    "qdwhg_dist_world_create": [_P, _I32],
+    "qdwhg_dist_world_destroy": [_P],
+    "qdwhg_dist_create_loopback": [_P, _P, _I32, _I32, _I32, _I32, _P],
+    "qdwhg_dist_destroy": [_P],
+    "qdwhg_dist_get_stats": [_P, _P, _P],
+    "qdwhg_dist_load": [_P, _I64, _I64, _P, _I64],
+    "qdwhg_dist_partial_eig_request": [_P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P],
+    "qdwhg_dist_partial_svd_request": [_P, _I64, _I64, _P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _P],
     "qdwhg_halley_weights": [_D, _P],
     "qdwhg_iterations_to_converge": [_D, _D, _I64, _P],
     "qdwhg_choose_shift": [_I64, _P],

@@ -14,9 +14,11 @@
 #include <mutex>
 #include <set>
 #include <string>
+#include <memory>
 #include <tuple>
 
 #include "../../include/qdwhg.h"
+#include "dist/dist.hpp"
 #include "drivers.hpp"
 
 namespace qdwhg {
@@ -158,27 +160,31 @@ void Ctx::prof_collect() {
   ev_used = 0;
 }
 
-std::vector<double> host_gaussian(int64_t count, uint64_t seed) {
-  // kernels.cpp:16-32 restated (splitmix64 + Box-Muller on counters 2i, 2i+1);
-  // glibc log/cos, so bit-identical to the reference's gaussian_matrix.
-  std::vector<double> out(count);
-  for (int64_t i = 0; i < count; ++i) {
-    auto h = [&](uint64_t c) {
-      uint64_t z = seed + (c + 1) * 0x9E3779B97F4A7C15ull;
-      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-      return z ^ (z >> 31);
-    };
-    const double u1 = static_cast<double>((h(2 * (uint64_t)i) >> 11) + 1) * 0x1.0p-53;
-    const double u2 = static_cast<double>((h(2 * (uint64_t)i + 1) >> 11) + 1) * 0x1.0p-53;
-    out[i] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
-  }
-  return out;
-}
 
 }  // namespace qdwhg
 
 using namespace qdwhg;
+
+namespace qdwhg {
+namespace dist {
+Engine* make_cuda_engine(qdwhg::Ctx& ctx);
+void nccl_unique_id(void* out128);
+Comm* nccl_comm_create(const void* uid128, int rank, int world, const Grid& g, void* stream);
+}  // namespace dist
+}  // namespace qdwhg
+
+// A rank of the distributed driver: its handle (device, stream, arena), the grid
+// position, the communicator and the engine, plus the resident input tiles.
+struct qdwhg_dist {
+  qdwhg_handle* h = nullptr;
+  dist::Grid g;
+  std::unique_ptr<dist::Comm> comm;
+  std::unique_ptr<dist::Engine> eng;
+  dist::Ctx dctx;
+  // resident input (qdwhg_dist_load): persistent allocation, not arena
+  dist::DistMat A;
+  double* a_mem = nullptr;
+};
 
 struct qdwhg_handle {
   int device = 0;
@@ -211,6 +217,9 @@ qdwhg_status guard(qdwhg_handle* h, F&& f) {
   } catch (const qdwhg::CudaError& e) {
     if (h) h->err = e.what();
     return QDWHG_CUDA_ERROR;
+  } catch (const qdwhg::NcclError& e) {
+    if (h) h->err = e.what();
+    return QDWHG_NCCL_ERROR;
   } catch (const std::invalid_argument& e) {
     if (h) h->err = e.what();
     return QDWHG_INVALID_ARGUMENT;
@@ -923,6 +932,271 @@ qdwhg_status qdwhg_iterations_to_converge(double ell0, double eps, int64_t max_i
 
 qdwhg_status qdwhg_choose_shift(int64_t qdwh_iters, double* s) {
   return guard(nullptr, [&] { *s = choose_shift((size_t)qdwh_iters); });
+}
+
+// ------------------------------------------------------------------ distributed driver
+static qdwhg_status dist_init(qdwhg_dist** out, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb, int32_t rank,
+                              const std::function<dist::Comm*(const dist::Grid&)>& mk) {
+  if (!out || !h) return QDWHG_INVALID_ARGUMENT;
+  *out = nullptr;
+  auto* d = new qdwhg_dist();
+  d->h = h;
+  const qdwhg_status st = guard(h, [&] {
+    if (P < 1 || Q < 1 || rank < 0 || rank >= P * Q) throw InvalidArgument("dist: bad grid / rank");
+    if (nb < 32 || nb % 32 != 0) throw InvalidArgument("dist: nb must be a positive multiple of 32");
+    d->g.P = P;
+    d->g.Q = Q;
+    d->g.p = rank / Q;
+    d->g.q = rank % Q;
+    d->g.nb = nb;
+    d->eng.reset(dist::make_cuda_engine(h->ctx));
+    d->comm.reset(mk(d->g));
+    d->dctx.g = d->g;
+    d->dctx.comm = d->comm.get();
+    d->dctx.eng = d->eng.get();
+  });
+  if (st != QDWHG_OK) {
+    delete d;
+    return st;
+  }
+  *out = d;
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_dist_unique_id(void* id128) {
+  if (!id128) return QDWHG_INVALID_ARGUMENT;
+  return guard(nullptr, [&] { dist::nccl_unique_id(id128); });
+}
+
+qdwhg_status qdwhg_dist_create_nccl(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                    int32_t rank, const void* id128) {
+  if (!id128) return QDWHG_INVALID_ARGUMENT;
+  return dist_init(d, h, P, Q, nb, rank, [&](const dist::Grid& g) {
+    return dist::nccl_comm_create(id128, rank, P * Q, g, h->ctx.stream);
+  });
+}
+
+qdwhg_status qdwhg_dist_world_create(void** world, int32_t nranks) {
+  if (!world || nranks < 1) return QDWHG_INVALID_ARGUMENT;
+  *world = dist::loopback_world_create(nranks);
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_dist_world_destroy(void* world) {
+  dist::loopback_world_destroy(static_cast<dist::LoopbackWorld*>(world));
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_dist_create_loopback(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                        int32_t rank, void* world) {
+  if (!world) return QDWHG_INVALID_ARGUMENT;
+  return dist_init(d, h, P, Q, nb, rank, [&](const dist::Grid& g) {
+    qdwhg_handle* hh = h;
+    return dist::loopback_comm_create(
+        static_cast<dist::LoopbackWorld*>(world), rank, g,
+        [hh](void* dst, const void* src, size_t bytes) {
+          QDWHG_CUDA(cudaSetDevice(hh->device));
+          QDWHG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+        },
+        [hh] {
+          QDWHG_CUDA(cudaSetDevice(hh->device));
+          QDWHG_CUDA(cudaStreamSynchronize(hh->ctx.stream));
+        });
+  });
+}
+
+qdwhg_status qdwhg_dist_destroy(qdwhg_dist* d) {
+  if (!d) return QDWHG_OK;
+  cudaSetDevice(d->h->device);
+  cudaStreamSynchronize(d->h->ctx.stream);
+  d->comm.reset();
+  if (d->a_mem) cudaFree(d->a_mem);
+  delete d;
+  return QDWHG_OK;
+}
+
+qdwhg_status qdwhg_dist_get_stats(const qdwhg_dist* d, uint64_t* collectives, uint64_t* local_gemms) {
+  if (!d) return QDWHG_INVALID_ARGUMENT;
+  if (collectives) *collectives = d->dctx.collectives;
+  if (local_gemms) *local_gemms = d->dctx.gemms;
+  return QDWHG_OK;
+}
+
+static void dist_load_impl(qdwhg_dist* d, int64_t m, int64_t n, const double* A, int64_t lda) {
+  if (m < 1 || n < 1 || !A) throw InvalidArgument("dist_load: empty matrix");
+  check_ld(m, lda, "dist_load");
+  dist::DistMat X;
+  X.m = m;
+  X.n = n;
+  X.g = &d->dctx.g;
+  X.lr = dist::numroc(m, d->g.nb, d->g.p, d->g.P);
+  X.lc = dist::numroc(n, d->g.nb, d->g.q, d->g.Q);
+  X.ld = round_ld(std::max<int64_t>(X.lr, 1));
+  const size_t bytes = sizeof(double) * (size_t)X.ld * (size_t)std::max<int64_t>(X.lc, 1);
+  if (d->a_mem && (d->A.ld != X.ld || d->A.lc != X.lc)) {
+    QDWHG_CUDA(cudaFree(d->a_mem));
+    d->a_mem = nullptr;
+  }
+  if (!d->a_mem) QDWHG_CUDA(cudaMalloc(&d->a_mem, bytes));
+  X.a = d->a_mem;
+  d->A = X;
+  dist::scatter_from_full(d->dctx, A, lda, !is_device_ptr(A), d->A);
+}
+
+qdwhg_status qdwhg_dist_load(qdwhg_dist* d, int64_t m, int64_t n, const double* A, int64_t lda) {
+  if (!d) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    dist_load_impl(d, m, n, A, lda);
+    QDWHG_CUDA(cudaStreamSynchronize(d->h->ctx.stream));
+  });
+}
+
+namespace {
+struct DistTimer {
+  cudaEvent_t e0, e1;
+  cudaStream_t s;
+  explicit DistTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  double stop() {
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms * 1e-3;
+  }
+  ~DistTimer() {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+};
+}  // namespace
+
+qdwhg_status qdwhg_dist_partial_eig_request(qdwhg_dist* d, int64_t n, const double* A, int64_t lda,
+                                            const qdwhg_eig_request* req, double* lambda, double* V,
+                                            int64_t ldv, int64_t k_cap, qdwhg_eig_info* info) {
+  if (!d || !req) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    qdwhg_eig_info tmp{};
+    qdwhg_eig_info* inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    Ctx& ctx = d->h->ctx;
+    DistTimer tm(ctx.stream);
+    if (A) dist_load_impl(d, n, n, A, lda);
+    if (!d->a_mem || d->A.m != n || d->A.n != n) throw InvalidArgument("dist eig: no loaded n x n matrix");
+    const int iters = req->iters ? req->iters : 3;
+    const double s = choose_shift((size_t)iters);
+    const double tol = req->tol > 0 ? req->tol : 0.01;
+    dist::Ctx& dc = d->dctx;
+    // working copy with the shift map: B = cI - A / A - cI / A
+    dist::DistMat B = dist::make_dist(*d->eng, dc.g, n, n);
+    if (req->which == QDWHG_LARGEST) dist::axpby_identity(dc, &d->A, -1.0, B, 0.0, req->c);
+    else if (req->which == QDWHG_SMALLEST) dist::axpby_identity(dc, &d->A, 1.0, B, 0.0, -req->c);
+    else if (req->which == QDWHG_NEGATIVE) dist::axpby_identity(dc, &d->A, 1.0, B, 0.0, 0.0);
+    else throw InvalidArgument("eig_request: unknown 'which'");
+    dist::EigResult r = dist::partial_eig(dc, B, s, (size_t)iters, req->randomize != 0, tol, req->seed);
+    const double c = (req->which == QDWHG_NEGATIVE) ? 0.0 : req->c;
+    const int64_t kf = (int64_t)r.lambda.size();
+    int64_t k = kf;
+    if (req->k > 0) k = std::min<int64_t>(k, req->k);
+    if (k > k_cap) throw CapacityError("k exceeds k_cap");
+    std::vector<double> lam(k);
+    for (int64_t i = 0; i < k; ++i)
+      lam[i] = (req->which == QDWHG_LARGEST) ? c - r.lambda[i]
+               : (req->which == QDWHG_SMALLEST) ? c + r.lambda[i] : r.lambda[i];
+    if (k > 0) {
+      copy_vec_out(ctx, lam, lambda);
+      if (r.V && V) {
+        check_ld(n, ldv, "V");
+        DMat Vd;
+        Vd.base = r.V;
+        Vd.ld = r.vld;
+        Vd.rows = n;
+        Vd.cols = k;
+        stage_out(ctx, Vd, V, ldv);
+      }
+    }
+    inf->seconds = tm.stop();
+    inf->mu = r.mu;
+    inf->shift = s;
+    inf->tol = tol;
+    inf->c_shift = c;
+    inf->rank_index = (int64_t)r.rank_index;
+    inf->subspace_size = (int64_t)r.subspace_size;
+    inf->k = k;
+    inf->k_found = kf;
+    inf->iters_chol = (int64_t)r.iters_chol;
+    inf->borderline = (int64_t)r.borderline;
+    inf->no_savings = r.no_savings;
+    inf->randomized = req->randomize != 0;
+    inf->flops = r.flops;
+    fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
+}
+
+qdwhg_status qdwhg_dist_partial_svd_request(qdwhg_dist* d, int64_t m, int64_t n, const double* A, int64_t lda,
+                                            const qdwhg_svd_request* req, double* sigma, double* U, int64_t ldu,
+                                            double* V, int64_t ldv, int64_t k_cap, qdwhg_svd_info* info) {
+  if (!d || !req) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    qdwhg_svd_info tmp{};
+    qdwhg_svd_info* inf = info ? info : &tmp;
+    std::memset(inf, 0, sizeof(*inf));
+    Ctx& ctx = d->h->ctx;
+    DistTimer tm(ctx.stream);
+    if (A) dist_load_impl(d, m, n, A, lda);
+    if (!d->a_mem || d->A.m != m || d->A.n != n) throw InvalidArgument("dist svd: no loaded m x n matrix");
+    const double tol = req->tol > 0 ? req->tol : 0.01;
+    double s = 0.0, s_abs = 0.0;
+    if (req->mode == 0) s = req->value;
+    else if (req->mode == 1) s_abs = req->value;
+    else throw InvalidArgument("svd_request: unknown mode");
+    if (req->mode == 1 && !(s_abs > 0.0)) throw InvalidArgument("svd_request: cut must be positive");
+    dist::SvdResult r = dist::partial_svd(d->dctx, d->A, s, s_abs, tol, req->randomize != 0, req->seed);
+    const int64_t kf = (int64_t)r.sigma.size();
+    int64_t k = kf;
+    if (req->k > 0) k = std::min<int64_t>(k, req->k);
+    if (k > k_cap) throw CapacityError("k exceeds k_cap");
+    if (k > 0) {
+      std::vector<double> sg(r.sigma.begin(), r.sigma.begin() + k);
+      copy_vec_out(ctx, sg, sigma);
+      if (r.U && U) {
+        check_ld(m, ldu, "U");
+        DMat Ud;
+        Ud.base = r.U;
+        Ud.ld = r.uld;
+        Ud.rows = m;
+        Ud.cols = k;
+        stage_out(ctx, Ud, U, ldu);
+      }
+      if (r.V && V) {
+        check_ld(n, ldv, "V");
+        DMat Vd;
+        Vd.base = r.V;
+        Vd.ld = r.vld;
+        Vd.rows = n;
+        Vd.cols = k;
+        stage_out(ctx, Vd, V, ldv);
+      }
+    }
+    inf->seconds = tm.stop();
+    inf->alpha = r.alpha;
+    inf->threshold = r.threshold;
+    inf->tol = tol;
+    inf->cut = r.threshold * r.alpha;
+    inf->rank_index = (int64_t)r.rank_index;
+    inf->subspace_size = (int64_t)r.subspace_size;
+    inf->k = k;
+    inf->k_found = kf;
+    inf->iters_qr = (int64_t)r.iters_qr;
+    inf->iters_chol = (int64_t)r.iters_chol;
+    inf->no_savings = r.no_savings;
+    inf->randomized = req->randomize != 0;
+    inf->flops = r.flops;
+    fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
 }
 
 }  // extern "C"

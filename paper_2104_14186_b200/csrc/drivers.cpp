@@ -16,41 +16,6 @@ extern const int kJacobiMaxN;
 void syev_jacobi(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout);
 void permute_cols(Ctx& ctx, const DMat& V, const std::vector<int>& order, const DMat& Vout);
 
-// ----------------------------------------------------------------- scalars
-WeightStep halley_weights(double ell) {  // polar.cpp:12-27 (same libm calls, same order)
-  if (!(ell > 0.0) || ell > 1.0) throw InvalidArgument("halley_weights: ell must be in (0, 1]");
-  const double l2 = ell * ell;
-  const double dd = std::cbrt(4.0 * (1.0 - l2)) * std::pow(ell, -4.0 / 3.0);
-  const double sqd = std::sqrt(1.0 + dd);
-  const double inner = 8.0 - 4.0 * dd + 8.0 * (2.0 - l2) / (l2 * sqd);
-  WeightStep w;
-  w.a = sqd + std::sqrt(inner) / 2.0;
-  w.b = (w.a - 1.0) * (w.a - 1.0) / 4.0;
-  w.c = w.a + w.b - 1.0;
-  w.ell_in = ell;
-  w.ell_out = ell * (w.a + w.b * l2) / (1.0 + w.c * l2);
-  return w;
-}
-
-size_t iterations_to_converge(double ell0, double eps, size_t max_iters) {  // polar.cpp:40-51
-  double ell = ell0;
-  for (size_t k = 0; k < max_iters; ++k) {
-    if (std::abs(ell - 1.0) < eps) return k;
-    ell = halley_weights(ell).ell_out;
-  }
-  if (std::abs(ell - 1.0) < eps) return max_iters;
-  std::ostringstream msg;
-  msg << "ell recurrence from " << ell0 << " not within " << eps << " of 1 after " << max_iters
-      << " steps (ell = " << ell << ")";
-  throw NotConverged(msg.str());
-}
-
-double choose_shift(size_t iters) {  // partial.cpp:26-30
-  if (iters == 2) return 0.875;
-  if (iters == 3) return 0.2;
-  throw InvalidArgument("choose_shift: unsupported plan, tabulated iteration counts are 2 and 3");
-}
-
 // ----------------------------------------------------------------- stage clock
 StageClock::StageClock(Ctx& c) : ctx(c) {
   cudaEvent_t e;

@@ -7,16 +7,10 @@
 #include <vector>
 
 #include "internal.hpp"
+#include "scalars.hpp"
 
 namespace qdwhg {
 
-// polar.cpp:12-27 / 29-38 / 40-51, partial.cpp:26-30 (host scalars)
-struct WeightStep {
-  double a, b, c, ell_in, ell_out;
-};
-WeightStep halley_weights(double ell);
-size_t iterations_to_converge(double ell0, double eps, size_t max_iters = 60);
-double choose_shift(size_t iters);  // returns s
 
 struct StageClock {
   explicit StageClock(Ctx& c);

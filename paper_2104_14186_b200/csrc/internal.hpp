@@ -9,8 +9,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "errors.hpp"
+
 #include <cstdint>
 #include <functional>
+#include <mutex>
 #include <cstdlib>
 #include <utility>
 #include <stdexcept>
@@ -19,21 +22,6 @@
 
 namespace qdwhg {
 
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct InvalidArgument : std::invalid_argument {
-  using std::invalid_argument::invalid_argument;
-};
-struct NotPositiveDefinite : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct NotConverged : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct CapacityError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
 
 #define QDWHG_CUDA(expr)                                                                   \
   do {                                                                                     \
@@ -205,6 +193,26 @@ MatStats mat_stats(Ctx& ctx, const DMat& X, bool want_asym);
 void gaussian_fill(Ctx& ctx, const DMat& X, uint64_t seed);
 void mirror_lower_to_upper(Ctx& ctx, const DMat& X);
 void zero_strict_lower(Ctx& ctx, const DMat& X);
+
+// ------------------------------------------------------------------ tiles.cu
+// (local-array kernels of the distributed driver)
+struct TileDesc {
+  const double* src;
+  int64_t lds;
+  double* dst;
+  int64_t ldd;
+  int32_t rows, cols;  // of src
+  int32_t trans;       // dst (cols x rows) = src^T
+};
+void copy_tiles(Ctx& ctx, const std::vector<TileDesc>& list);
+// Y = a X + b Y (X may be null: Y = b Y; b == 0: Y is not read)
+void axpby(Ctx& ctx, const double* X, int64_t ldx, double* Y, int64_t ldy, int64_t m, int64_t n, double a,
+           double b);
+void add_diag(Ctx& ctx, double* Y, int64_t ld, int64_t len, double v);
+void zero_strict_upper(Ctx& ctx, const DMat& X);
+// entries (gr0 + i, gc0 + j) of the gm-row matrix of gaussian_fill's stream
+void gaussian_fill_at(Ctx& ctx, double* X, int64_t ld, int64_t m, int64_t n, uint64_t seed, int64_t gr0,
+                      int64_t gc0, int64_t gm);
 
 // ------------------------------------------------------------------ potrf.cu
 // Z = W^T W with W upper; only the lower triangle of Z is read (it is used as

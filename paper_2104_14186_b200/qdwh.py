@@ -419,6 +419,130 @@ def partial_svd_request(a, cut: Optional[float] = None, s: Optional[float] = Non
     return _svd_result(info, sig, U, V, info.k)
 
 
+# ------------------------------------------------------------------ distributed driver
+class LoopbackWorld:
+    """In-process world for ranks emulated as threads (tests; qdwhg_dist_world_create)."""
+
+    def __init__(self, nranks: int):
+        self.lib = _lib.load()
+        self.w = ctypes.c_void_p()
+        if self.lib.qdwhg_dist_world_create(ctypes.byref(self.w), int(nranks)) != 0:
+            raise RuntimeError("qdwhg_dist_world_create failed")
+
+    def close(self):
+        if self.w:
+            self.lib.qdwhg_dist_world_destroy(self.w)
+            self.w = ctypes.c_void_p()
+
+
+def dist_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it and shares it, e.g. over torch.distributed)."""
+    lib = _lib.load()
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.qdwhg_dist_unique_id(buf)
+    if rc != 0:
+        raise _STATUS.get(rc, RuntimeError)("qdwhg_dist_unique_id failed")
+    return buf.raw
+
+
+class Dist:
+    """One rank of the distributed QDWHpartial driver (P x Q grid, 2D block-cyclic
+    nb x nb tiles; include/qdwhg.h qdwhg_dist_*).  Every rank calls the same
+    methods with its own Handle.  Results: values on every rank, vectors on
+    rank 0 (None elsewhere)."""
+
+    def __init__(self, handle: Handle, P: int, Q: int, nb: int = 512, rank: int = 0, *,
+                 unique_id: Optional[bytes] = None, world: Optional[LoopbackWorld] = None):
+        self.h = handle
+        self.lib = handle.lib
+        self.P, self.Q, self.nb, self.rank = P, Q, nb, rank
+        self.d = ctypes.c_void_p()
+        if world is not None:
+            rc = self.lib.qdwhg_dist_create_loopback(ctypes.byref(self.d), handle.h, P, Q, nb, rank, world.w)
+        else:
+            if unique_id is None:
+                raise ValueError("Dist: unique_id (NCCL) or world (loopback) required")
+            self._uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+            rc = self.lib.qdwhg_dist_create_nccl(ctypes.byref(self.d), handle.h, P, Q, nb, rank, self._uid)
+        handle.check(rc)
+        self._kind = None  # (device, torch device) of the loaded matrix
+
+    def close(self):
+        if self.d:
+            self.lib.qdwhg_dist_destroy(self.d)
+            self.d = ctypes.c_void_p()
+
+    def stats(self) -> dict:
+        c, g = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        self.h.check(self.lib.qdwhg_dist_get_stats(self.d, ctypes.byref(c), ctypes.byref(g)))
+        return dict(collectives=c.value, local_gemms=g.value)
+
+    def load(self, a):
+        """Keep this rank's tiles of the full matrix a resident (host or device)."""
+        A = _Mat(a)
+        self._kind = A
+        self.h.check(self.lib.qdwhg_dist_load(self.d, A.shape[0], A.shape[1], A.ptr, A.ld))
+
+    def _out(self, ref, m, n):
+        return _empty_like_kind(ref, m, n) if self.rank == 0 else None
+
+    def partial_eig_request(self, a=None, which: str = "largest", c: float = 0.0, k: int = 0, iters: int = 3,
+                            tol: float = 0.01, use_randomization: bool = False, seed: int = 0, *,
+                            n: Optional[int] = None, k_cap: Optional[int] = None) -> "PartialEigResult":
+        A = _Mat(a) if a is not None else None
+        ref = A if A is not None else self._kind
+        if ref is None:
+            raise ValueError("no matrix: pass a or load() one")
+        nn = ref.shape[0] if n is None else n
+        which_id = {"negative": 0, "largest": 1, "smallest": 2}[which]
+        kc = (k if k > 0 else nn) if k_cap is None else k_cap
+        lam = np.zeros(max(kc, 1))
+        V = self._out(ref, nn, max(kc, 1))
+        vp, ldv = _ptr_ld(V) if V is not None else (None, 1)
+        req = _lib.EigRequest(which_id, iters, float(c), int(k), float(tol), int(bool(use_randomization)),
+                              0, int(seed) & (2**64 - 1))
+        info = _lib.EigInfo()
+        self.h.check(self.lib.qdwhg_dist_partial_eig_request(
+            self.d, nn, A.ptr if A is not None else None, A.ld if A is not None else 0, ctypes.byref(req),
+            lam.ctypes.data, vp, ldv, kc, ctypes.byref(info)))
+        if A is not None:
+            self._kind = A
+        return _eig_result(info, lam, V if V is not None else np.zeros((0, max(kc, 1))), info.k)
+
+    def partial_svd_request(self, a=None, cut: Optional[float] = None, s: Optional[float] = None, k: int = 0,
+                            tol: float = 0.01, use_randomization: bool = False, seed: int = 0, *,
+                            shape=None, k_cap: Optional[int] = None) -> "PartialSvdResult":
+        A = _Mat(a) if a is not None else None
+        ref = A if A is not None else self._kind
+        if ref is None:
+            raise ValueError("no matrix: pass a or load() one")
+        m, n = ref.shape if shape is None else shape
+        if (cut is None) == (s is None):
+            raise ValueError("give exactly one of cut / s")
+        req = _lib.SvdRequest(1 if cut is not None else 0, int(bool(use_randomization)),
+                              float(cut if cut is not None else s), int(k), float(tol), int(seed) & (2**64 - 1))
+        kc = (k if k > 0 else n) if k_cap is None else k_cap
+        sig = np.zeros(max(kc, 1))
+        U = self._out(ref, m, max(kc, 1))
+        V = self._out(ref, n, max(kc, 1))
+        up, ldu = _ptr_ld(U) if U is not None else (None, 1)
+        vp, ldv = _ptr_ld(V) if V is not None else (None, 1)
+        info = _lib.SvdInfo()
+        self.h.check(self.lib.qdwhg_dist_partial_svd_request(
+            self.d, m, n, A.ptr if A is not None else None, A.ld if A is not None else 0, ctypes.byref(req),
+            sig.ctypes.data, up, ldu, vp, ldv, kc, ctypes.byref(info)))
+        if A is not None:
+            self._kind = A
+        z = np.zeros((0, max(kc, 1)))
+        return _svd_result(info, sig, U if U is not None else z, V if V is not None else z, info.k)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class PolarConfig:
     """polar.hpp:34-40"""
