@@ -286,6 +286,18 @@ qdwhg_status qdwhg_dist_partial_svd_request(qdwhg_dist* d, int64_t m, int64_t n,
                                             int64_t ldu, double* V, int64_t ldv, int64_t k_cap,
                                             qdwhg_svd_info* info);
 
+/* Distributed building blocks on FULL operands (every rank passes its copy; the
+ * result is gathered to rank 0): pgemm (flags: 1 op(A) upper, 2 op(A) lower,
+ * 4 op(B) upper, 8 op(B) lower, 16 only C's lower tiles), the recursive
+ * Cholesky-and-inverse, and Householder QR |diag R| + Q(:, c0:c0+ell). */
+qdwhg_status qdwhg_dist_pgemm(qdwhg_dist* d, int32_t ta, int32_t tb, int64_t m, int64_t n, int64_t k, double alpha,
+                              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                              const double* C0, int64_t ldc0, double* C, int64_t ldc, int32_t flags);
+qdwhg_status qdwhg_dist_cholesky_inverse(qdwhg_dist* d, int64_t n, const double* Z, int64_t ldz, double* Winv,
+                                         int64_t ldwi);
+qdwhg_status qdwhg_dist_qr(qdwhg_dist* d, int64_t m, int64_t n, const double* X, int64_t ldx, int64_t c0,
+                           int64_t ell, double* rdiag, double* Q2, int64_t ldq);
+
 /* ---- host scalars (bit-identical to the reference: same libm calls) ---- */
 qdwhg_status qdwhg_halley_weights(double ell, double out5[5]); /* a, b, c, ell_in, ell_out */
 qdwhg_status qdwhg_iterations_to_converge(double ell0, double eps, int64_t max_iters,

@@ -113,6 +113,10 @@ SIGNATURES = {
     "qdwhg_dist_load": [_P, _I64, _I64, _P, _I64],
     "qdwhg_dist_partial_eig_request": [_P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P],
     "qdwhg_dist_partial_svd_request": [_P, _I64, _I64, _P, _I64, _P, _P, _P, _I64, _P, _I64, _I64, _P],
+    "qdwhg_dist_pgemm": [_P, _I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _P, _I64,
+                         _I32],
+    "qdwhg_dist_cholesky_inverse": [_P, _I64, _P, _I64, _P, _I64],
+    "qdwhg_dist_qr": [_P, _I64, _I64, _P, _I64, _I64, _I64, _P, _P, _I64],
     "qdwhg_halley_weights": [_D, _P],
     "qdwhg_iterations_to_converge": [_D, _D, _I64, _P],
     "qdwhg_choose_shift": [_I64, _P],

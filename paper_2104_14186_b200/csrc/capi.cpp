@@ -995,8 +995,12 @@ qdwhg_status qdwhg_dist_create_loopback(qdwhg_dist** d, qdwhg_handle* h, int32_t
     return dist::loopback_comm_create(
         static_cast<dist::LoopbackWorld*>(world), rank, g,
         [hh](void* dst, const void* src, size_t bytes) {
+          // on the rank's own stream, then waited for: a plain cudaMemcpy from
+          // pageable memory may return before the DMA lands, and the rank's
+          // non-blocking stream would not be ordered after it
           QDWHG_CUDA(cudaSetDevice(hh->device));
-          QDWHG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+          QDWHG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, hh->ctx.stream));
+          QDWHG_CUDA(cudaStreamSynchronize(hh->ctx.stream));
         },
         [hh] {
           QDWHG_CUDA(cudaSetDevice(hh->device));
@@ -1196,6 +1200,79 @@ qdwhg_status qdwhg_dist_partial_svd_request(qdwhg_dist* d, int64_t m, int64_t n,
     inf->randomized = req->randomize != 0;
     inf->flops = r.flops;
     fill_trace(r.trace, &inf->n_trace, inf->ell_trace);
+  });
+}
+
+
+// ---- distributed building blocks on full matrices (every rank passes the full
+// operands; results gathered to rank 0) — the distributed analogues of
+// qdwhg_gemm_ex / qdwhg_cholesky_inverse_fast / qdwhg_subspace_q2
+namespace {
+dist::DistMat dist_scratch(qdwhg_dist* d, int64_t m, int64_t n, const double* full, int64_t ld) {
+  dist::DistMat X = dist::make_dist(*d->eng, d->dctx.g, m, n);
+  if (full) dist::scatter_from_full(d->dctx, full, ld, !is_device_ptr(full), X);
+  return X;
+}
+void dist_gather_out(qdwhg_dist* d, const dist::DistMat& X, double* out, int64_t ldo) {
+  const bool root = d->g.p == 0 && d->g.q == 0;
+  double* dst = nullptr;
+  int64_t ldd = 0;
+  if (root) dst = d->eng->alloc(X.m, X.n, &ldd);
+  dist::gather(d->dctx, X, dst, ldd, 0);
+  if (root && out) {
+    DMat v;
+    v.base = dst;
+    v.ld = ldd;
+    v.rows = X.m;
+    v.cols = X.n;
+    stage_out(d->h->ctx, v, out, ldo);
+    QDWHG_CUDA(cudaStreamSynchronize(d->h->ctx.stream));
+  }
+}
+}  // namespace
+
+qdwhg_status qdwhg_dist_pgemm(qdwhg_dist* d, int32_t ta, int32_t tb, int64_t m, int64_t n, int64_t k, double alpha,
+                              const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                              const double* C0, int64_t ldc0, double* C, int64_t ldc, int32_t flags) {
+  if (!d) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    dist::DistMat Am = dist_scratch(d, ta ? k : m, ta ? m : k, A, lda);
+    dist::DistMat Bm = dist_scratch(d, tb ? n : k, tb ? k : n, B, ldb);
+    dist::DistMat Cm = dist_scratch(d, m, n, C0, ldc0);
+    dist::Structure st;
+    st.a_upper = flags & 1;
+    st.a_lower = flags & 2;
+    st.b_upper = flags & 4;
+    st.b_lower = flags & 8;
+    st.c_lower = flags & 16;
+    dist::pgemm(d->dctx, ta != 0, tb != 0, alpha, dist::whole(Am), dist::whole(Bm), beta, dist::whole(Cm), st);
+    dist_gather_out(d, Cm, C, ldc);
+  });
+}
+
+qdwhg_status qdwhg_dist_cholesky_inverse(qdwhg_dist* d, int64_t n, const double* Z, int64_t ldz, double* Winv,
+                                         int64_t ldwi) {
+  if (!d) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    dist::DistMat Zm = dist_scratch(d, n, n, Z, ldz);
+    dist::DistMat Wm = dist_scratch(d, n, n, nullptr, 0);
+    dist::chol_inv(d->dctx, Zm, Wm);
+    dist_gather_out(d, Wm, Winv, ldwi);
+  });
+}
+
+qdwhg_status qdwhg_dist_qr(qdwhg_dist* d, int64_t m, int64_t n, const double* X, int64_t ldx, int64_t c0,
+                           int64_t ell, double* rdiag, double* Q2, int64_t ldq) {
+  if (!d) return QDWHG_INVALID_ARGUMENT;
+  return guard(d->h, [&] {
+    if (c0 < 0 || ell < 1 || c0 + ell > m) throw InvalidArgument("dist_qr: bad column range");
+    dist::DistMat Xm = dist_scratch(d, m, n, X, ldx);
+    dist::QrDist qr;
+    dist::pgeqrf(d->dctx, Xm, qr);
+    dist::DistMat Qm = dist_scratch(d, m, ell, nullptr, 0);
+    dist::porgqr_cols(d->dctx, qr, c0, Qm);
+    dist_gather_out(d, Qm, Q2, ldq);
+    if (rdiag) std::memcpy(rdiag, qr.rdiag.data(), sizeof(double) * (size_t)n);
   });
 }
 

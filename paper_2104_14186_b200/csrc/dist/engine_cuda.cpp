@@ -5,6 +5,7 @@
 // asynchronous on the handle's stream except the host reads (dot, stats, QR
 // diagonal, eigen/singular values).
 #include <cmath>
+#include <cstdio>
 
 #include "../drivers.hpp"
 #include "../internal.hpp"
@@ -33,10 +34,19 @@ class CudaEngine : public Engine {
   double* alloc(int64_t rows, int64_t cols, int64_t* ld) override {
     DMat d = c_.arena->alloc(std::max<int64_t>(rows, 1), std::max<int64_t>(cols, 1));
     *ld = d.ld;
+    if (poison()) qdwhg::fill(c_, view(d.base, d.ld, d.ld, d.cols), NAN, 0.0);
     return d.base;
   }
   double* alloc_vec(size_t count) override {
-    return static_cast<double*>(c_.arena->alloc_bytes(sizeof(double) * std::max<size_t>(count, 1)));
+    double* p = static_cast<double*>(c_.arena->alloc_bytes(sizeof(double) * std::max<size_t>(count, 1)));
+    if (poison()) qdwhg::fill(c_, view(p, (int64_t)count, (int64_t)count, 1), NAN, 0.0);
+    return p;
+  }
+  // QDWHG_DIST_POISON: every workspace allocation starts as NaN (debug: a read of
+  // memory the driver never wrote shows up as a non-finite result)
+  static bool poison() {
+    static const bool on = getenv("QDWHG_DIST_POISON") != nullptr;
+    return on;
   }
   EMark mark() override {
     const Arena::Mark m = c_.arena->mark();
@@ -54,7 +64,38 @@ class CudaEngine : public Engine {
     }
     const DMat Av = ta ? view(A, lda, k, m) : view(A, lda, m, k);
     const DMat Bv = tb ? view(B, ldb, n, k) : view(B, ldb, k, n);
+    static const bool verify = getenv("QDWHG_DIST_VERIFY") != nullptr;
+    std::vector<double> ha, hb, hc;
+    if (verify) {
+      ha = host(A, lda, ta ? k : m, ta ? m : k);
+      hb = host(B, ldb, tb ? n : k, tb ? k : n);
+      hc = host(C, ldc, m, n);
+    }
     qdwhg::gemm(c_, ta ? Op::T : Op::N, tb ? Op::T : Op::N, alpha, Av, Bv, beta, view(C, ldc, m, n));
+    if (verify) {
+      const std::vector<double> got = host(C, ldc, m, n);
+      double err = 0, scale = 1e-300;
+      for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) {
+          double acc = 0;
+          for (int64_t p = 0; p < k; ++p)
+            acc += (ta ? ha[p + i * k] : ha[i + p * m]) * (tb ? hb[j + p * n] : hb[p + j * k]);
+          const double want = alpha * acc + (beta == 0.0 ? 0.0 : beta * hc[i + j * m]);
+          err = std::max(err, std::abs(got[i + j * m] - want));
+          scale = std::max(scale, std::abs(want));
+        }
+      if (!(err <= 1e-11 * scale * std::max<int64_t>(k, 1)))
+        fprintf(stderr, "DIST_VERIFY gemm mismatch ta=%d tb=%d m=%ld n=%ld k=%ld lda=%ld ldb=%ld ldc=%ld "
+                        "alpha=%g beta=%g A=%p B=%p C=%p err=%.3e scale=%.3e\n",
+                (int)ta, (int)tb, (long)m, (long)n, (long)k, (long)lda, (long)ldb, (long)ldc, alpha, beta,
+                (const void*)A, (const void*)B, (void*)C, err, scale);
+    }
+  }
+  std::vector<double> host(const double* p, int64_t ld, int64_t rows, int64_t cols) {
+    std::vector<double> h((size_t)(rows * cols));
+    QDWHG_CUDA(cudaMemcpy2DAsync(h.data(), rows * 8, p, ld * 8, rows * 8, cols, cudaMemcpyDefault, c_.stream));
+    QDWHG_CUDA(cudaStreamSynchronize(c_.stream));
+    return h;
   }
   void copy_tiles(const std::vector<TileCopy>& list) override {
     std::vector<TileDesc> d;

@@ -536,6 +536,35 @@ class Dist:
         z = np.zeros((0, max(kc, 1)))
         return _svd_result(info, sig, U if U is not None else z, V if V is not None else z, info.k)
 
+    # ---- distributed building blocks on full host operands (result on rank 0)
+    def pgemm(self, a, b, c0=None, alpha=1.0, beta=0.0, trans_a=False, trans_b=False, flags=0):
+        A, B = np.asfortranarray(a, dtype=np.float64), np.asfortranarray(b, dtype=np.float64)
+        m = A.shape[1] if trans_a else A.shape[0]
+        k = A.shape[0] if trans_a else A.shape[1]
+        n = B.shape[0] if trans_b else B.shape[1]
+        C0 = np.asfortranarray(c0 if c0 is not None else np.zeros((m, n)), dtype=np.float64)
+        out = np.zeros((m, n), order="F")
+        self.h.check(self.lib.qdwhg_dist_pgemm(self.d, int(trans_a), int(trans_b), m, n, k, float(alpha),
+                                               A.ctypes.data, A.shape[0], B.ctypes.data, B.shape[0], float(beta),
+                                               C0.ctypes.data, m, out.ctypes.data, m, int(flags)))
+        return out if self.rank == 0 else None
+
+    def cholesky_inverse(self, z):
+        Z = np.asfortranarray(z, dtype=np.float64)
+        n = Z.shape[0]
+        out = np.zeros((n, n), order="F")
+        self.h.check(self.lib.qdwhg_dist_cholesky_inverse(self.d, n, Z.ctypes.data, n, out.ctypes.data, n))
+        return out if self.rank == 0 else None
+
+    def qr(self, x, c0, ell):
+        X = np.asfortranarray(x, dtype=np.float64)
+        m, n = X.shape
+        rd = np.zeros(n)
+        q2 = np.zeros((m, ell), order="F")
+        self.h.check(self.lib.qdwhg_dist_qr(self.d, m, n, X.ctypes.data, m, int(c0), int(ell), rd.ctypes.data,
+                                            q2.ctypes.data, m))
+        return rd, (q2 if self.rank == 0 else None)
+
     def __del__(self):
         try:
             self.close()

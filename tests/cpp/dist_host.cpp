@@ -311,6 +311,8 @@ class HostEngine : public Engine {
  private:
   double* push(size_t count) {
     bufs_.emplace_back(new double[count]());
+    if (getenv("QDWHG_DIST_POISON"))
+      for (size_t i = 0; i < count; ++i) bufs_.back()[i] = NAN;
     return bufs_.back().get();
   }
   std::vector<std::unique_ptr<double[]>> bufs_;

@@ -44,6 +44,45 @@ def run_grid(P, Q, nb, body):
     return out
 
 
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2)])
+@pytest.mark.parametrize("ta,tb,flags", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0), (0, 0, 1), (0, 0, 4),
+                                         (0, 1, 1 | 8 | 16), (1, 0, 16)])
+def test_emulated_pgemm(P, Q, ta, tb, flags):
+    rng = np.random.default_rng(7)
+    n, nb = 1536, 256
+    U = np.triu(rng.standard_normal((n, n)))
+    X = rng.standard_normal((n, n))
+    A = U if flags & 1 else X
+    B = U if flags & 4 or flags & 8 else rng.standard_normal((n, n))
+    C0 = rng.standard_normal((n, n))
+    res = run_grid(P, Q, nb, lambda d, r: d.pgemm(A, B, C0, 0.5, -1.0, ta, tb, flags))
+    want = 0.5 * (A.T if ta else A) @ (B.T if tb else B) - C0
+    got = res[0]
+    if flags & 16:
+        tl = np.kron(np.tril(np.ones((n // nb, n // nb))), np.ones((nb, nb))).astype(bool)
+        np.testing.assert_allclose(got[tl], want[tl], rtol=1e-10, atol=1e-10)
+    else:
+        np.testing.assert_allclose(got, want, rtol=1e-10, atol=1e-10)
+
+
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2)])
+def test_emulated_chol_inv_and_qr(P, Q):
+    rng = np.random.default_rng(11)
+    n, nb = 1536, 256
+    X = rng.standard_normal((n, n)) / np.sqrt(n)
+    Z = np.eye(n) + 3.0 * X.T @ X
+    res = run_grid(P, Q, nb, lambda d, r: d.cholesky_inverse(Z))
+    W = np.linalg.cholesky(Z).T
+    np.testing.assert_allclose(res[0], np.linalg.inv(W), rtol=1e-9, atol=1e-11)
+    c0, ell = 1000, 536
+    res = run_grid(P, Q, nb, lambda d, r: d.qr(X, c0, ell))
+    q, r = np.linalg.qr(X, mode="complete")
+    for rd, _ in res:
+        np.testing.assert_allclose(rd, np.abs(np.diag(r)), rtol=1e-9)
+    q2 = res[0][1]
+    np.testing.assert_allclose(np.abs(q2), np.abs(q[:, c0:c0 + ell]), atol=1e-10)
+
+
 def planted(n, family, k, seed=42):
     lam = matgen.config_eigenvalues(family, n, seed)
     q, _ = np.linalg.qr(O.gaussian_matrix(n, n, seed))
