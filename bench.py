@@ -19,8 +19,9 @@ scan, Q2 formation, Rayleigh-Ritz, back-transform) through libqdwhg.
 
 --impl reference runs the reference's own CPU implementation on the host
 cores (one single-threaded reference solve per core, concurrently).
-Multi-GPU (torchrun): the path does not shard in round 1 — replicas, weak
-scaling.
+Multi-GPU (torchrun, N > 1): ONE solve split over the ranks by the C++
+distributed driver (P x Q grid, 2D block-cyclic 512 x 512 tiles, NCCL over
+NVLink; strong scaling, max-over-ranks device time).
 """
 import argparse
 import json
@@ -50,116 +51,121 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="skip live GEMM event timing")
     p.add_argument("--dist", action="store_true",
-                   help="one solve split over the ranks (1D row blocks, strong scaling) "
-                        "instead of one replica per rank")
+                   help="at N=1 too: the distributed driver on a 1x1 grid (N>1 always uses it)")
+    p.add_argument("--nb", type=int, default=512, help="tile size of the 2D block-cyclic layout")
     return p.parse_args()
 
 
-def run_dist(args, world, rank, dev, handle, dist):
-    """Strong scaling: ONE config solve over all ranks (paper_2104_14186_b200/dist.py).
-    A is generated on rank 0 and broadcast; rank r keeps its row block."""
-    import torch
-    from paper_2104_14186_b200 import dist as D
-    comm = D.Comm(dist) if world > 1 else None
-    if comm is None:
-        import socket
-        with socket.socket() as s:
-            s.bind(("127.0.0.1", 0))
-            port = s.getsockname()[1]
-        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
-                                world_size=1)
-        comm = D.Comm(dist)
-    inp = make_input(args.config, dev, handle) if rank == 0 else None
-    c = config_desc(args.config)
-    m = c["n"] if c["kind"] == "eig" else c["m"]
-    n = c["n"]
-    A = inp["A"] if rank == 0 else torch.empty((n, m), dtype=torch.float64, device=dev).t()
-    comm.broadcast(A)
-    meta = torch.tensor([inp["c"] if (rank == 0 and c["kind"] == "eig") else
-                         (inp["cut"] if rank == 0 else 0.0)], dtype=torch.float64, device=dev)
-    comm.broadcast(meta)
-    r0, r1 = D.row_range(m, rank, world)
-    A_r = A[r0:r1].t().contiguous().t()
-    be = D.GpuBackend(handle)
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
-    def one(Ar):
+
+def grid_shape(world):
+    """P x Q process grid with Q >= P: 1x1, 1x2, 2x2, 2x4, ..."""
+    p = int(np.sqrt(world))
+    while world % p:
+        p -= 1
+    return p, world // p
+
+
+def run_dist(args, world, rank, dev, handle, dist):
+    """Strong scaling: ONE config solve split over all ranks by the C++ driver
+    (libqdwhg qdwhg_dist_*: P x Q grid, 2D block-cyclic nb x nb tiles, NCCL
+    panel / diagonal-block broadcasts and short all-reductions).  Every rank
+    generates the same deterministic input (matgen.device_input) and keeps only
+    its tiles resident; the timed region is the solve (max over ranks)."""
+    import torch
+    from paper_2104_14186_b200 import matgen, qdwh
+    P, Q = grid_shape(world)
+    nb = args.nb
+    uid = [qdwh.dist_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    D = qdwh.Dist(handle, P, Q, nb, rank, unique_id=uid[0])
+    c = config_desc(args.config)
+    inp = make_input(args.config, dev, handle)
+    A = inp["A"]
+    m, n = A.shape
+    rnd = bool(inp.get("randomize", False))
+    D.load(A)
+    torch.cuda.synchronize(dev)
+
+    def solve_d(a=None):
         if c["kind"] == "eig":
-            B_r = -Ar.clone()
-            idx = torch.arange(r1 - r0, device=dev)
-            B_r[idx, r0 + idx] += float(meta.item())        # rows of cI - A (LARGEST)
-            return D.dist_partial_eig(be, comm, B_r.t().contiguous().t(), m)
-        return D.dist_partial_svd(be, comm, Ar, m, n, cut=float(meta.item()))
+            return D.partial_eig_request(a, "largest", inp["c"], inp["k"], use_randomization=rnd, n=n)
+        return D.partial_svd_request(a, cut=inp["cut"], k=inp["k"], use_randomization=rnd, shape=(m, n))
 
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device=dev)  # 256 MiB > L2
     for _ in range(max(args.warmup, 0)):
-        res = one(A_r)
+        res = solve_d()
     times, flops = [], []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = handle.launches()
-    sampler = ClockSampler(int(str(dev).split(":")[-1]) if ":" in str(dev) else 0)
+    sampler = ClockSampler(dev.index or 0)
     sampler.start()
     for s_ in range(args.steps):
         flush.fill_(float(s_))
+        torch.cuda.synchronize(dev)
         dist.barrier()
         torch.cuda.synchronize(dev)
         e0.record()
-        res = one(A_r)
+        res = solve_d()
         e1.record()
         torch.cuda.synchronize(dev)
         times.append(e0.elapsed_time(e1) / 1e3)
         flops.append(res.flops)
     clocks = sampler.stop()
     launches = (handle.launches() - launches0) // max(args.steps, 1)
-    # ---- e2e: every rank's row block from pinned host memory (H2D inside the
-    # timed region), the distributed solve, the result values and vectors to host
+    coll = D.stats()["collectives"]
+    # ---- e2e: the full matrix from pinned host memory (each rank copies only its
+    # own tiles in), the solve, values + vectors to the host on rank 0
     e2e_steps = args.e2e_steps or args.steps
-    A_pin = torch.empty((r1 - r0, A_r.shape[1]), dtype=torch.float64).t().contiguous().t().pin_memory()
-    A_pin.copy_(A_r.cpu())
-    A_dev = torch.empty_like(A_r)
-    e_t, e_f, h2d, d2h = 0.0, 0.0, 0, 0
+    A_pin = torch.empty((n, m), dtype=torch.float64).t().pin_memory()
+    A_pin.copy_(A.cpu())
+    A_host = A_pin.numpy()
+    e_t, e_f = 0.0, 0.0
     for s_ in range(e2e_steps):
         flush.fill_(float(s_))
+        torch.cuda.synchronize(dev)
         dist.barrier()
+        t0 = time.perf_counter()
+        res_h = solve_d(A_host)
         torch.cuda.synchronize(dev)
-        e0.record()
-        A_dev.copy_(A_pin, non_blocking=True)
-        res = one(A_dev)
-        out_b = 0
-        if rank == 0 and res.v is not None:
-            vh = res.v.cpu() if hasattr(res.v, "cpu") else res.v
-            out_b += int(np.asarray(vh).size) * 8
-        if res.u_rows is not None:
-            uh = res.u_rows.cpu() if hasattr(res.u_rows, "cpu") else res.u_rows
-            out_b += int(np.asarray(uh).size) * 8
-        e1.record()
-        torch.cuda.synchronize(dev)
-        e_t += e0.elapsed_time(e1) / 1e3
-        e_f += res.flops
-        h2d = A_pin.numel() * 8
-        d2h = out_b + len(res.values) * 8
-    tt = torch.tensor([sum(times), e_t, float(h2d), float(d2h)], dtype=torch.float64, device=dev)
-    mx = tt.clone()
-    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-    tot_t, e_t = float(mx[0]), float(mx[1])
+        e_t += time.perf_counter() - t0
+        e_f += res_h.flops
+    kk = res.count()
+    loc = (int(np.ceil(m / nb)), int(np.ceil(n / nb)))
+    h2d = m * n * 8  # every tile crosses once, summed over the ranks
+    d2h = kk * 8 + ((m + n) if c["kind"] == "svd" else n) * kk * 8
+    check = {}
     if rank == 0:
-        kk = len(res.values)
+        check = verify(inp, res)
+        check.update(oracle_check(args.config, inp, res))
+    tt = torch.tensor([sum(times), e_t], dtype=torch.float64,
+                      device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    tot_t, e_t = float(tt[0]), float(tt[1])
+    if rank == 0:
         line = {"metric": METRIC, "value": sum(flops) / tot_t / 1e12, "unit": "TFLOP/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded Gaussian factors, planted spectrum, generated on device)",
-                "config": dict(config_json(args.config, world), parallelism=f"rows{world}",
-                               randomized_detection=False),
+                "config": dict(config_json(args.config, world), parallelism=f"grid{P}x{Q}",
+                               nb=nb, tiles=list(loc)),
                 "time_to_solution_s": tot_t / args.steps,
                 "e2e": {"value": e_f / e_t / 1e12, "unit": "TFLOP/s",
-                        "h2d_bytes_per_step": int(tt[2]), "d2h_bytes_per_step": int(tt[3]),
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                         "time_to_solution_s": e_t / e2e_steps},
                 "gpu_launches": int(launches), "clocks": clocks,
-                "result": {"k": kk, "subspace_size": res.subspace_size,
-                           "iters_chol": res.iters_chol, "iters_qr": res.iters_qr}}
-        print(json.dumps(line))
+                "result": {"k": kk, "subspace_size": res.subspace_size, "iters_chol": res.iters_chol,
+                           "iters_qr": res.iters_qr, "algorithmic_flops": flops[-1],
+                           "collectives_issued_total": int(coll), **check}}
+        print(json.dumps(line), flush=True)
+    D.close()
     dist.destroy_process_group()
 
 
@@ -399,7 +405,7 @@ def config_json(cfg, gpus):
     d = {"workload": f"cfg{cfg}: QDWHpartial-{c['kind'].upper()} "
                      + (f"n={c['n']}" if c["kind"] == "eig" else f"{c['m']}x{c['n']}")
                      + f" {c['family']} spectrum, top {c['k']}",
-         "k": c["k"], "parallelism": f"replicas{gpus}" if gpus > 1 else "single",
+         "k": c["k"], "parallelism": "single",
          "l2": "flushed (256 MiB write) before every timed step"}
     d.update({kk: v for kk, v in c.items() if kk in ("n", "m")})
     env = os.environ.get("BENCH_RANDOMIZE")
@@ -427,11 +433,12 @@ def main():
     handle = qdwh.Handle(device=local)
     handle.set_stream(torch.cuda.current_stream(dev).cuda_stream)
 
-    # --dist: one solve distributed over the ranks (1D row blocks with all-reduced
-    # Grams, dist.py; strong scaling).  Default for N > 1: independent replicas —
-    # the distributed driver is validated at world size 1 only (one-GPU pool) and
-    # is still slower than the single-GPU path there (cfg2 142 vs 45 ms)
-    if args.dist:
+    # N > 1: ONE solve split over the ranks (strong scaling) by the C++ 2D
+    # block-cyclic driver over NCCL; N = 1: the single-GPU driver
+    if world > 1 or args.dist:
+        if world == 1:
+            dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % free_port(), rank=0,
+                                    world_size=1)
         run_dist(args, world, rank, dev, handle, dist)
         return
     inp = make_input(args.config, dev, handle)

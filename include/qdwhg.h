@@ -274,6 +274,23 @@ qdwhg_status qdwhg_dist_world_create(void** world, int32_t nranks);
 qdwhg_status qdwhg_dist_world_destroy(void* world);
 qdwhg_status qdwhg_dist_create_loopback(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
                                         int32_t rank, void* world);
+/* Caller-supplied transport (MPI, torch.distributed, ...): buffers are device
+ * pointers on the rank's GPU, its stream synchronized before every call.  team:
+ * 0 world, 1 grid row (ranks with the same p), 2 grid column; root / peer are
+ * world ranks (rank = p * Q + q); op: 0 sum, 1 max, 2 min.  Inside a
+ * group_begin/group_end bracket, results may complete at group_end (receives
+ * must not block sends of the same group).  Return 0 on success. */
+typedef struct qdwhg_comm_callbacks {
+  void* ctx;
+  int (*bcast)(void* ctx, double* buf, size_t count, int root, int team);
+  int (*allreduce)(void* ctx, double* buf, size_t count, int op, int team);
+  int (*send)(void* ctx, const double* buf, size_t count, int peer);
+  int (*recv)(void* ctx, double* buf, size_t count, int peer);
+  int (*group_begin)(void* ctx); /* optional (NULL) */
+  int (*group_end)(void* ctx);   /* optional (NULL) */
+} qdwhg_comm_callbacks;
+qdwhg_status qdwhg_dist_create_callback(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                        int32_t rank, const qdwhg_comm_callbacks* cb);
 qdwhg_status qdwhg_dist_destroy(qdwhg_dist* d);
 qdwhg_status qdwhg_dist_get_stats(const qdwhg_dist* d, uint64_t* collectives, uint64_t* local_gemms);
 /* Keep the rank's tiles of A resident (solves with A == NULL reuse them). */

@@ -108,6 +108,7 @@ SIGNATURES = {
     "qdwhg_dist_world_create": [_P, _I32],
     "qdwhg_dist_world_destroy": [_P],
     "qdwhg_dist_create_loopback": [_P, _P, _I32, _I32, _I32, _I32, _P],
+    "qdwhg_dist_create_callback": [_P, _P, _I32, _I32, _I32, _I32, _P],
     "qdwhg_dist_destroy": [_P],
     "qdwhg_dist_get_stats": [_P, _P, _P],
     "qdwhg_dist_load": [_P, _I64, _I64, _P, _I64],

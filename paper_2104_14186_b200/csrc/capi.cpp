@@ -1009,6 +1009,21 @@ qdwhg_status qdwhg_dist_create_loopback(qdwhg_dist** d, qdwhg_handle* h, int32_t
   });
 }
 
+qdwhg_status qdwhg_dist_create_callback(qdwhg_dist** d, qdwhg_handle* h, int32_t P, int32_t Q, int32_t nb,
+                                        int32_t rank, const qdwhg_comm_callbacks* cb) {
+  if (!cb) return QDWHG_INVALID_ARGUMENT;
+  static_assert(sizeof(qdwhg_comm_callbacks) == sizeof(dist::CommCallbacks), "callback layout");
+  dist::CommCallbacks c;
+  std::memcpy(&c, cb, sizeof(c));
+  return dist_init(d, h, P, Q, nb, rank, [&](const dist::Grid& g) {
+    qdwhg_handle* hh = h;
+    return dist::callback_comm_create(c, rank, P * Q, g, [hh] {
+      QDWHG_CUDA(cudaSetDevice(hh->device));
+      QDWHG_CUDA(cudaStreamSynchronize(hh->ctx.stream));
+    });
+  });
+}
+
 qdwhg_status qdwhg_dist_destroy(qdwhg_dist* d) {
   if (!d) return QDWHG_OK;
   cudaSetDevice(d->h->device);

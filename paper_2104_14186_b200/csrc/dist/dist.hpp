@@ -244,6 +244,22 @@ struct SvdResult {
 SvdResult partial_svd(Ctx& c, const DistMat& A, double s, double s_abs, double tol, bool randomize,
                       uint64_t seed, const std::function<double()>& clock = nullptr);
 
+// Communicator over caller callbacks (same layout as qdwhg_comm_callbacks).
+// team: 0 world, 1 row, 2 column; op: 0 sum, 1 max, 2 min.  Received data and
+// reduced results must be in place when the callback returns, except inside a
+// group_begin/group_end bracket, where they must be in place at group_end.
+struct CommCallbacks {
+  void* ctx;
+  int (*bcast)(void* ctx, double* buf, size_t count, int root, int team);
+  int (*allreduce)(void* ctx, double* buf, size_t count, int op, int team);
+  int (*send)(void* ctx, const double* buf, size_t count, int peer);
+  int (*recv)(void* ctx, double* buf, size_t count, int peer);
+  int (*group_begin)(void* ctx);
+  int (*group_end)(void* ctx);
+};
+Comm* callback_comm_create(const CommCallbacks& cb, int rank, int world, const Grid& g,
+                           std::function<void()> sync);
+
 // In-process loopback world for emulated ranks (threads of one process).
 class LoopbackWorld;
 LoopbackWorld* loopback_world_create(int nranks);

@@ -322,6 +322,30 @@ struct Run {
   std::string err;
 };
 
+// one rank of a multi-process run: the comm is the caller's (callbacks)
+template <class Body>
+int run_one(int P, int Q, int nb, int rank, const CommCallbacks* cb, char* err, int errlen, Body body) {
+  try {
+    HostEngine e;
+    Grid g;
+    g.P = P;
+    g.Q = Q;
+    g.p = rank / Q;
+    g.q = rank % Q;
+    g.nb = nb;
+    std::unique_ptr<Comm> comm(callback_comm_create(*cb, rank, P * Q, g, [] {}));
+    Ctx c;
+    c.g = g;
+    c.comm = comm.get();
+    c.eng = &e;
+    body(c, rank);
+  } catch (const std::exception& ex) {
+    if (err && errlen > 0) std::snprintf(err, (size_t)errlen, "rank %d: %s", rank, ex.what());
+    return 1;
+  }
+  return 0;
+}
+
 template <class Body>
 int run_ranks(int P, int Q, int nb, char* err, int errlen, Body body) {
   const int nr = P * Q;
@@ -410,6 +434,28 @@ int dh_qr(int P, int Q, int nb, int64_t m, int64_t n, const double* X, int64_t l
     porgqr_cols(c, qr, c0, Qm);
     gather(c, Qm, r == 0 ? Q2 : nullptr, ldq, 0);
     if (r == 0) std::memcpy(rdiag, qr.rdiag.data(), sizeof(double) * (size_t)n);
+  });
+}
+
+// partial.cpp:40-99 (LARGEST map) as ONE rank of a multi-process run whose
+// communicator is the caller's callbacks (the CPU gloo test)
+int dh_partial_eig_rank(int P, int Q, int nb, int rank, const CommCallbacks* cb, int64_t n, const double* A,
+                        int64_t lda, double cshift, int64_t kreq, double* lambda, double* V, int64_t ldv,
+                        int64_t* k_out, int64_t* ell_out, double* mu_out, char* err, int errlen) {
+  return run_one(P, Q, nb, rank, cb, err, errlen, [&](Ctx& c, int r) {
+    DistMat Am = make_dist(*c.eng, c.g, n, n), Bm = make_dist(*c.eng, c.g, n, n);
+    scatter_from_full(c, A, lda, true, Am);
+    axpby_identity(c, &Am, -1.0, Bm, 0.0, cshift);
+    EigResult res = partial_eig(c, Bm, choose_shift(3), 3, false, 0.01, 0);
+    int64_t k = (int64_t)res.lambda.size();
+    if (kreq > 0) k = std::min(k, kreq);
+    *k_out = k;
+    *ell_out = (int64_t)res.subspace_size;
+    *mu_out = res.mu;
+    for (int64_t i = 0; i < k; ++i) lambda[i] = cshift - res.lambda[(size_t)i];
+    if (r == 0)
+      for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < n; ++i) V[i + j * ldv] = res.V[i + j * res.vld];
   });
 }
 
