@@ -317,3 +317,29 @@ def test_cholesky_inverse_fast_and_subspace_q2(cuda):
     assert np.linalg.norm(q2.T @ q2 - np.eye(q2.shape[1])) <= 1e-12 * n
     # same subspace: the projectors agree
     assert np.linalg.norm(q2 @ q2.T - ref @ ref.T) <= 1e-10
+
+
+def test_device_gaussian_reference_stream_determinism_and_moments(cuda):
+    """qdwhg_gaussian_matrix (kernels.cpp:441-447 counter scheme on the device;
+    test_kernels.cpp:284-302 determinism and moments): the reference's own
+    draws (golden, produced by the reference) to device-libm rounding, identical
+    bits run to run, a different stream per seed, N(0,1) moments."""
+    import torch
+    g = golden("gaussian")
+    for key, (m, n, seed) in {"g1": (17, 5, 0), "g2": (3, 11, 42), "g3": (64, 1, 0x6C616E637A),
+                              "g4": (64, 1, 0x6E6F726D32)}.items():
+        d = qdwh.gaussian_matrix_device(m, n, seed, device=cuda).cpu().numpy()
+        np.testing.assert_allclose(d, g[key], rtol=1e-14, atol=1e-14)  # log/cospi vs glibc log/cos
+    a = qdwh.gaussian_matrix_device(1500, 1000, 42, device=cuda)
+    b = qdwh.gaussian_matrix_device(1500, 1000, 42, device=cuda)
+    assert torch.equal(a, b)
+    c = qdwh.gaussian_matrix_device(1500, 1000, 43, device=cuda)
+    assert not torch.equal(a, c)
+    np.testing.assert_allclose(a[:300, :200].cpu().numpy(), O.gaussian_matrix(1500, 1000, 42)[:300, :200],
+                               rtol=1e-13, atol=1e-13)
+    x = a.flatten().cpu().numpy()
+    N = x.size
+    assert abs(x.mean()) < 5.0 / np.sqrt(N)
+    assert abs(x.var() - 1.0) < 5.0 * np.sqrt(2.0 / N)
+    assert abs(np.mean(x ** 4) - 3.0) < 5.0 * np.sqrt(96.0 / N)
+    assert abs(np.mean(x ** 3)) < 5.0 * np.sqrt(15.0 / N)
