@@ -45,6 +45,8 @@ def call():
         return qdwh.qdwh_chol_step(X, 0.5, handle=h)
     if what == "sym":  # one symmetric Cholesky-based step (the EIG path)
         return qdwh.run_fixed_iterations(Xs, 0.2, 1, handle=h)
+    if what == "fast":  # the recursive Cholesky-and-inverse of the QDWH step
+        return qdwh.cholesky_inverse_fast(Z, handle=h)
     if what == "qr":
         return qdwh.qr_factor(G, handle=h)
     return qdwh.cholesky_factor_inverse(Z, handle=h)
