@@ -69,7 +69,8 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
   // (only for mid-size n — measured per step: -0.3 ms at 3072, -0.1 ms at 4096,
   // neutral at 4546, +3.5 ms at 6144, where the capped side launches run well
   // below the GEMM rate and the chain is a small share)
-  if (!no_overlap && !stable_env && ctx.side != nullptr && n >= 2048 && n <= 5120 && n1 < n) {
+  if (!no_overlap && !stable_env && ctx.side != nullptr && n >= 2048 && n <= 5120 && n1 < n &&
+      !chol_dag_applicable(n)) {
     // Overlapped schedule: the latency-bound recursive Cholesky-and-inverse
     // chain runs on the main stream while independent GEMM work runs on the
     // side stream in launches of <= 64 128x128 tiles (so the chain's small

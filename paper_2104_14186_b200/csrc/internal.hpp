@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <cstdlib>
 #include <utility>
@@ -99,6 +100,8 @@ enum class KRange { Full, BUpper, BLower, AUpper, ALower };
 // Lower: only the lower triangle of a square C is written; LowerMirror also mirrors it.
 enum class OutMode { Full, LowerMirror, Lower };
 
+struct DagCache;  // chol_dag.cu: per-handle task list + counters
+
 struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // look-ahead stream (handle-owned, lowest priority)
@@ -116,6 +119,7 @@ struct Ctx {
   double* dscratch = nullptr;   // small device scratch (>= 64 KiB)
   double* hscratch = nullptr;   // pinned host mirror of dscratch
   int* dflag = nullptr;         // device status flag
+  std::shared_ptr<DagCache> dag;  // tile-DAG Cholesky state (chol_dag.cu)
   uint64_t gemm_launches = 0;   // our kernels launched (for bench accounting)
   uint64_t other_launches = 0;
   void count(int n = 1) { other_launches += n; }
@@ -224,6 +228,14 @@ void gaussian_fill_at(Ctx& ctx, double* X, int64_t ld, int64_t m, int64_t n, uin
 // only for the QDWH Cholesky steps where kappa(Z) <= 1 + c).
 void potrf_upper_and_inverse(Ctx& ctx, const DMat& Z, const DMat& Winv, bool want_w = false,
                              bool stable = true);
+
+// ------------------------------------------------------------------ chol_dag.cu
+// Tile-DAG Cholesky-and-inverse (n = 128 T, 2 <= T <= QDWHG_CHOL_DAG_TMAX): one
+// persistent kernel.  Winv receives W^{-1} (upper; its strict lower must be zero
+// already); all of Z is workspace (lower tiles: L, diagonal tiles: L_kk^{-1},
+// upper tiles: partial sums of the inverse).  Pivot failures set ctx.dflag.
+bool chol_dag_applicable(int64_t n);
+void chol_dag(Ctx& ctx, const DMat& Z, const DMat& Winv);
 
 // R^{-1} (upper, explicit zeros below) of an upper-triangular R; false if a
 // diagonal entry is zero / non-finite.

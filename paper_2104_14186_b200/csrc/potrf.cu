@@ -17,30 +17,16 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "potrf_leaf.cuh"
 
 namespace qdwhg {
 
 namespace {
 
-constexpr int kDiagThreads = 256;
-
-// 1/sqrt(d) without the libdevice slow-path call (which forces the unrolled
-// register row to the stack): hardware double-precision estimate
-// (rsqrt.approx.f64) refined by one third-order step.  Non-positive d returns NaN
-// (the caller flags it).
-QDWHG_DEV double rsqrt_newton(double d) {
-  // branch-free (a branch here splits the unrolled Cholesky step into basic
-  // blocks and stops the scheduler from hiding this chain behind the updates)
-  // One third-order step from the ~2^-20 hardware estimate: with
-  // e = 1 - d y^2, y' = y + y e (1/2 + 3/8 e) (error 5/16 e^3 < 2^-56),
-  // dependency depth 4 instead of 6 for two Newton steps.
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(d));
-  const double e = fma(-d * y, y, 1.0);
-  const double p = fma(e, 0.375, 0.5);
-  y = fma(y * e, p, y);
-  return (d > 0.0) ? y : __longlong_as_double(0x7ff8000000000000ll);
-}
+using leaf::kDiagThreads;
+using leaf::kLDA;
+using leaf::kLDT;
+using leaf::kSB;
 #ifdef QDWHG_DIAG_TRACE
 __device__ long long g_diag_trace[64];
 #define DIAG_MARK(i) \
@@ -48,58 +34,6 @@ __device__ long long g_diag_trace[64];
 #else
 #define DIAG_MARK(i)
 #endif
-constexpr int kSB = 32;          // sub-block handled by one warp
-// padded smem leading dimension: 132 = 4 (mod 16) makes the DMMA fragment loads
-// (8 rows x 4 k, or 4 k x 8 columns, one double per lane) bank-conflict free
-constexpr int kLDA = 132;
-
-// One right-looking Cholesky column step of a 32x32 block held as one row per
-// lane (template recursion: compile-time register indices).  The pivot comes
-// by one shuffle; the scaled column J goes to shared memory (its final place
-// in L) and every lane reads the entries it needs as broadcast loads — half
-// the instructions of shuffling each double.
-template <int J>
-struct CholStep {
-  // djj: the pivot L_JJ^2, already broadcast by the previous step (look-ahead)
-  static QDWHG_DEV void run(double (&row)[kSB], double* L, int lane, bool& bad, double& my_inv,
-                            double djj) {
-    if (!(djj > 0.0)) bad = true;
-    const double inv = rsqrt_newton(djj);
-    if (lane > J) row[J] *= inv;
-    if (lane == J) {
-      row[J] = djj * inv;
-      my_inv = inv;
-    }
-    // look-ahead: lane J+1 updates its own diagonal from its own register
-    // (same fma as the loop below) and broadcasts the next pivot right away, so
-    // the next step's rsqrt does not wait for the shared-memory round trip
-    double dnext = 0.0;
-    if (J + 1 < kSB) dnext = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[(J + 1) % kSB]), (J + 1) % kSB);
-    if (lane >= J) L[J * kLDA + lane] = row[J];
-    __syncwarp();
-    // unpredicated: entries above a lane's diagonal pick up junk that is never
-    // read (the pivot and the written column only use entries on/below it)
-#pragma unroll
-    for (int c = J + 1; c < kSB; ++c) row[c] -= row[J] * L[J * kLDA + c];
-    CholStep<J + 1>::run(row, L, lane, bad, my_inv, dnext);
-  }
-};
-template <>
-struct CholStep<kSB> {
-  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&, double) {}
-};
-
-// D^{-1} of a factored 32x32 lower block by forward substitution, one warp,
-// lane j computing column j in registers (x[i] = 0 above the diagonal)
-QDWHG_DEV void block_inverse(const double* Lb, const double* sinv, int lane, double (&x)[kSB]) {
-#pragma unroll
-  for (int i = 0; i < kSB; ++i) {
-    double s[4] = {(i == lane) ? 1.0 : 0.0, 0.0, 0.0, 0.0};  // 4 chains
-#pragma unroll
-    for (int k = 0; k < i; ++k) s[k & 3] -= Lb[k * kLDA + i] * x[k];  // x[k] == 0 for k < lane
-    x[i] = (i >= lane) ? ((s[0] + s[1]) + (s[2] + s[3])) * sinv[i] : 0.0;
-  }
-}
 
 // Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
 // -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
@@ -117,7 +51,6 @@ QDWHG_DEV void block_inverse(const double* Lb, const double* sinv, int lane, dou
 //     of a level at once (2 levels x 2 products instead of 3 x 2 block columns);
 //   Winv = L^{-T} written out (upper triangle only with kDiagUpperOnly).
 // The block is padded to a multiple of 32 with an identity (chol([Z 0;0 I]) = [L 0;0 I]).
-constexpr int kLDT = 68;  // T (<= 64 x 64, the doubling products' scratch) leading dimension
 // launch flags
 constexpr int kDiagInvertOnly = 1;  // input is an upper R: only R^{-1}
 constexpr int kDiagNoW = 2;         // W = L^T is not wanted (not written)
@@ -132,9 +65,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   double* Sinv = T + 64 * kLDT;      // 128: 1 / L_ii
   __shared__ int bad_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, q = lane & 3;  // DMMA fragment coordinates
   const int nbp = ((nb + kSB - 1) / kSB) * kSB;
-  const int nsb = nbp / kSB;
   if (tid == 0) bad_s = 0;
   DIAG_MARK(20);
   griddep_wait();
@@ -169,91 +100,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   __syncthreads();
   DIAG_MARK(0);
 
-  for (int kb = 0; kb < nsb; ++kb) {
-    const int b0 = kb * kSB;
-    if (warp == 0) {
-      // ---- factor the 32x32 diagonal block in registers: lane i owns row i.
-      // No division/sqrt library calls in here (their slow-path CALL would push
-      // the unrolled register rows to the stack): pivots use rsqrt_newton.
-      double row[kSB];
-#pragma unroll
-      for (int c = 0; c < kSB; ++c) row[c] = A[(b0 + c) * kLDA + b0 + lane];  // strict upper is 0
-      bool bad = false;
-      double my_inv = 0.0;
-      CholStep<0>::run(row, A + b0 * kLDA + b0, lane, bad, my_inv,
-                       __shfl_sync(0xffffffffu, row[0], 0));  // writes L in place
-      if (bad && lane == 0) bad_s = 1;
-      Sinv[b0 + lane] = my_inv;
-    }
-    __syncthreads();
-    DIAG_MARK(1 + 3 * kb);
-    const int p0 = b0 + kSB, R = nbp - p0;
-    if (R > 0) {
-      // ---- panel rows by forward substitution, one row per thread:
-      // L(i, b0+c) = (Z(i, b0+c) - sum_{t<c} L(i, b0+t) L(b0+c, b0+t)) / L(b0+c, b0+c)
-      if (tid < R) {
-        const int i = p0 + tid;
-        double x[kSB];
-#pragma unroll
-        for (int c = 0; c < kSB; ++c) x[c] = A[(b0 + c) * kLDA + i];
-#pragma unroll
-        for (int c = 0; c < kSB; ++c) {
-          double s0 = x[c], s1 = 0.0;  // two chains: half the FMA latency
-#pragma unroll
-          for (int t = 0; t < c; ++t) {
-            const double l = A[(b0 + t) * kLDA + b0 + c];  // broadcast
-            if (t & 1) s1 -= x[t] * l;
-            else s0 -= x[t] * l;
-          }
-          x[c] = (s0 + s1) * Sinv[b0 + c];
-        }
-#pragma unroll
-        for (int c = 0; c < kSB; ++c) A[(b0 + c) * kLDA + i] = x[c];
-      }
-      __syncthreads();
-      DIAG_MARK(2 + 3 * kb);
-      // ---- trailing rank-32 update of the lower triangle on 8x8 DMMA tiles:
-      // A(i, j) -= sum_t L(i, b0+t) L(j, b0+t),  i >= j >= p0.  A work unit is
-      // one row tile x up to 4 column tiles (4 independent accumulator chains).
-      const int nt = R / 8;
-      int nunits = 0;
-      for (int ti = 0; ti < nt; ++ti) nunits += ti / 4 + 1;
-      for (int u = warp; u < nunits; u += kDiagThreads / 32) {
-        int ti = 0, rem = u;
-        while (rem >= ti / 4 + 1) {
-          rem -= ti / 4 + 1;
-          ++ti;
-        }
-        const int tj0 = 4 * rem;
-        const int i0 = p0 + 8 * ti;
-        double c[4][2];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int j0 = p0 + 8 * min(tj0 + v, ti);
-          c[v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
-          c[v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
-        }
-#pragma unroll
-        for (int k4 = 0; k4 < kSB / 4; ++k4) {
-          const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
-          const double a = -lc[i0 + g];
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            dmma_8x8x4(c[v][0], c[v][1], a, lc[p0 + 8 * min(tj0 + v, ti) + g]);
-        }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int tj = tj0 + v;
-          if (tj > ti) break;
-          const int j0 = p0 + 8 * tj;
-          if (tj != ti || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[v][0];
-          if (tj != ti || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[v][1];
-        }
-      }
-      __syncthreads();
-    }
-    DIAG_MARK(3 + 3 * kb);
-  }
+  leaf::factor(A, Sinv, nbp, &bad_s);
   // ---- W = L^T (upper) with explicit zeros below
   if (!(flags & kDiagNoW)) {
     const int rend = (flags & kDiagUpperOnly) ? 0 : nb;
@@ -267,81 +114,7 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   }  // !invert_only
   if (tid == 0 && bad_s) atomicExch(flag, 1);
 
-  // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each, in place
-  if (warp < nsb) {
-    const int b0 = warp * kSB;
-    double x[kSB];
-    block_inverse(A + b0 * kLDA + b0, Sinv + b0, lane, x);
-    __syncwarp();
-    double* D = A + (b0 + lane) * kLDA + b0;  // column lane of the block (zeros above)
-#pragma unroll
-    for (int i = 0; i < kSB; ++i) D[i] = x[i];
-  }
-  __syncthreads();
-  DIAG_MARK(14);
-
-  // ---- L^{-1} by recursive doubling over the diagonal blocks: for each pair of
-  // adjacent groups (P = [a0, a0+h), Q = [a0+h, a0+2h)) with P^{-1}, Q^{-1} in
-  // place:  L^{-1}_QP = -Q^{-1} (L_QP P^{-1}).  Two levels for nb = 128, each
-  // two DMMA products over all pairs at once (a unit = one 8-row tile x 32 columns).
-  for (int h = kSB; h < nbp; h *= 2) {
-    const int npairs = (nbp - h + 2 * h - 1) / (2 * h);  // pairs with a non-empty Q
-    const int cgs = h / kSB;                             // 32-column groups per pair
-    int units = 0;
-    for (int p = 0; p < npairs; ++p) units += min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
-    // phase 1: T_p = L_QP * P^{-1}   (P^{-1} lower: k >= column)
-    for (int u = warp; u < units; u += kDiagThreads / 32) {
-      int p = 0, rem = u;
-      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
-        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
-        ++p;
-      }
-      const int ti = rem / cgs, cg = rem % cgs;
-      const int a0 = 2 * p * h, q0 = a0 + h;
-      double c[4][2] = {};
-      for (int k4 = 8 * cg; k4 < h / 4; ++k4) {
-        const int k = a0 + 4 * k4 + q;
-        const double a = A[k * kLDA + q0 + 8 * ti + g];
-#pragma unroll
-        for (int tj = 0; tj < 4; ++tj)
-          dmma_8x8x4(c[tj][0], c[tj][1], a, A[(a0 + kSB * cg + 8 * tj + g) * kLDA + k]);
-      }
-#pragma unroll
-      for (int tj = 0; tj < 4; ++tj) {
-        const int col = p * h + kSB * cg + 8 * tj + 2 * q;
-        T[col * kLDT + 8 * ti + g] = c[tj][0];
-        T[(col + 1) * kLDT + 8 * ti + g] = c[tj][1];
-      }
-    }
-    __syncthreads();
-    // phase 2: L^{-1}_QP = -Q^{-1} T_p   (Q^{-1} lower: k <= row), heaviest rows first
-    for (int u = warp; u < units; u += kDiagThreads / 32) {
-      int p = 0, rem = u;
-      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
-        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
-        ++p;
-      }
-      const int nti = min(h, nbp - (2 * p + 1) * h) / 8;
-      const int ti = nti - 1 - rem / cgs, cg = rem % cgs;
-      const int a0 = 2 * p * h, q0 = a0 + h;
-      double c[4][2] = {};
-      for (int k4 = 0; k4 < 2 * (ti + 1); ++k4) {
-        const int k = 4 * k4 + q;
-        const double a = -A[(q0 + k) * kLDA + q0 + 8 * ti + g];
-#pragma unroll
-        for (int tj = 0; tj < 4; ++tj)
-          dmma_8x8x4(c[tj][0], c[tj][1], a, T[(p * h + kSB * cg + 8 * tj + g) * kLDT + k]);
-      }
-#pragma unroll
-      for (int tj = 0; tj < 4; ++tj) {
-        const int col = a0 + kSB * cg + 8 * tj + 2 * q;
-        A[col * kLDA + q0 + 8 * ti + g] = c[tj][0];
-        A[(col + 1) * kLDA + q0 + 8 * ti + g] = c[tj][1];
-      }
-    }
-    __syncthreads();
-    DIAG_MARK(21 + h / kSB);
-  }
+  leaf::invert(A, T, Sinv, nbp);
   DIAG_MARK(15);
 
   // PDL: the dependent GEMM's launch and prologue overlap the write-out below
@@ -372,19 +145,26 @@ void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, i
   ctx.count();
 }
 
-void trtri_rec(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t r0, int64_t n, int nb) {
+// W's off-diagonal blocks: from W itself (upper) or, with lower, transposed from
+// the L = W^T stored in the lower triangle of the same matrix (chol_dag output).
+DMat w_offdiag(const DMat& W, int64_t r0, int64_t c0, int64_t m, int64_t n, bool lower) {
+  return lower ? W.sub(c0, r0, n, m) : W.sub(r0, c0, m, n);
+}
+
+void trtri_rec(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t r0, int64_t n, int nb,
+               bool lower = false) {
   if (n <= nb) return;
   int64_t n1 = ((n / 2 + nb - 1) / nb) * nb;
   if (n1 >= n) n1 = n - nb;
   const int64_t n2 = n - n1;
-  trtri_rec(ctx, W, Winv, r0, n1, nb);
-  trtri_rec(ctx, W, Winv, r0 + n1, n2, nb);
+  trtri_rec(ctx, W, Winv, r0, n1, nb, lower);
+  trtri_rec(ctx, W, Winv, r0 + n1, n2, nb, lower);
   const Arena::Mark mark = ctx.arena->mark();
   DMat T = ctx.arena->alloc(n1, n2);
   GemmExtra e1;
   e1.krange = KRange::BUpper;  // B = W22^-1 upper
-  gemm(ctx, Op::N, Op::N, 1.0, W.sub(r0, r0 + n1, n1, n2), Winv.sub(r0 + n1, r0 + n1, n2, n2), 0.0,
-       T, e1);
+  gemm(ctx, lower ? Op::T : Op::N, Op::N, 1.0, w_offdiag(W, r0, r0 + n1, n1, n2, lower),
+       Winv.sub(r0 + n1, r0 + n1, n2, n2), 0.0, T, e1);
   GemmExtra e2;
   e2.krange = KRange::AUpper;  // A = W11^-1 upper
   gemm(ctx, Op::N, Op::N, -1.0, Winv.sub(r0, r0, n1, n1), T, 0.0, Winv.sub(r0, r0 + n1, n1, n2),
@@ -394,7 +174,7 @@ void trtri_rec(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
 
 // Same recursion, level by level for n = nb * 2^L: all merges of one level are
 // independent, so each level is two batched GEMM launches instead of 2 * pairs.
-void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb) {
+void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb, bool lower = false) {
   for (int64_t h = nb; h < n; h *= 2) {
     const int64_t pairs = n / (2 * h);
     const Arena::Mark mark = ctx.arena->mark();
@@ -405,7 +185,8 @@ void trtri_levels(Ctx& ctx, const DMat& W, const DMat& Winv, int64_t n, int nb) 
     e1.a_step_r = e1.a_step_c = 2 * h;
     e1.b_step_r = e1.b_step_c = 2 * h;
     e1.c_step_c = h;
-    gemm(ctx, Op::N, Op::N, 1.0, W.sub(0, h, h, h), Winv.sub(h, h, h, h), 0.0, T.sub(0, 0, h, h), e1);
+    gemm(ctx, lower ? Op::T : Op::N, Op::N, 1.0, w_offdiag(W, 0, h, h, h, lower), Winv.sub(h, h, h, h),
+         0.0, T.sub(0, 0, h, h), e1);
     GemmExtra e2;
     e2.krange = KRange::AUpper;  // W11^-1 upper
     e2.batch = (int)pairs;
@@ -470,6 +251,11 @@ void launch_panel_trsm(Ctx& ctx, const DMat& Wkk, const DMat& Zr, const DMat& X)
 // diag kernel.  Only the lower triangle of Z is read/updated.
 void chol_inv_rec(Ctx& ctx, const DMat& Z, const DMat& W, const DMat& Winv, int64_t r0, int64_t n,
                   int nb, int leaf_flags) {
+  // sub-trees up to QDWHG_CHOL_DAG_TMAX tiles: one tile-DAG kernel (W^{-1} only)
+  if (nb == 128 && (leaf_flags & kDiagNoW) && chol_dag_applicable(n)) {
+    chol_dag(ctx, Z.sub(r0, r0, n, n), Winv.sub(r0, r0, n, n));
+    return;
+  }
   if (n <= nb) {
     launch_diag(ctx, Z.sub(r0, r0, n, n), W.sub(r0, r0, n, n), Winv.sub(r0, r0, n, n), leaf_flags);
     return;

@@ -1,0 +1,263 @@
+// Device building blocks of the 128 x 128 Cholesky-and-inverse leaf, shared by
+// the stand-alone leaf kernel (potrf.cu: potrf_diag_kernel) and the tile-DAG
+// Cholesky (chol_dag.cu).  256 threads; the block lives in shared memory,
+// column-major with leading dimension kLDA, lower triangle = L (then L^{-1}).
+#pragma once
+#include "common.cuh"
+
+namespace qdwhg {
+namespace leaf {
+
+constexpr int kThreads = 256;
+constexpr int kDiagThreads = kThreads;
+// 1/sqrt(d) without the libdevice slow-path call (which forces the unrolled
+// register row to the stack): hardware double-precision estimate
+// (rsqrt.approx.f64) refined by one third-order step.  Non-positive d returns NaN
+// (the caller flags it).
+QDWHG_DEV double rsqrt_newton(double d) {
+  // branch-free (a branch here splits the unrolled Cholesky step into basic
+  // blocks and stops the scheduler from hiding this chain behind the updates)
+  // One third-order step from the ~2^-20 hardware estimate: with
+  // e = 1 - d y^2, y' = y + y e (1/2 + 3/8 e) (error 5/16 e^3 < 2^-56),
+  // dependency depth 4 instead of 6 for two Newton steps.
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(y) : "d"(d));
+  const double e = fma(-d * y, y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  y = fma(y * e, p, y);
+  return (d > 0.0) ? y : __longlong_as_double(0x7ff8000000000000ll);
+}
+constexpr int kSB = 32;          // sub-block handled by one warp
+// padded smem leading dimension: 132 = 4 (mod 16) makes the DMMA fragment loads
+// (8 rows x 4 k, or 4 k x 8 columns, one double per lane) bank-conflict free
+constexpr int kLDA = 132;
+
+// One right-looking Cholesky column step of a 32x32 block held as one row per
+// lane (template recursion: compile-time register indices).  The pivot comes
+// by one shuffle; the scaled column J goes to shared memory (its final place
+// in L) and every lane reads the entries it needs as broadcast loads — half
+// the instructions of shuffling each double.
+template <int J>
+struct CholStep {
+  // djj: the pivot L_JJ^2, already broadcast by the previous step (look-ahead)
+  static QDWHG_DEV void run(double (&row)[kSB], double* L, int lane, bool& bad, double& my_inv,
+                            double djj) {
+    if (!(djj > 0.0)) bad = true;
+    const double inv = rsqrt_newton(djj);
+    if (lane > J) row[J] *= inv;
+    if (lane == J) {
+      row[J] = djj * inv;
+      my_inv = inv;
+    }
+    // look-ahead: lane J+1 updates its own diagonal from its own register
+    // (same fma as the loop below) and broadcasts the next pivot right away, so
+    // the next step's rsqrt does not wait for the shared-memory round trip
+    double dnext = 0.0;
+    if (J + 1 < kSB) dnext = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[(J + 1) % kSB]), (J + 1) % kSB);
+    if (lane >= J) L[J * kLDA + lane] = row[J];
+    __syncwarp();
+    // unpredicated: entries above a lane's diagonal pick up junk that is never
+    // read (the pivot and the written column only use entries on/below it)
+#pragma unroll
+    for (int c = J + 1; c < kSB; ++c) row[c] -= row[J] * L[J * kLDA + c];
+    CholStep<J + 1>::run(row, L, lane, bad, my_inv, dnext);
+  }
+};
+template <>
+struct CholStep<kSB> {
+  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double&, double) {}
+};
+
+// D^{-1} of a factored 32x32 lower block by forward substitution, one warp,
+// lane j computing column j in registers (x[i] = 0 above the diagonal)
+QDWHG_DEV void block_inverse(const double* Lb, const double* sinv, int lane, double (&x)[kSB]) {
+#pragma unroll
+  for (int i = 0; i < kSB; ++i) {
+    double s[4] = {(i == lane) ? 1.0 : 0.0, 0.0, 0.0, 0.0};  // 4 chains
+#pragma unroll
+    for (int k = 0; k < i; ++k) s[k & 3] -= Lb[k * kLDA + i] * x[k];  // x[k] == 0 for k < lane
+    x[i] = (i >= lane) ? ((s[0] + s[1]) + (s[2] + s[3])) * sinv[i] : 0.0;
+  }
+}
+
+constexpr int kLDT = 68;  // T (<= 64 x 64, the doubling products' scratch) leading dimension
+// shared-memory doubles used by factor + invert: A (128 x kLDA), T (64 x kLDT), Sinv (128)
+constexpr int kSmemDoubles = 128 * kLDA + 64 * kLDT + 128;
+
+// Right-looking blocked Cholesky of the nbp x nbp lower block in A (strict upper
+// zero; nbp a multiple of 32, <= 128): L in place, Sinv[i] = 1 / L_ii.  A
+// non-positive pivot sets *bad_s.  Per 32-column step: warp 0 factors the
+// diagonal block in registers, the panel rows below by forward substitution (one
+// row per thread), the trailing lower triangle by a rank-32 DMMA update.
+QDWHG_DEV void factor(double* A, double* Sinv, int nbp, int* bad_s) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;  // DMMA fragment coordinates
+  const int nsb = nbp / kSB;
+  for (int kb = 0; kb < nsb; ++kb) {
+    const int b0 = kb * kSB;
+    if (warp == 0) {
+      // ---- factor the 32x32 diagonal block in registers: lane i owns row i.
+      // No division/sqrt library calls in here (their slow-path CALL would push
+      // the unrolled register rows to the stack): pivots use rsqrt_newton.
+      double row[kSB];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) row[c] = A[(b0 + c) * kLDA + b0 + lane];  // strict upper is 0
+      bool bad = false;
+      double my_inv = 0.0;
+      CholStep<0>::run(row, A + b0 * kLDA + b0, lane, bad, my_inv,
+                       __shfl_sync(0xffffffffu, row[0], 0));  // writes L in place
+      if (bad && lane == 0) *bad_s = 1;
+      Sinv[b0 + lane] = my_inv;
+    }
+    __syncthreads();
+    const int p0 = b0 + kSB, R = nbp - p0;
+    if (R > 0) {
+      // ---- panel rows by forward substitution, one row per thread:
+      // L(i, b0+c) = (Z(i, b0+c) - sum_{t<c} L(i, b0+t) L(b0+c, b0+t)) / L(b0+c, b0+c)
+      if (tid < R) {
+        const int i = p0 + tid;
+        double x[kSB];
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) x[c] = A[(b0 + c) * kLDA + i];
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) {
+          double s0 = x[c], s1 = 0.0;  // two chains: half the FMA latency
+#pragma unroll
+          for (int t = 0; t < c; ++t) {
+            const double l = A[(b0 + t) * kLDA + b0 + c];  // broadcast
+            if (t & 1) s1 -= x[t] * l;
+            else s0 -= x[t] * l;
+          }
+          x[c] = (s0 + s1) * Sinv[b0 + c];
+        }
+#pragma unroll
+        for (int c = 0; c < kSB; ++c) A[(b0 + c) * kLDA + i] = x[c];
+      }
+      __syncthreads();
+      // ---- trailing rank-32 update of the lower triangle on 8x8 DMMA tiles:
+      // A(i, j) -= sum_t L(i, b0+t) L(j, b0+t),  i >= j >= p0.  A work unit is
+      // one row tile x up to 4 column tiles (4 independent accumulator chains).
+      const int nt = R / 8;
+      int nunits = 0;
+      for (int ti = 0; ti < nt; ++ti) nunits += ti / 4 + 1;
+      for (int u = warp; u < nunits; u += kDiagThreads / 32) {
+        int ti = 0, rem = u;
+        while (rem >= ti / 4 + 1) {
+          rem -= ti / 4 + 1;
+          ++ti;
+        }
+        const int tj0 = 4 * rem;
+        const int i0 = p0 + 8 * ti;
+        double c[4][2];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int j0 = p0 + 8 * min(tj0 + v, ti);
+          c[v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
+          c[v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < kSB / 4; ++k4) {
+          const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
+          const double a = -lc[i0 + g];
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            dmma_8x8x4(c[v][0], c[v][1], a, lc[p0 + 8 * min(tj0 + v, ti) + g]);
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int tj = tj0 + v;
+          if (tj > ti) break;
+          const int j0 = p0 + 8 * tj;
+          if (tj != ti || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[v][0];
+          if (tj != ti || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[v][1];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// L^{-1} in place (lower) from the factored block: the 32x32 diagonal-block
+// inverses in parallel (one warp each), then recursive doubling over the
+// diagonal blocks, L^{-1}_QP = -Q^{-1} (L_QP P^{-1}), on DMMA tiles (T scratch).
+QDWHG_DEV void invert(double* A, double* T, const double* Sinv, int nbp) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const int nsb = nbp / kSB;
+  // ---- D_kb^{-1} (lower 32x32) of every diagonal block, one warp each, in place
+  if (warp < nsb) {
+    const int b0 = warp * kSB;
+    double x[kSB];
+    block_inverse(A + b0 * kLDA + b0, Sinv + b0, lane, x);
+    __syncwarp();
+    double* D = A + (b0 + lane) * kLDA + b0;  // column lane of the block (zeros above)
+#pragma unroll
+    for (int i = 0; i < kSB; ++i) D[i] = x[i];
+  }
+  __syncthreads();
+
+  // ---- L^{-1} by recursive doubling over the diagonal blocks: for each pair of
+  // adjacent groups (P = [a0, a0+h), Q = [a0+h, a0+2h)) with P^{-1}, Q^{-1} in
+  // place:  L^{-1}_QP = -Q^{-1} (L_QP P^{-1}).  Two levels for nb = 128, each
+  // two DMMA products over all pairs at once (a unit = one 8-row tile x 32 columns).
+  for (int h = kSB; h < nbp; h *= 2) {
+    const int npairs = (nbp - h + 2 * h - 1) / (2 * h);  // pairs with a non-empty Q
+    const int cgs = h / kSB;                             // 32-column groups per pair
+    int units = 0;
+    for (int p = 0; p < npairs; ++p) units += min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+    // phase 1: T_p = L_QP * P^{-1}   (P^{-1} lower: k >= column)
+    for (int u = warp; u < units; u += kDiagThreads / 32) {
+      int p = 0, rem = u;
+      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
+        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+        ++p;
+      }
+      const int ti = rem / cgs, cg = rem % cgs;
+      const int a0 = 2 * p * h, q0 = a0 + h;
+      double c[4][2] = {};
+      for (int k4 = 8 * cg; k4 < h / 4; ++k4) {
+        const int k = a0 + 4 * k4 + q;
+        const double a = A[k * kLDA + q0 + 8 * ti + g];
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+          dmma_8x8x4(c[tj][0], c[tj][1], a, A[(a0 + kSB * cg + 8 * tj + g) * kLDA + k]);
+      }
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int col = p * h + kSB * cg + 8 * tj + 2 * q;
+        T[col * kLDT + 8 * ti + g] = c[tj][0];
+        T[(col + 1) * kLDT + 8 * ti + g] = c[tj][1];
+      }
+    }
+    __syncthreads();
+    // phase 2: L^{-1}_QP = -Q^{-1} T_p   (Q^{-1} lower: k <= row), heaviest rows first
+    for (int u = warp; u < units; u += kDiagThreads / 32) {
+      int p = 0, rem = u;
+      while (rem >= min(h, nbp - (2 * p + 1) * h) / 8 * cgs) {
+        rem -= min(h, nbp - (2 * p + 1) * h) / 8 * cgs;
+        ++p;
+      }
+      const int nti = min(h, nbp - (2 * p + 1) * h) / 8;
+      const int ti = nti - 1 - rem / cgs, cg = rem % cgs;
+      const int a0 = 2 * p * h, q0 = a0 + h;
+      double c[4][2] = {};
+      for (int k4 = 0; k4 < 2 * (ti + 1); ++k4) {
+        const int k = 4 * k4 + q;
+        const double a = -A[(q0 + k) * kLDA + q0 + 8 * ti + g];
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+          dmma_8x8x4(c[tj][0], c[tj][1], a, T[(p * h + kSB * cg + 8 * tj + g) * kLDT + k]);
+      }
+#pragma unroll
+      for (int tj = 0; tj < 4; ++tj) {
+        const int col = a0 + kSB * cg + 8 * tj + 2 * q;
+        A[col * kLDA + q0 + 8 * ti + g] = c[tj][0];
+        A[(col + 1) * kLDA + q0 + 8 * ti + g] = c[tj][1];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace leaf
+}  // namespace qdwhg
