@@ -62,7 +62,7 @@ struct DagParams {
   unsigned* done;  // T*T completion counters (zero on entry, reset on exit)
   unsigned* ctrl;  // [0] queue head, [1] CTAs exited
   int* flag;       // set on a non-positive pivot
-  unsigned long long* trace;  // QDWHG_DAG_TRACE: per task {grab, ready, end, smid} (ns)
+  unsigned long long* trace;  // QDWHG_DAG_TRACE: per task {grab, ready, end, smid} (ns), clocks at ready/end
   unsigned long long* ltrace; // ... and per leaf {loaded, factored, inverted, written}
 };
 
@@ -257,8 +257,9 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
           while (ld_acquire_gpu(&p.done[tk.dep[0]]) < tk.cnt[0]) __nanosleep(20);
         __threadfence();
         if (p.trace) {
-          p.trace[4 * t] = tg;
-          p.trace[4 * t + 1] = globaltimer();
+          p.trace[6 * t] = tg;
+          p.trace[6 * t + 1] = globaltimer();
+          p.trace[6 * t + 4] = clock64();
         }
       }
       __syncthreads();
@@ -268,8 +269,9 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         __threadfence();
         red_release_add_gpu(&p.done[tk.slot], 1u);
         if (p.trace) {
-          p.trace[4 * t + 2] = globaltimer();
-          p.trace[4 * t + 3] = smid();
+          p.trace[6 * t + 2] = globaltimer();
+          p.trace[6 * t + 5] = clock64();
+          p.trace[6 * t + 3] = smid();
         }
       }
     }
@@ -288,8 +290,9 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
             while (ld_acquire_gpu(&p.done[tk.dep[d]]) < tk.cnt[d]) __nanosleep(32);
         __threadfence();
         if (p.trace) {
-          p.trace[4 * t] = tg;
-          p.trace[4 * t + 1] = globaltimer();
+          p.trace[6 * t] = tg;
+          p.trace[6 * t + 1] = globaltimer();
+          p.trace[6 * t + 4] = clock64();
         }
       }
       __syncthreads();
@@ -346,8 +349,9 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         __threadfence();
         red_release_add_gpu(&p.done[tk.slot], 1u);
         if (p.trace) {
-          p.trace[4 * t + 2] = globaltimer();
-          p.trace[4 * t + 3] = smid();
+          p.trace[6 * t + 2] = globaltimer();
+          p.trace[6 * t + 5] = clock64();
+          p.trace[6 * t + 3] = smid();
         }
       }
     }
@@ -592,7 +596,7 @@ void chol_dag(Ctx& ctx, const DMat& Z, const DMat& Winv) {
   static const char* trace_path = getenv("QDWHG_DAG_TRACE");
   p.trace = p.ltrace = nullptr;
   if (trace_path) {
-    if (!c.d_trace) QDWHG_CUDA(cudaMalloc(&c.d_trace, (size_t)c.ntasks * 4 * sizeof(unsigned long long)));
+    if (!c.d_trace) QDWHG_CUDA(cudaMalloc(&c.d_trace, (size_t)c.ntasks * 6 * sizeof(unsigned long long)));
     if (!c.d_ltrace) QDWHG_CUDA(cudaMalloc(&c.d_ltrace, (size_t)T * 4 * sizeof(unsigned long long)));
     p.trace = c.d_trace;
     p.ltrace = c.d_ltrace;
@@ -604,7 +608,7 @@ void chol_dag(Ctx& ctx, const DMat& Z, const DMat& Winv) {
   ctx.count();
   if (trace_path) {
     // debug: append {type,i,j,k,r0,nr, grab,ready,end,smid} rows of this launch
-    std::vector<unsigned long long> tr((size_t)c.ntasks * 4), lt((size_t)T * 4);
+    std::vector<unsigned long long> tr((size_t)c.ntasks * 6), lt((size_t)T * 4);
     QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
     QDWHG_CUDA(cudaMemcpy(tr.data(), c.d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
     QDWHG_CUDA(cudaMemcpy(lt.data(), c.d_ltrace, lt.size() * 8, cudaMemcpyDeviceToHost));
@@ -612,8 +616,8 @@ void chol_dag(Ctx& ctx, const DMat& Z, const DMat& Winv) {
       fprintf(f, "# launch T=%d ntasks=%d grid=%d\n", T, c.ntasks, grid);
       for (int t = 0; t < c.ntasks; ++t) {
         const DagTask& x = c.h_tasks[t];
-        fprintf(f, "%d %d %d %d %d %d %llu %llu %llu %llu\n", x.type, x.i, x.j, x.k, x.r0, x.nr, tr[4 * t],
-                tr[4 * t + 1], tr[4 * t + 2], tr[4 * t + 3]);
+        fprintf(f, "%d %d %d %d %d %d %llu %llu %llu %llu %llu\n", x.type, x.i, x.j, x.k, x.r0, x.nr, tr[6 * t],
+                tr[6 * t + 1], tr[6 * t + 2], tr[6 * t + 3], tr[6 * t + 5] - tr[6 * t + 4]);
       }
       for (int k = 0; k < T; ++k)
         fprintf(f, "L %d %llu %llu %llu %llu\n", k, lt[4 * k], lt[4 * k + 1], lt[4 * k + 2], lt[4 * k + 3]);

@@ -26,6 +26,10 @@ for r in last:
     a[0] += 1
     a[1] += (r[8] - r[7]) / 1e3
     a[2] += (r[7] - r[6]) / 1e3
+mhz = [r[10] / max(1, r[8] - r[7]) * 1e3 for r in last if len(r) > 10 and r[8] > r[7]]
+if mhz:
+    mhz.sort()
+    print(f"effective SM clock over tasks: median {mhz[len(mhz) // 2]:.0f} MHz (p10 {mhz[len(mhz) // 10]:.0f}, p90 {mhz[9 * len(mhz) // 10]:.0f})")
 for k, (n, run, wait) in sorted(agg.items()):
     print(f"{k[0]:7s} nr={k[1]:3d} n={n:6d} run avg {run / n:7.2f} us  wait avg {wait / n:7.2f} us  run total {run:9.1f}")
 busy = sum((r[8] - r[7]) for r in last) / 1e3
