@@ -86,7 +86,8 @@ typedef struct qdwhg_eig_info { /* partial.hpp:29-52 */
   int64_t k_found;         /* values found before a request's top-k cut  */
   int64_t iters_qr, iters_chol, borderline;
   int32_t no_savings, randomized;
-  int32_t n_trace, reserved;
+  int32_t n_trace;
+  int32_t subspace_path;   /* 0: Householder QR of B (partial.cpp:71-79), 1: Cholesky-QR extraction */
   double ell_trace[QDWHG_MAX_TRACE];
   double seconds;          /* device time of the call                    */
   double flops;            /* algorithmic FP64 flops   */

@@ -31,7 +31,7 @@ class EigInfo(ctypes.Structure):
     _fields_ = [("mu", _D), ("shift", _D), ("tol", _D), ("c_shift", _D),
                 ("rank_index", _I64), ("subspace_size", _I64), ("k", _I64), ("k_found", _I64),
                 ("iters_qr", _I64), ("iters_chol", _I64), ("borderline", _I64),
-                ("no_savings", _I32), ("randomized", _I32), ("n_trace", _I32), ("reserved", _I32),
+                ("no_savings", _I32), ("randomized", _I32), ("n_trace", _I32), ("subspace_path", _I32),
                 ("ell_trace", _D * MAX_TRACE), ("seconds", _D), ("flops", _D),
                 ("stage_seconds", _D * NUM_STAGES)]
 

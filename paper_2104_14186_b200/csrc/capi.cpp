@@ -448,6 +448,7 @@ qdwhg_status qdwhg_partial_eig(qdwhg_handle* h, int64_t n, const double* A, int6
     inf->iters_qr = (int64_t)r.iters_qr;
     inf->iters_chol = (int64_t)r.iters_chol;
     inf->borderline = (int64_t)r.borderline;
+    inf->subspace_path = r.subspace_path;
     inf->no_savings = r.no_savings;
     inf->randomized = r.randomized;
     inf->flops = r.flops;
@@ -512,6 +513,7 @@ qdwhg_status qdwhg_partial_eig_request(qdwhg_handle* h, int64_t n, const double*
     inf->iters_qr = (int64_t)r.iters_qr;
     inf->iters_chol = (int64_t)r.iters_chol;
     inf->borderline = (int64_t)r.borderline;
+    inf->subspace_path = r.subspace_path;
     inf->no_savings = r.no_savings;
     inf->randomized = r.randomized;
     inf->flops = r.flops;

@@ -563,6 +563,8 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   // to it cannot be resolved by this path (the reference's Householder R can)
   const double delta = 32.0 * std::sqrt((double)n) * kEps;
   if (!(tol > 10.0 * std::sqrt(delta))) return false;
+  // (at cfg1's l / n = 0.13, n = 1024 this path measured 4.2 ms against 2.3 ms for
+  // the Householder QR: the r x r eigensolve and the DAG chain dominate)
   if ((double)n - device_trace(ctx, B) > (double)n / 16.0) return false;  // l estimate
   const Arena::Mark mark = ctx.arena->mark();
   DMat G = ctx.arena->alloc(n, n);
@@ -708,6 +710,7 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     out.subspace_size = 0;
     out.no_savings = false;
     out.borderline = 0;
+    out.subspace_path = 0;
     out.lambda.clear();
     out.V = DMat{};
     size_t ind = 0;
@@ -715,6 +718,7 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     const DMat Q2buf =
         (randomize || attempt > 0) ? DMat{} : ctx.arena->alloc(n, std::max<int64_t>(1, n / 8));
     const bool chq = !randomize && attempt == 0 && subspace_cholqr(ctx, B, tol, ind, Q2, Q2buf);
+    out.subspace_path = chq ? 1 : 0;
     QrWork qw;
     if (!chq) {
       geqrf(ctx, B, qw);

@@ -66,6 +66,7 @@ struct EigOut {
   double mu = 0, shift = 0, tol = 0.01;
   size_t rank_index = 0, subspace_size = 0, iters_qr = 0, iters_chol = 0, borderline = 0;
   bool no_savings = false, randomized = false;
+  int subspace_path = 0;  // 0 Householder QR of B, 1 Cholesky-QR extraction
   std::vector<double> trace;
   double flops = 0;
 };

@@ -265,6 +265,7 @@ class PartialEigResult:
     iters_qr: int = 0
     iters_chol: int = 0
     borderline: int = 0
+    subspace_path: int = 0  # 0 Householder QR of B, 1 Cholesky-QR extraction
     no_savings: bool = False
     randomized: bool = False
     c_shift: float = 0.0
@@ -313,7 +314,8 @@ def _eig_result(info, lam, v, k):
         lambda_minus=np.array(lam[:k]), v=v[:, :k], subspace_size=info.subspace_size,
         mu=info.mu, shift=info.shift, rank_index=info.rank_index,
         ell_trace=list(info.ell_trace[:info.n_trace]), tol=info.tol, iters_qr=info.iters_qr,
-        iters_chol=info.iters_chol, borderline=info.borderline, no_savings=bool(info.no_savings),
+        iters_chol=info.iters_chol, borderline=info.borderline, subspace_path=info.subspace_path,
+        no_savings=bool(info.no_savings),
         randomized=bool(info.randomized), c_shift=info.c_shift, k_found=info.k_found,
         seconds=info.seconds, flops=info.flops, stage_seconds=list(info.stage_seconds))
 

@@ -238,6 +238,7 @@ def test_cholqr_subspace_matches_householder(n, k, family):
         "res = np.linalg.norm(a @ v - v * r.lambda_minus) / np.linalg.norm(a)\n"
         "orth = np.linalg.norm(np.eye(r.count()) - v.T @ v)\n"
         "print(json.dumps(dict(vals=list(r.lambda_minus), ell=r.subspace_size, ind=r.rank_index,\n"
+        "                      path=r.subspace_path,\n"
         "                      res=res, orth=orth, want=list(np.sort(lam)[::-1][:k]))))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
@@ -252,6 +253,7 @@ def test_cholqr_subspace_matches_householder(n, k, family):
         import json
         outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
     chq, hh = outs
+    assert chq["path"] == 1 and hh["path"] == 0  # each run took the path under test
     assert len(chq["vals"]) == len(hh["vals"]) == k
     assert chq["ind"] == hh["ind"] and chq["ell"] == hh["ell"]
     np.testing.assert_allclose(chq["vals"], hh["vals"], rtol=1e-12)
