@@ -21,6 +21,9 @@
  *   qdwhg_halley_weights     <- qdwh::halley_weights           polar.hpp:22
  *   qdwhg_iterations_to_converge <- qdwh::iterations_to_converge polar.hpp:30
  *   qdwhg_choose_shift       <- qdwh::choose_shift             partial.hpp:23
+ *   qdwhg_eig_full           <- qdwh::qdwh_eig_full            fullsolve.hpp:21
+ *   qdwhg_svd_full           <- qdwh::qdwh_svd_full            fullsolve.hpp:24
+ *   qdwhg_accuracy_report    <- qdwh::accuracy_report          metrics.hpp:25-28
  *
  * Conventions (mirroring the reference):
  *   - matrices are column-major FP64 with an explicit leading dimension;
@@ -114,7 +117,9 @@ typedef struct qdwhg_polar_config { /* polar.hpp:34-40 */
   double conv_eps;       /* 2.220446049250313e-16 */
   double chol_switch_c;  /* 100 */
   int32_t force_variant; /* 0 Auto, 1 QrOnly, 2 CholeskyOnly */
-  int32_t reserved;
+  int32_t estimate_ell0; /* 1: ell0 ignored, a lower bound of sigma_min(A)/||A||_2 is
+                            estimated from the R factor of A (no reference
+                            counterpart: polar.hpp:35 takes 1/kappa from the caller) */
 } qdwhg_polar_config;
 
 typedef struct qdwhg_polar_info { /* polar.hpp:42-50 */
@@ -218,6 +223,33 @@ qdwhg_status qdwhg_sym_eig_dense(qdwhg_handle* h, int64_t n, const double* S, in
                                  double* values, double* V, int64_t ldv);
 qdwhg_status qdwhg_svd_dense(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
                              double* U, int64_t ldu, double* sigma, double* V, int64_t ldv);
+/* Accuracy of a computed decomposition A ~ U diag(sigma) V^T (metrics.hpp:11-28,
+ * Eq. 5-7): orth = ||I - U^T U||_F / n, residuals = max per-pair 2-norms; sigma and
+ * delta (optional, may be NULL) are HOST arrays of length k; A m x n, U m x k, V n x k. */
+typedef struct qdwhg_accuracy {
+  double orth_left, orth_right;
+  double value_err;        /* valid when has_value_err */
+  double resid_right;      /* max ||A v_i - sigma_i u_i|| (paper pairing: the same)   */
+  double resid_left;       /* max ||A^T u_i - sigma_i v_i|| (paper: ||A u_i - sigma_i v_i||) */
+  int64_t n, k;
+  int32_t has_value_err, reserved;
+} qdwhg_accuracy;
+qdwhg_status qdwhg_accuracy_report(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                                   int64_t lda, int64_t k, const double* U, int64_t ldu,
+                                   const double* sigma, const double* V, int64_t ldv,
+                                   const double* delta, int32_t paper_pairing,
+                                   qdwhg_accuracy* out);
+
+/* Full spectrum (fullsolve.cpp:22-103): all eigenpairs of a symmetric A by QDWH
+ * spectral divide-and-conquer down to base_size (<= 0: the reference's 32),
+ * values ascending, V (n x n); *depth (may be NULL) = recursion depth reached.
+ * All singular triplets of A (m >= n) via the polar factor, sigma descending. */
+qdwhg_status qdwhg_eig_full(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                            int64_t base_size, double* lambda, double* V, int64_t ldv,
+                            int64_t* depth);
+qdwhg_status qdwhg_svd_full(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                            int64_t base_size, double* U, int64_t ldu, double* sigma, double* V,
+                            int64_t ldv);
 qdwhg_status qdwhg_two_norm_estimate(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
                                      int64_t lda, double* out);
 qdwhg_status qdwhg_lanczos_min_bound(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,

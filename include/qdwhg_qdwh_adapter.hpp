@@ -9,14 +9,20 @@
 //   qdwh::qdwh_partial_eig  partial.hpp:55-57
 //   qdwh::qdwh_partial_svd  partial.hpp:85-86
 //   qdwh::polar_decompose   polar.hpp:60
+//   qdwh::qdwh_eig_full / qdwh_svd_full   fullsolve.hpp:21-24
+//   qdwh::accuracy_report   metrics.hpp:25-28
 // The reference's own types (qdwh::DenseMatrix, ShiftPlan, PartialEigResult, ...)
 // are used unchanged; link with -lqdwhg (paper_2104_14186_b200/lib/libqdwhg.so).
 #pragma once
 
 #include <memory>
+#include <optional>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
+#include "qdwh/fullsolve.hpp"
+#include "qdwh/metrics.hpp"
 #include "qdwh/partial.hpp"
 #include "qdwh/polar.hpp"
 #include "qdwhg.h"
@@ -125,6 +131,60 @@ inline qdwh::PolarResult polar_decompose(const qdwh::DenseMatrix& a,
   r.iters_chol = static_cast<size_t>(info.iters_chol);
   r.ell_trace.assign(info.ell_trace, info.ell_trace + info.n_trace);
   r.converged = info.converged != 0;
+  return r;
+}
+
+inline qdwh::EigResult qdwh_eig_full(const qdwh::DenseMatrix& a, std::size_t base_size = 32) {
+  qdwhg_handle* h = thread_handle();
+  const int64_t n = static_cast<int64_t>(a.rows());
+  if (a.cols() != a.rows()) throw std::invalid_argument("qdwh_eig_full: matrix not square");
+  qdwh::EigResult r;
+  r.lambda.resize(n);
+  r.v = qdwh::DenseMatrix(n, n);
+  int64_t depth = 0;
+  throw_status(qdwhg_eig_full(h, n, a.data(), n, static_cast<int64_t>(base_size), r.lambda.data(),
+                              r.v.data(), n, &depth),
+               h);
+  r.depth = static_cast<std::size_t>(depth);
+  return r;
+}
+
+inline qdwh::SvdResult qdwh_svd_full(const qdwh::DenseMatrix& a, std::size_t base_size = 32) {
+  qdwhg_handle* h = thread_handle();
+  const int64_t m = static_cast<int64_t>(a.rows()), n = static_cast<int64_t>(a.cols());
+  qdwh::SvdResult r;
+  r.u = qdwh::DenseMatrix(m, n);
+  r.sigma.resize(n);
+  r.v = qdwh::DenseMatrix(n, n);
+  throw_status(qdwhg_svd_full(h, m, n, a.data(), m, static_cast<int64_t>(base_size), r.u.data(), m,
+                              r.sigma.data(), r.v.data(), n),
+               h);
+  return r;
+}
+
+inline qdwh::AccuracyReport accuracy_report(const qdwh::DenseMatrix& a, const qdwh::DenseMatrix& u,
+                                            const std::vector<double>& sigma, const qdwh::DenseMatrix& v,
+                                            const std::optional<std::vector<double>>& delta = std::nullopt,
+                                            bool paper_pairing = false) {
+  qdwhg_handle* h = thread_handle();
+  if (delta && delta->size() != sigma.size())
+    throw std::invalid_argument("accuracy_report: delta length differs from sigma");
+  qdwhg_accuracy out{};
+  throw_status(qdwhg_accuracy_report(h, static_cast<int64_t>(a.rows()), static_cast<int64_t>(a.cols()),
+                                     a.data(), static_cast<int64_t>(a.rows()),
+                                     static_cast<int64_t>(sigma.size()), u.data(),
+                                     static_cast<int64_t>(u.rows()), sigma.data(), v.data(),
+                                     static_cast<int64_t>(v.rows()), delta ? delta->data() : nullptr,
+                                     paper_pairing ? 1 : 0, &out),
+               h);
+  qdwh::AccuracyReport r;
+  r.orth_left = out.orth_left;
+  r.orth_right = out.orth_right;
+  if (out.has_value_err) r.value_err = out.value_err;
+  r.resid_right = out.resid_right;
+  r.resid_left = out.resid_left;
+  r.n = static_cast<std::size_t>(out.n);
+  r.k = static_cast<std::size_t>(out.k);
   return r;
 }
 

@@ -663,6 +663,89 @@ def qdwh_partial_svd(a: np.ndarray, s: float, tol: float = 0.01,
 
 
 # ---------------------------------------------------------------- flop model
+# ------------------------------------------------------------------ full spectrum + metrics
+_SPLIT_SEED = 0x73706C6974  # fullsolve.cpp:14 kSplitSeed
+
+
+def _eig_recurse(a: np.ndarray, base: int):
+    """fullsolve.cpp:22-72"""
+    n = a.shape[0]
+    if n <= base:
+        lam, v = sym_eig_dense(a)
+        return lam, v, 0
+    sigma = np.trace(a) / n
+    shifted = a - sigma * np.eye(n)
+    if np.linalg.norm(shifted) <= 10.0 * n * EPS * max(1.0, abs(sigma)):  # fullsolve.cpp:31-38
+        return np.full(n, sigma), np.eye(n), 0
+    polar = polar_decompose(shifted, ell0=1e-15)  # fullsolve.cpp:40
+    c = symmetrize(-0.5 * polar.up + 0.5 * np.eye(n))
+    k = int(round(np.trace(c)))
+    if k == 0 or k >= n:
+        lam, v = sym_eig_dense(a)
+        return lam, v, 0
+    q, _ = qr_factor(c @ gaussian_matrix(n, n, _SPLIT_SEED))
+    v_lo, v_hi = q[:, :k], q[:, k:]
+    lo = _eig_recurse(symmetrize(v_lo.T @ (a @ v_lo)), base)
+    hi = _eig_recurse(symmetrize(v_hi.T @ (a @ v_hi)), base)
+    return (np.concatenate([lo[0], hi[0]]), np.hstack([v_lo @ lo[1], v_hi @ hi[1]]),
+            1 + max(lo[2], hi[2]))
+
+
+def qdwh_eig_full(a: np.ndarray, base_size: int = 32):
+    """fullsolve.cpp:76-80 -> (ascending lambda, V, depth)."""
+    require_finite(a, "qdwh_eig_full")
+    if a.shape[0] != a.shape[1]:
+        raise ValueError("qdwh_eig_full: matrix not square")
+    return _eig_recurse(symmetrize(a), max(base_size, 2))
+
+
+def qdwh_svd_full(a: np.ndarray, base_size: int = 32):
+    """fullsolve.cpp:82-103 -> (U, sigma descending, V)."""
+    require_finite(a, "qdwh_svd_full")
+    if a.shape[0] < a.shape[1]:
+        raise ValueError("qdwh_svd_full: requires rows >= cols")
+    polar = polar_decompose(a)
+    lam, w, _ = qdwh_eig_full(polar.h, base_size)
+    u_full = polar.up @ w
+    return u_full[:, ::-1].copy(), np.maximum(lam[::-1], 0.0), w[:, ::-1].copy()
+
+
+def accuracy_report(a, u, sigma, v, delta=None, paper_pairing=False):
+    """metrics.cpp:58-100 (Eq. 5-7) -> [orth_left, orth_right, value_err (NaN: none),
+    resid_right, resid_left]."""
+    a, u, v = (np.asarray(x, dtype=np.float64) for x in (a, u, v))
+    sigma = np.asarray(sigma, dtype=np.float64)
+    k = sigma.shape[0]
+    if u.shape[1] != k or v.shape[1] != k:
+        raise ValueError("accuracy_report: sigma length must match U and V columns")
+    if u.shape[0] != a.shape[0] or v.shape[0] != a.shape[1]:
+        raise ValueError("accuracy_report: factor shapes do not conform with A")
+    if paper_pairing and a.shape[0] != a.shape[1]:
+        raise ValueError("accuracy_report: paper pairing needs a square A")
+    nd = max(a.shape[1], 1)
+
+    def gram_defect(x):  # metrics.cpp:10-24
+        return np.linalg.norm(np.eye(x.shape[1]) - x.T @ x)
+
+    def max_pair(x, y, op):  # metrics.cpp:26-55
+        r = op @ x - y * sigma[None, :]
+        return float(np.max(np.linalg.norm(r, axis=0))) if k else 0.0
+
+    out = np.zeros(5)
+    out[0], out[1] = gram_defect(u) / nd, gram_defect(v) / nd
+    if delta is None:
+        out[2] = np.nan
+    else:
+        delta = np.asarray(delta, dtype=np.float64)
+        num, den = np.sum((sigma - delta) ** 2), np.sum(delta ** 2)
+        out[2] = np.sqrt(num / den) if den > 0 else np.sqrt(num)
+    if paper_pairing:
+        out[4], out[3] = max_pair(u, v, a), max_pair(v, u, a)
+    else:
+        out[3], out[4] = max_pair(v, u, a), max_pair(u, v, a.T)
+    return out
+
+
 def flops_partial_eig(n: int, ell: int, k: int, it_chol: int, randomized: bool) -> float:
     """Algorithmic FP64 count: SYRK n^3 + POTRF n^3/3 + 2 TRSM 2n^3
     per Cholesky step, GEQRF 4/3 n^3, Q2 formation 2n^2 l - 2l^3/3, A Q2 2n^2 l,

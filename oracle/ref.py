@@ -53,6 +53,9 @@ def _lib():
             "ref_run_fixed_iterations": [_I, _I, _P, _D, _I, ctypes.c_int, _P, _P],
             "ref_gen_sym_eig_test": [_I, _I, _U, _P, _P],
             "ref_gen_svd_test": [_I, _U, _P, _P],
+            "ref_eig_full": [_I, _P, _I, _P, _P, _P],
+            "ref_svd_full": [_I, _I, _P, _I, _P, _P, _P],
+            "ref_accuracy_report": [_I, _I, _P, _I, _P, _P, _P, _P, ctypes.c_int, _P],
         }
         for name, args in sig.items():
             f = getattr(lib, name)
@@ -241,3 +244,40 @@ def gen_svd_test(n, seed):
     d = np.zeros(n)
     _check(_lib().ref_gen_svd_test(n, seed, _ptr(a), _ptr(d)))
     return a, d
+
+
+def eig_full(a, base_size=32):
+    """fullsolve.hpp:21 -> (ascending lambda, V, depth)."""
+    a = _f(a)
+    n = a.shape[0]
+    lam = np.zeros(n)
+    v = np.zeros((n, n), order="F")
+    depth = ctypes.c_int64(0)
+    _check(_lib().ref_eig_full(n, a.ctypes.data, base_size, lam.ctypes.data, v.ctypes.data,
+                               ctypes.byref(depth)))
+    return lam, v, depth.value
+
+
+def svd_full(a, base_size=32):
+    """fullsolve.hpp:24 -> (U, sigma descending, V)."""
+    a = _f(a)
+    m, n = a.shape
+    u = np.zeros((m, n), order="F")
+    v = np.zeros((n, n), order="F")
+    s = np.zeros(n)
+    _check(_lib().ref_svd_full(m, n, a.ctypes.data, base_size, u.ctypes.data, s.ctypes.data,
+                               v.ctypes.data))
+    return u, s, v
+
+
+def accuracy_report(a, u, sigma, v, delta=None, paper_pairing=False):
+    """metrics.hpp:25-28 -> [orth_left, orth_right, value_err (NaN: none), resid_right, resid_left]."""
+    a, u, v = _f(a), _f(u), _f(v)
+    sg = np.ascontiguousarray(sigma, dtype=np.float64)
+    dl = None if delta is None else np.ascontiguousarray(delta, dtype=np.float64)
+    out = np.zeros(5)
+    _check(_lib().ref_accuracy_report(a.shape[0], a.shape[1], a.ctypes.data, sg.shape[0], u.ctypes.data,
+                                      sg.ctypes.data, v.ctypes.data,
+                                      dl.ctypes.data if dl is not None else None, int(paper_pairing),
+                                      out.ctypes.data))
+    return out

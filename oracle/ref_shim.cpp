@@ -7,16 +7,23 @@
 //   qdwh::qdwh_partial_eig   (partial.hpp:55-57, partial.cpp:40-99)
 //   qdwh::qdwh_partial_svd   (partial.hpp:85-86, partial.cpp:101-158)
 //   qdwh::polar_decompose    (polar.hpp:60,      polar.cpp:130-177)
+//   qdwh::qdwh_eig_full / qdwh_svd_full (fullsolve.hpp:21-24), qdwh::accuracy_report
+//   (metrics.hpp:25-28)
 // plus the kernels/scalars the parity tests pin one by one.
 // Status codes mirror include/qdwhg.h: 0 ok, 1 invalid_argument,
 // 2 NotPositiveDefinite, 3 NotConverged, 8 other.
 #include <cstdint>
 #include <cstring>
+#include <limits>
+#include <optional>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
+#include "qdwh/fullsolve.hpp"
 #include "qdwh/kernels.hpp"
 #include "qdwh/matgen.hpp"
+#include "qdwh/metrics.hpp"
 #include "qdwh/partial.hpp"
 #include "qdwh/polar.hpp"
 
@@ -233,6 +240,41 @@ int ref_gen_svd_test(int64_t n, uint64_t seed, double* a, double* d) {
     SvdTestMatrix g = gen_svd_test(n, Seed{seed});
     store(g.a, a);
     for (int64_t i = 0; i < n; ++i) d[i] = g.d[i];
+  });
+}
+
+int ref_eig_full(int64_t n, const double* a, int64_t base, double* lambda, double* v, int64_t* depth) {
+  return guard([&] {
+    EigResult r = qdwh_eig_full(load(a, n, n), static_cast<size_t>(base));
+    for (int64_t i = 0; i < n; ++i) lambda[i] = r.lambda[i];
+    store(r.v, v);
+    *depth = static_cast<int64_t>(r.depth);
+  });
+}
+
+int ref_svd_full(int64_t m, int64_t n, const double* a, int64_t base, double* u, double* sigma, double* v) {
+  return guard([&] {
+    SvdResult r = qdwh_svd_full(load(a, m, n), static_cast<size_t>(base));
+    for (int64_t i = 0; i < n; ++i) sigma[i] = r.sigma[i];
+    store(r.u, u);
+    store(r.v, v);
+  });
+}
+
+// out: [0] orth_left [1] orth_right [2] value_err (NaN if none) [3] resid_right [4] resid_left
+int ref_accuracy_report(int64_t m, int64_t n, const double* a, int64_t k, const double* u,
+                        const double* sigma, const double* v, const double* delta, int paper,
+                        double* out) {
+  return guard([&] {
+    std::vector<double> sg(sigma, sigma + k);
+    std::optional<std::vector<double>> dl;
+    if (delta) dl = std::vector<double>(delta, delta + k);
+    AccuracyReport r = accuracy_report(load(a, m, n), load(u, m, k), sg, load(v, n, k), dl, paper != 0);
+    out[0] = r.orth_left;
+    out[1] = r.orth_right;
+    out[2] = r.value_err ? *r.value_err : std::numeric_limits<double>::quiet_NaN();
+    out[3] = r.resid_right;
+    out[4] = r.resid_left;
   });
 }
 

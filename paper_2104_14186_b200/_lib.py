@@ -45,9 +45,15 @@ class SvdInfo(ctypes.Structure):
                 ("stage_seconds", _D * NUM_STAGES)]
 
 
+class Accuracy(ctypes.Structure):
+    _fields_ = [("orth_left", _D), ("orth_right", _D), ("value_err", _D), ("resid_right", _D),
+                ("resid_left", _D), ("n", _I64), ("k", _I64), ("has_value_err", _I32),
+                ("reserved", _I32)]
+
+
 class PolarConfigC(ctypes.Structure):
     _fields_ = [("ell0", _D), ("max_iters", _I64), ("conv_eps", _D), ("chol_switch_c", _D),
-                ("force_variant", _I32), ("reserved", _I32)]
+                ("force_variant", _I32), ("estimate_ell0", _I32)]
 
 
 class PolarInfo(ctypes.Structure):
@@ -95,6 +101,9 @@ SIGNATURES = {
     "qdwhg_sym_eig_dense": [_P, _I64, _P, _I64, _P, _P, _I64],
     "qdwhg_svd_dense": [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _I64],
     "qdwhg_two_norm_estimate": [_P, _I64, _I64, _P, _I64, _P],
+    "qdwhg_eig_full": [_P, _I64, _P, _I64, _I64, _P, _P, _I64, _P],
+    "qdwhg_svd_full": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _I64],
+    "qdwhg_accuracy_report": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _I32, _P],
     "qdwhg_lanczos_min_bound": [_P, _I64, _P, _I64, _I64, _P],
     "qdwhg_gemm": [_P, _I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64],
     "qdwhg_gemm_ex": [_P, _I32, _I32, _I64, _I64, _I64, _D, _P, _I64, _P, _I64, _D, _P, _I64, _I32,

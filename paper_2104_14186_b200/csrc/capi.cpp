@@ -620,6 +620,8 @@ qdwhg_status qdwhg_polar(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
       pc.chol_switch_c = cfg->chol_switch_c;
       pc.force_variant = cfg->force_variant;
     }
+    // estimate_ell0: l0 from the R factor of A (no caller-supplied 1/kappa)
+    if (cfg && cfg->estimate_ell0) pc.ell0 = polar_ell0_estimate(ctx, Ad);
     DMat Upd = ctx.arena->alloc(m, n);
     DMat Hd = ctx.arena->alloc(n, n);
     PolarOut r = polar_decompose(ctx, Ad, pc, Upd, Hd);
@@ -758,6 +760,72 @@ qdwhg_status qdwhg_svd_dense(qdwhg_handle* h, int64_t m, int64_t n, const double
     DMat Ud = ctx.arena->alloc(m, n), Vd = ctx.arena->alloc(n, n);
     std::vector<double> sg;
     svd_polar(ctx, Ad, Ud, sg, Vd);
+    copy_vec_out(ctx, sg, sigma);
+    stage_out(ctx, Ud, U, ldu);
+    stage_out(ctx, Vd, V, ldv);
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_accuracy_report(qdwhg_handle* h, int64_t m, int64_t n, const double* A,
+                                   int64_t lda, int64_t k, const double* U, int64_t ldu,
+                                   const double* sigma, const double* V, int64_t ldv,
+                                   const double* delta, int32_t paper_pairing, qdwhg_accuracy* out) {
+  if (!h || !out) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("accuracy_report: empty matrix");
+    if (k < 0 || (k > 0 && (!U || !V || !sigma))) throw InvalidArgument("accuracy_report: missing factors");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    const int64_t kk = std::max<int64_t>(k, 1);
+    DMat Ud = k > 0 ? stage_in(ctx, U, m, k, ldu, nullptr) : ctx.arena->alloc(m, kk).col_block(0, 0);
+    DMat Vd = k > 0 ? stage_in(ctx, V, n, k, ldv, nullptr) : ctx.arena->alloc(n, kk).col_block(0, 0);
+    std::vector<double> sg(sigma, sigma + k);
+    const AccuracyOut r = accuracy_report(ctx, Ad, Ud, sg, Vd, delta, paper_pairing != 0);
+    std::memset(out, 0, sizeof(*out));
+    out->orth_left = r.orth_left;
+    out->orth_right = r.orth_right;
+    out->value_err = r.value_err;
+    out->has_value_err = r.has_value_err;
+    out->resid_right = r.resid_right;
+    out->resid_left = r.resid_left;
+    out->n = r.n;
+    out->k = r.k;
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_eig_full(qdwhg_handle* h, int64_t n, const double* A, int64_t lda,
+                            int64_t base_size, double* lambda, double* V, int64_t ldv, int64_t* depth) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (n < 1 || !A) throw InvalidArgument("qdwh_eig_full: empty matrix");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, n, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0) throw InvalidArgument("qdwh_eig_full: non-finite entry");
+    DMat Vd = ctx.arena->alloc(n, n);
+    std::vector<double> vals;
+    const int64_t d = eig_full(ctx, Ad, base_size > 0 ? base_size : 32, vals, Vd);
+    copy_vec_out(ctx, vals, lambda);
+    stage_out(ctx, Vd, V, ldv);
+    if (depth) *depth = d;
+    QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  });
+}
+
+qdwhg_status qdwhg_svd_full(qdwhg_handle* h, int64_t m, int64_t n, const double* A, int64_t lda,
+                            int64_t base_size, double* U, int64_t ldu, double* sigma, double* V,
+                            int64_t ldv) {
+  if (!h) return QDWHG_INVALID_ARGUMENT;
+  return guard(h, [&] {
+    if (m < 1 || n < 1 || !A) throw InvalidArgument("qdwh_svd_full: empty matrix");
+    if (m < n) throw InvalidArgument("qdwh_svd_full: requires rows >= cols");
+    Ctx& ctx = h->ctx;
+    DMat Ad = stage_in(ctx, A, m, n, lda, nullptr);
+    if (mat_stats(ctx, Ad, false).nonfinite > 0) throw InvalidArgument("qdwh_svd_full: non-finite entry");
+    DMat Ud = ctx.arena->alloc(m, n), Vd = ctx.arena->alloc(n, n);
+    std::vector<double> sg;
+    svd_full(ctx, Ad, base_size > 0 ? base_size : 32, Ud, sg, Vd);
     copy_vec_out(ctx, sg, sigma);
     stage_out(ctx, Ud, U, ldu);
     stage_out(ctx, Vd, V, ldv);

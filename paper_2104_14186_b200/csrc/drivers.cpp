@@ -423,6 +423,124 @@ static void syev_dc(Ctx& ctx, const DMat& A, std::vector<double>& vals, const DM
 bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout, double vlo,
                   double vhi, int64_t* sel0);
 
+// ----------------------------------------------------------------- full-spectrum drivers
+// qdwh_eig_full (fullsolve.cpp:22-80): shift by the trace mean, split with the
+// spectral projector C = (I - Up)/2 of the QDWH polar factor, a QR of C Omega
+// (the reference's fixed split seed at every depth) for the two invariant
+// subspaces, Rayleigh-Ritz on each, recursion down to base_size and a dense
+// finish (the device eigensolver) on the leaves; no split (k = 0 or n) also
+// finishes densely.  Every O(n^3) step is a DMMA GEMM / QDWH iteration.
+static int64_t eig_full_rec(Ctx& ctx, const DMat& A, int64_t base, std::vector<double>& vals,
+                            const DMat& Vout) {
+  const int64_t n = A.rows;
+  if (n <= base) {
+    syev(ctx, A, vals, Vout);
+    return 0;
+  }
+  const Arena::Mark mark = ctx.arena->mark();
+  const double sigma0 = device_trace(ctx, A) / (double)n;
+  DMat Sh = ctx.arena->alloc(n, n);
+  DMat Up = ctx.arena->alloc(n, n);
+  // the reference's shift is the trace mean; when it lands on an eigenvalue
+  // (trace(C) not an integer: that direction is split between the two subspaces,
+  // which are then not invariant) the next candidate is tried — points between
+  // the mean and the Frobenius spread, as in syev_dc
+  const double spread = std::sqrt(mat_stats(ctx, A, false).fro2 / (double)n);
+  const double cand[5] = {sigma0, sigma0 + 0.01 * spread, sigma0 - 0.01 * spread, sigma0 + 0.1 * spread,
+                          sigma0 - 0.1 * spread};
+  int64_t k = 0;
+  for (int attempt = 0; attempt < 5; ++attempt) {
+    const double sigma = cand[attempt];
+    axpby_identity(ctx, A, 1.0, -sigma, Sh);
+    if (attempt == 0 && std::sqrt(mat_stats(ctx, Sh, false).fro2) <=
+                            10.0 * (double)n * kEps * std::max(1.0, std::abs(sigma))) {
+      // constant-diagonal block: the shift exhausted the spectrum (fullsolve.cpp:31-38)
+      vals.assign(n, sigma);
+      fill(ctx, Vout, 0.0, 1.0);
+      ctx.arena->release_to(mark);
+      return 0;
+    }
+    PolarCfg cfg;
+    cfg.ell0 = 1e-15;  // fullsolve.cpp:40: no condition estimate, the safe bound
+    DMat none;
+    polar_decompose(ctx, Sh, cfg, Up, none);
+    symmetrize_scale(ctx, Up, -0.5, 0.5, Up);  // C = sym((I - Up)/2)
+    const double tr = device_trace(ctx, Up);
+    k = std::llround(tr);
+    static const bool dbg = getenv("QDWHG_DEBUG_FULL") != nullptr;
+    if (dbg) fprintf(stderr, "eig_full n=%ld attempt=%d sigma=%.17g trace(C)=%.17g\n", (long)n, attempt, sigma, tr);
+    // a clean split leaves trace(C) an integer to rounding; an eigenvalue within
+    // ~l0 ||A|| of the shift is only partly mapped by QDWH (C keeps a fractional
+    // eigenvalue, 0.046 measured on a singular shift) and splits its vector
+    if (std::abs(tr - (double)k) < 1e-6) break;
+    k = -1;  // ambiguous: an eigenvalue at the shift
+  }
+  if (k <= 0 || k >= n) {
+    ctx.arena->release_to(mark);
+    syev(ctx, A, vals, Vout);
+    return 0;
+  }
+  DMat Om = ctx.arena->alloc(n, n);
+  gaussian_fill(ctx, Om, 0x73706c6974ull);  // kSplitSeed (fullsolve.cpp:14)
+  DMat CO = ctx.arena->alloc(n, n);
+  gemm(ctx, Op::N, Op::N, 1.0, Up, Om, 0.0, CO);
+  QrWork qw;
+  geqrf(ctx, CO, qw);
+  DMat Q = ctx.arena->alloc(n, n);
+  orgqr_cols(ctx, qw, n, n, 0, Q);
+  const DMat Vlo = Q.sub(0, 0, n, k), Vhi = Q.sub(0, k, n, n - k);
+  DMat T = ctx.arena->alloc(n, std::max(k, n - k));
+  DMat Alo = ctx.arena->alloc(k, k), Ahi = ctx.arena->alloc(n - k, n - k);
+  GemmExtra rr;  // Rayleigh quotients V^T (A V): lower tiles, mirrored (exactly symmetric)
+  rr.out = OutMode::LowerMirror;
+  gemm(ctx, Op::N, Op::N, 1.0, A, Vlo, 0.0, T.sub(0, 0, n, k));
+  gemm(ctx, Op::T, Op::N, 1.0, Vlo, T.sub(0, 0, n, k), 0.0, Alo, rr);
+  gemm(ctx, Op::N, Op::N, 1.0, A, Vhi, 0.0, T.sub(0, 0, n, n - k));
+  gemm(ctx, Op::T, Op::N, 1.0, Vhi, T.sub(0, 0, n, n - k), 0.0, Ahi, rr);
+  DMat Wlo = ctx.arena->alloc(k, k), Whi = ctx.arena->alloc(n - k, n - k);
+  std::vector<double> vlo, vhi;
+  const int64_t dlo = eig_full_rec(ctx, Alo, base, vlo, Wlo);
+  const int64_t dhi = eig_full_rec(ctx, Ahi, base, vhi, Whi);
+  gemm(ctx, Op::N, Op::N, 1.0, Vlo, Wlo, 0.0, Vout.sub(0, 0, n, k));
+  gemm(ctx, Op::N, Op::N, 1.0, Vhi, Whi, 0.0, Vout.sub(0, k, n, n - k));
+  vals = vlo;
+  vals.insert(vals.end(), vhi.begin(), vhi.end());
+  ctx.arena->release_to(mark);
+  return 1 + std::max(dlo, dhi);
+}
+
+int64_t eig_full(Ctx& ctx, const DMat& A, int64_t base_size, std::vector<double>& vals, const DMat& Vout) {
+  const int64_t n = A.rows;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat S = ctx.arena->alloc(n, n);
+  symmetrize_scale(ctx, A, 1.0, 0.0, S);  // fullsolve.cpp:78: symmetrize(a)
+  const int64_t depth = eig_full_rec(ctx, S, std::max<int64_t>(base_size, 2), vals, Vout);
+  ctx.arena->release_to(mark);
+  return depth;
+}
+
+// qdwh_svd_full (fullsolve.cpp:82-103): A = Up H, H = V diag(sigma) V^T by
+// eig_full, U = Up V; descending order, negative rounding-level values clamped.
+void svd_full(Ctx& ctx, const DMat& A, int64_t base_size, const DMat& U, std::vector<double>& sigma,
+              const DMat& V) {
+  const int64_t m = A.rows, n = A.cols;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat Up = ctx.arena->alloc(m, n), H = ctx.arena->alloc(n, n), W = ctx.arena->alloc(n, n);
+  PolarCfg cfg;  // polar.hpp defaults (ell0 = 1e-15)
+  polar_decompose(ctx, A, cfg, Up, H);
+  std::vector<double> lam;
+  eig_full(ctx, H, base_size, lam, W);
+  sigma.resize(n);
+  std::vector<int> order(n);
+  for (int64_t j = 0; j < n; ++j) {
+    sigma[j] = std::max(lam[n - 1 - j], 0.0);
+    order[j] = (int)(n - 1 - j);
+  }
+  permute_cols(ctx, W, order, V);
+  gemm(ctx, Op::N, Op::N, 1.0, Up, V, 0.0, U);
+  ctx.arena->release_to(mark);
+}
+
 void syev(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat& Vout) {
   int64_t i0;
   syev_range(ctx, S, vals, Vout, -INFINITY, INFINITY, &i0);
@@ -460,6 +578,45 @@ int64_t syev_range(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMa
   return i1 - i0;
 }
 
+// A lower bound of sigma_min(R) / alpha for an upper-triangular R (the QDWH l0,
+// polar.hpp:35 leaves it to the caller with a 1e-15 default): from R^-1 (one
+// triangular inverse, ~n^3/3 flops) sigma_min(R) = 1 / ||R^-1||_2, estimated by
+// the power iteration with a 2x safety margin and floored by the guaranteed
+// 1 / ||R^-1||_F.  Falls back to 1e-15 when R is singular to working precision.
+double ell0_lower_bound(Ctx& ctx, const DMat& R, double alpha) {
+  const int64_t n = R.rows;
+  double l0 = 1e-15;
+  const Arena::Mark m2 = ctx.arena->mark();
+  DMat Ri = ctx.arena->alloc(n, n);
+  if (trtri_upper(ctx, R, Ri)) {
+    const MatStats st = mat_stats(ctx, Ri, false);
+    if (st.nonfinite == 0 && st.fro2 > 0) {
+      const double inv2 = two_norm_estimate(ctx, Ri);  // ~||R^-1||_2 (x1.05)
+      const double lb = std::max(1.0 / (std::sqrt(st.fro2) * alpha), 1.0 / (2.0 * inv2 * alpha));
+      if (std::isfinite(lb) && lb > l0) l0 = std::min(1.0, lb);
+    }
+  }
+  ctx.arena->release_to(m2);
+  return l0;
+}
+
+// l0 for polar_decompose(A) when the caller has none: the R factor of a
+// Householder QR of A (sigma(R) = sigma(A)), then ell0_lower_bound against the
+// polar's own alpha.
+double polar_ell0_estimate(Ctx& ctx, const DMat& A) {
+  const int64_t m = A.rows, n = A.cols;
+  const Arena::Mark mark = ctx.arena->mark();
+  DMat Aw = ctx.arena->alloc(m, n);
+  copy(ctx, A, Aw);
+  QrWork qw;
+  geqrf(ctx, Aw, qw);
+  DMat R = ctx.arena->alloc(n, n);
+  copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
+  const double l0 = ell0_lower_bound(ctx, R, two_norm_estimate(ctx, A));
+  ctx.arena->release_to(mark);
+  return l0;
+}
+
 int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& sigma, const DMat& V,
                   double cut, double ell0) {
   // fullsolve.cpp:82-103: A = Up H, H = W diag W^T, U = Up W, descending order.
@@ -478,27 +635,10 @@ int64_t svd_polar(Ctx& ctx, const DMat& A, const DMat& U, std::vector<double>& s
     QrWork qw;
     geqrf(ctx, Aw, qw);
     copy(ctx, Aw.sub(0, 0, n, n), R);  // upper triangle (zeros below from the panels)
-    // l0 for the polar of R: a lower bound of sigma_min(R / alpha) from R^-1
-    // (one triangular inverse, ~n^3/3 flops): sigma_min(R) = 1 / ||R^-1||_2,
-    // estimated by the power iteration with a 2x safety margin, floored by the
-    // guaranteed 1 / ||R^-1||_F.  A good l0 saves QDWH iterations, the QR-based
-    // ones above all (iterations_to_converge: 1e-15 -> 2 QR + 4 Cholesky steps,
-    // 1e-4 -> 1 QR + 3 Cholesky steps).
-    double l0 = 1e-15;
-    {
-      const Arena::Mark m2 = ctx.arena->mark();
-      DMat Ri = ctx.arena->alloc(n, n);
-      if (trtri_upper(ctx, R, Ri)) {
-        const MatStats st = mat_stats(ctx, Ri, false);
-        if (st.nonfinite == 0 && st.fro2 > 0) {
-          const double alpha = two_norm_estimate(ctx, R);  // the polar's own (deterministic) alpha
-          const double inv2 = two_norm_estimate(ctx, Ri);   // ~||R^-1||_2 (x1.05)
-          const double lb = std::max(1.0 / (std::sqrt(st.fro2) * alpha), 1.0 / (2.0 * inv2 * alpha));
-          if (std::isfinite(lb) && lb > l0) l0 = std::min(1.0, lb);
-        }
-      }
-      ctx.arena->release_to(m2);
-    }
+    // l0 for the polar of R: a lower bound of sigma_min(R / alpha) (saves QDWH
+    // iterations, the QR-based ones above all: iterations_to_converge gives
+    // 1e-15 -> 2 QR + 4 Cholesky steps, 1e-4 -> 1 QR + 3 Cholesky steps)
+    const double l0 = ell0_lower_bound(ctx, R, two_norm_estimate(ctx, R));
     const int64_t k = svd_polar(ctx, R, U.sub(0, 0, n, n), sigma, V, cut, l0);
     // U = Q [U_R; 0]: the reflectors applied to U_R directly (no explicit Q,
     // no m x n x k GEMM)

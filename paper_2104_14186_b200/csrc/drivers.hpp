@@ -53,6 +53,23 @@ struct PolarCfg {
 // polar.cpp:130-177.  Up (m x n) and H (n x n, optional: H.base == nullptr to skip).
 PolarOut polar_decompose(Ctx& ctx, const DMat& A, const PolarCfg& cfg, const DMat& Up,
                          const DMat& H);
+// Full-spectrum drivers (fullsolve.cpp:76-103): all eigenpairs (ascending) by QDWH
+// spectral divide-and-conquer down to base_size (returns the depth); all singular
+// triplets (descending) via the polar factor.
+int64_t eig_full(Ctx& ctx, const DMat& A, int64_t base_size, std::vector<double>& vals, const DMat& Vout);
+void svd_full(Ctx& ctx, const DMat& A, int64_t base_size, const DMat& U, std::vector<double>& sigma,
+              const DMat& V);
+// metrics.cpp:58-100 (accuracy_report) on the device.
+struct AccuracyOut {
+  double orth_left = 0, orth_right = 0, value_err = 0, resid_right = 0, resid_left = 0;
+  bool has_value_err = false;
+  int64_t n = 0, k = 0;
+};
+AccuracyOut accuracy_report(Ctx& ctx, const DMat& A, const DMat& U, const std::vector<double>& sigma,
+                            const DMat& V, const double* delta, bool paper_pairing);
+// Lower bound of sigma_min(A) / ||A||_2 for the polar's l0 (QR of A, R^-1 power iteration).
+double polar_ell0_estimate(Ctx& ctx, const DMat& A);
+double ell0_lower_bound(Ctx& ctx, const DMat& R, double alpha);
 
 // svd_dense (kernels.cpp:217-330) restated for the device as polar + EIG
 // (fullsolve.cpp:82-103): U (m x n), sigma descending (host), V (n x n).

@@ -582,6 +582,9 @@ class PolarConfig:
     conv_eps: float = EPS
     chol_switch_c: float = 100.0
     force_variant: str = "Auto"  # Auto | QrOnly | CholeskyOnly
+    # (no reference counterpart) ignore ell0 and estimate a lower bound of
+    # sigma_min(A)/||A||_2 from the R factor of A
+    estimate_ell0: bool = False
 
 
 @dataclass
@@ -610,7 +613,8 @@ def polar_decompose(a, cfg: Optional[PolarConfig] = None, *,
     upp, ldu = _ptr_ld(Up)
     hp, ldh = _ptr_ld(H)
     c = _lib.PolarConfigC(cfg.ell0, cfg.max_iters, cfg.conv_eps, cfg.chol_switch_c,
-                          {"Auto": 0, "QrOnly": 1, "CholeskyOnly": 2}[cfg.force_variant], 0)
+                          {"Auto": 0, "QrOnly": 1, "CholeskyOnly": 2}[cfg.force_variant],
+                          int(bool(cfg.estimate_ell0)))
     info = _lib.PolarInfo()
     h.check(h.lib.qdwhg_polar(h.h, m, n, A.ptr, A.ld, ctypes.byref(c), upp, ldu, hp, ldh,
                               ctypes.byref(info)))
@@ -718,6 +722,92 @@ def svd_dense(a, *, handle: Optional[Handle] = None):
     vp, ldv = _ptr_ld(V)
     h.check(h.lib.qdwhg_svd_dense(h.h, m, n, A.ptr, A.ld, up, ldu, sig.ctypes.data, vp, ldv))
     return U, sig, V
+
+
+@dataclass
+class FullEigResult:
+    """fullsolve.hpp:7-11"""
+    lam: np.ndarray  # ascending
+    v: object
+    depth: int = 0
+
+
+@dataclass
+class FullSvdResult:
+    """fullsolve.hpp:13-17"""
+    u: object
+    sigma: np.ndarray  # descending
+    v: object
+
+
+def qdwh_eig_full(a, base_size: int = 32, *, handle: Optional[Handle] = None) -> FullEigResult:
+    """fullsolve.hpp:21 — every eigenpair by QDWH spectral divide-and-conquer."""
+    h = handle or default_handle()
+    A = _Mat(a)
+    n = A.shape[0]
+    if A.shape[1] != n:
+        raise ValueError("qdwh_eig_full: matrix not square")
+    lam = np.zeros(n)
+    V = _empty_like_kind(A, n, n)
+    vp, ldv = _ptr_ld(V)
+    depth = ctypes.c_int64(0)
+    h.check(h.lib.qdwhg_eig_full(h.h, n, A.ptr, A.ld, int(base_size), lam.ctypes.data, vp, ldv,
+                                 ctypes.byref(depth)))
+    return FullEigResult(lam=lam, v=V, depth=depth.value)
+
+
+def qdwh_svd_full(a, base_size: int = 32, *, handle: Optional[Handle] = None) -> FullSvdResult:
+    """fullsolve.hpp:24 — every singular triplet via the polar factor (m >= n)."""
+    h = handle or default_handle()
+    A = _Mat(a)
+    m, n = A.shape
+    U = _empty_like_kind(A, m, n)
+    V = _empty_like_kind(A, n, n)
+    sig = np.zeros(n)
+    up, ldu = _ptr_ld(U)
+    vp, ldv = _ptr_ld(V)
+    h.check(h.lib.qdwhg_svd_full(h.h, m, n, A.ptr, A.ld, int(base_size), up, ldu, sig.ctypes.data,
+                                 vp, ldv))
+    return FullSvdResult(u=U, sigma=sig, v=V)
+
+
+@dataclass
+class AccuracyReport:
+    """metrics.hpp:11-20"""
+    orth_left: float
+    orth_right: float
+    value_err: Optional[float]
+    resid_right: float
+    resid_left: float
+    n: int
+    k: int
+
+
+def accuracy_report(a, u, sigma, v, delta=None, paper_pairing: bool = False, *,
+                    handle: Optional[Handle] = None) -> AccuracyReport:
+    """metrics.hpp:25-28 (Eq. 5-7) on the device.  For a symmetric eigenreport pass
+    u = v and the eigenvalues as sigma."""
+    h = handle or default_handle()
+    A = _Mat(a)
+    m, n = A.shape
+    sig = np.ascontiguousarray(np.asarray(sigma, dtype=np.float64).reshape(-1))
+    k = sig.shape[0]
+    dl = None if delta is None else np.ascontiguousarray(np.asarray(delta, dtype=np.float64).reshape(-1))
+    if dl is not None and dl.shape[0] != k:
+        raise ValueError("accuracy_report: delta length differs from sigma")
+    U = _Mat(u) if k else None
+    V = _Mat(v) if k else None
+    if k and (U.shape[1] != k or V.shape[1] != k):
+        raise ValueError("accuracy_report: sigma length must match U and V columns")
+    if k and (U.shape[0] != m or V.shape[0] != n):
+        raise ValueError("accuracy_report: factor shapes do not conform with A")
+    out = _lib.Accuracy()
+    h.check(h.lib.qdwhg_accuracy_report(
+        h.h, m, n, A.ptr, A.ld, k, U.ptr if U else None, U.ld if U else 1, sig.ctypes.data,
+        V.ptr if V else None, V.ld if V else 1, dl.ctypes.data if dl is not None else None,
+        int(bool(paper_pairing)), ctypes.byref(out)))
+    return AccuracyReport(out.orth_left, out.orth_right, out.value_err if out.has_value_err else None,
+                          out.resid_right, out.resid_left, out.n, out.k)
 
 
 def two_norm_estimate(a, *, handle: Optional[Handle] = None) -> float:

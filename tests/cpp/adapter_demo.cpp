@@ -29,6 +29,18 @@ int main() {
   }
   for (size_t i = 0; i < rs.count(); ++i)
     worst = std::fmax(worst, std::fabs(rs.sigma1[i] - gs.sigma1[i]) / rs.sigma1[i]);
+  // full-spectrum driver and the Eq. 5-7 report (fullsolve.hpp, metrics.hpp)
+  const qdwh::EigResult rf = qdwh::qdwh_eig_full(gen.a, 32);
+  const qdwh::EigResult gf = qdwhg::qdwh_eig_full(gen.a, 32);
+  for (size_t i = 0; i < rf.lambda.size(); ++i)
+    worst = std::fmax(worst, std::fabs(rf.lambda[i] - gf.lambda[i]) / std::fmax(1.0, std::fabs(rf.lambda[i])));
+  const qdwh::AccuracyReport ra = qdwh::accuracy_report(sg.a, rs.u1, rs.sigma1, rs.v1);
+  const qdwh::AccuracyReport ga = qdwhg::accuracy_report(sg.a, rs.u1, rs.sigma1, rs.v1);
+  const double scale = std::fmax(ra.resid_right, 1e-300);
+  if (std::fabs(ra.resid_right - ga.resid_right) > 1e-6 * scale + 1e-15 || ra.k != ga.k) {
+    std::printf("FAIL accuracy_report %.3e vs %.3e\n", ra.resid_right, ga.resid_right);
+    return 1;
+  }
   bool threw = false;
   try {
     qdwhg::qdwh_partial_svd(sg.a, 1.5);

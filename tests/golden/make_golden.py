@@ -160,9 +160,41 @@ def wishart_cases():
         eig_case(f"eig_cfg4_wishart_n{n}", b, shift_c=c, k_want=k, keep_v=(n <= 512))
 
 
+def full_cases():
+    """fullsolve.cpp (qdwh_eig_full / qdwh_svd_full) and metrics.cpp
+    (accuracy_report) run through the reference itself: a 96 x 96 symmetric
+    matrix with a spread spectrum and a cluster (two levels of spectral
+    divide-and-conquer at base 32), a 72 x 48 SVD, and the Eq. 5-7 report of a
+    perturbed partial decomposition in both pairings."""
+    n = 96
+    lam = np.concatenate([np.linspace(-3.0, -0.5, 40), np.full(16, 0.25), np.linspace(1.0, 4.0, 40)])
+    a = sym_with_eigs(lam, 77)
+    lam_r, v_r, depth = R.eig_full(a, 32)
+    save("full_eig", a=a, base=32, planted=lam, lam=lam_r, v=v_r, depth=depth)
+    sig = np.logspace(0, -6, 48)
+    b = with_spectrum(np.concatenate([sig, np.zeros(0)]), 78, 79)[:, :48]
+    b = np.vstack([b, 1e-3 * R.gaussian_matrix(24, 48, 80)])
+    u_r, s_r, vv_r = R.svd_full(b, 32)
+    save("full_svd", a=b, base=32, u=u_r, sigma=s_r, v=vv_r)
+    # metrics: a k = 10 partial SVD of b from the reference's full SVD, perturbed
+    k = 10
+    pu = u_r[:, :k] + 1e-9 * R.gaussian_matrix(b.shape[0], k, 81)
+    pv = vv_r[:, :k] + 1e-9 * R.gaussian_matrix(b.shape[1], k, 82)
+    ps = s_r[:k] * (1 + 1e-10 * np.arange(k))
+    rep = R.accuracy_report(b, pu, ps, pv, s_r[:k], False)
+    sq = a  # square case for the paper pairing: the symmetric eigen report (U = V)
+    ev = v_r[:, -k:] + 1e-9 * R.gaussian_matrix(n, k, 83)
+    rep_p = R.accuracy_report(sq, ev, lam_r[-k:], ev, None, True)
+    save("metrics", a=b, u=pu, sigma=ps, v=pv, delta=s_r[:k], report=rep, a_sq=sq, v_sq=ev,
+         lam_sq=lam_r[-k:], report_paper=rep_p)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "wishart":
         wishart_cases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "full":
+        full_cases()
     else:
         main()
         wishart_cases()
+        full_cases()

@@ -1,0 +1,76 @@
+"""Full-spectrum drivers (fullsolve.cpp) and the Eq. 5-7 accuracy report
+(metrics.cpp) on the device, against the reference's own outputs
+(tests/golden/full_*.npz, metrics.npz from tests/golden/make_golden.py) and, at
+sizes the reference would take minutes on, against LAPACK and the oracle."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import qdwh_oracle as O
+from paper_2104_14186_b200 import qdwh
+from test_oracle_pins import _same_subspaces
+
+pytestmark = pytest.mark.gpu
+
+
+def test_eig_full_matches_reference():
+    g = golden("full_eig")
+    r = qdwh.qdwh_eig_full(g["a"], int(g["base"]))
+    assert r.depth == int(g["depth"])
+    np.testing.assert_allclose(r.lam, g["lam"], rtol=0, atol=1e-12 * np.abs(g["lam"]).max())
+    v = np.asarray(r.v)
+    _same_subspaces(v, g["v"], g["lam"], 1e-10)
+    n = v.shape[0]
+    assert np.linalg.norm(g["a"] @ v - v * r.lam) <= 1e-12 * np.sqrt(n) * np.linalg.norm(g["a"])
+    assert np.linalg.norm(np.eye(n) - v.T @ v) <= 1e-12 * np.sqrt(n)
+
+
+def test_svd_full_matches_reference():
+    g = golden("full_svd")
+    r = qdwh.qdwh_svd_full(g["a"], int(g["base"]))
+    np.testing.assert_allclose(r.sigma, g["sigma"], rtol=1e-10, atol=1e-14)
+    u, v = np.asarray(r.u), np.asarray(r.v)
+    _same_subspaces(v, g["v"], g["sigma"], 1e-8)
+    a = g["a"]
+    assert np.linalg.norm(a @ v - u * r.sigma) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(np.eye(v.shape[1]) - v.T @ v) <= 1e-12 * np.sqrt(v.shape[1])
+
+
+@pytest.mark.parametrize("n,base", [(700, 32), (1024, 160), (259, 160)])
+def test_eig_full_large(n, base):
+    # two clusters + a continuum: several split levels; LAPACK values as truth.  At
+    # n = 259 (odd continuum) the trace-mean shift of a sub-block lands exactly on an
+    # eigenvalue: the split must move to the next candidate shift
+    m8 = n // 8
+    lam = np.concatenate([np.full(m8, -1.0), np.linspace(-0.5, 0.5, n - 2 * m8), np.full(m8, 2.0)])
+    if n == 259:
+        lam = np.linspace(-0.44, 0.12, n)
+    q, _ = np.linalg.qr(O.gaussian_matrix(n, n, 91))
+    a = (q * lam) @ q.T
+    a = 0.5 * (a + a.T)
+    r = qdwh.qdwh_eig_full(a, base)
+    assert r.depth >= 1
+    np.testing.assert_allclose(r.lam, np.linalg.eigvalsh(a), rtol=0, atol=1e-12 * 2.0 * np.sqrt(n))
+    v = np.asarray(r.v)
+    assert np.linalg.norm(a @ v - v * r.lam) <= 1e-12 * np.sqrt(n) * np.linalg.norm(a)
+    assert np.linalg.norm(np.eye(n) - v.T @ v) <= 1e-12 * np.sqrt(n)
+
+
+def test_accuracy_report_matches_reference():
+    g = golden("metrics")
+    rep = qdwh.accuracy_report(g["a"], g["u"], g["sigma"], g["v"], g["delta"])
+    got = [rep.orth_left, rep.orth_right, rep.value_err, rep.resid_right, rep.resid_left]
+    np.testing.assert_allclose(got, g["report"], rtol=1e-6)
+    rep = qdwh.accuracy_report(g["a_sq"], g["v_sq"], g["lam_sq"], g["v_sq"], paper_pairing=True)
+    assert rep.value_err is None
+    got = [rep.orth_left, rep.orth_right, rep.resid_right, rep.resid_left]
+    np.testing.assert_allclose(got, np.delete(g["report_paper"], 2), rtol=1e-6)
+    assert (rep.n, rep.k) == (g["a_sq"].shape[1], len(g["lam_sq"]))
+
+
+def test_accuracy_report_errors():
+    a = O.gaussian_matrix(8, 6, 3)
+    with pytest.raises(ValueError):
+        qdwh.accuracy_report(a, np.zeros((8, 2)), [1.0, 2.0, 3.0], np.zeros((6, 3)))
+    with pytest.raises(ValueError):
+        qdwh.accuracy_report(a, np.zeros((8, 2)), [1.0, 2.0], np.zeros((6, 2)), paper_pairing=True)

@@ -257,6 +257,27 @@ def test_polar_matches_reference(name):
     assert np.array_equal(p.h, p.h.T)
 
 
+@pytest.mark.parametrize("m,n,cond", [(300, 200, 1e8), (256, 256, 1e4)])
+def test_polar_estimated_ell0(m, n, cond):
+    """estimate_ell0: a certified lower bound of sigma_min(A)/||A||_2
+    from the R factor, fewer QDWH iterations than the 1e-15 default, same polar factor."""
+    u, _ = np.linalg.qr(O.gaussian_matrix(m, n, 61))
+    v, _ = np.linalg.qr(O.gaussian_matrix(n, n, 62))
+    sig = np.logspace(0, -np.log10(cond), n)
+    a = (u * sig) @ v.T
+    p0 = qdwh.polar_decompose(a)
+    pe = qdwh.polar_decompose(a, qdwh.PolarConfig(estimate_ell0=True))
+    ell0 = pe.ell_trace[0] * 1.10  # the trace starts at ell0 / 1.10 (polar.cpp:137)
+    assert 0.0 < ell0 <= sig[-1] / sig[0] * 1.0000001
+    assert ell0 >= 0.1 * sig[-1] / sig[0]  # within the 2x power-iteration margin (+ alpha)
+    assert pe.iters_qr + pe.iters_chol < p0.iters_qr + p0.iters_chol
+    # H is well conditioned (perturbations ~ u ||A||); Up moves by ~ u kappa
+    assert np.abs(pe.h - p0.h).max() < 1e-12
+    assert np.abs(pe.up - p0.up).max() < 1e-14 * cond
+    assert np.linalg.norm(pe.up @ pe.h - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.linalg.norm(pe.up.T @ pe.up - np.eye(n)) / np.sqrt(n) <= 1e-13
+
+
 def test_polar_config_errors():
     a = O.gaussian_matrix(4, 4, 51)
     with pytest.raises(ValueError):

@@ -154,3 +154,46 @@ def test_live_reference_matches_oracle_small():
     s, _, _, d = R.partial_svd(a, 0.1)
     r = O.qdwh_partial_svd(a, 0.1)
     np.testing.assert_allclose(r.sigma1, s, rtol=1e-10)
+
+
+def _same_subspaces(v, w, lam, tol):
+    """Columns of v and w span the same eigenspaces: per group of equal values
+    (a cluster is compared through its projector, single values up to sign)."""
+    i = 0
+    n = len(lam)
+    while i < n:
+        j = i + 1
+        while j < n and abs(lam[j] - lam[i]) <= 1e-9 * max(1.0, abs(lam[i])):
+            j += 1
+        p = v[:, i:j] @ v[:, i:j].T
+        q = w[:, i:j] @ w[:, i:j].T
+        assert np.abs(p - q).max() <= tol, (i, j, np.abs(p - q).max())
+        i = j
+
+
+def test_oracle_eig_full_pinned():
+    # fullsolve.cpp:22-80 restated vs the reference's own qdwh_eig_full (two split levels)
+    g = golden("full_eig")
+    lam, v, depth = O.qdwh_eig_full(g["a"], int(g["base"]))
+    assert depth == int(g["depth"]) == 2
+    np.testing.assert_allclose(lam, g["lam"], rtol=0, atol=1e-12 * np.abs(g["lam"]).max())
+    _same_subspaces(v, g["v"], g["lam"], 1e-10)
+    np.testing.assert_allclose(g["lam"], np.sort(g["planted"]), atol=1e-12 * 4)
+
+
+def test_oracle_svd_full_pinned():
+    g = golden("full_svd")
+    u, s, v = O.qdwh_svd_full(g["a"], int(g["base"]))
+    np.testing.assert_allclose(s, g["sigma"], rtol=1e-10, atol=1e-14)
+    _same_subspaces(v, g["v"], g["sigma"], 1e-8)
+    _same_subspaces(u, g["u"], g["sigma"], 1e-8)
+
+
+def test_oracle_accuracy_report_pinned():
+    # metrics.cpp:58-100 (Eq. 5-7), both residual pairings, with and without delta
+    g = golden("metrics")
+    rep = O.accuracy_report(g["a"], g["u"], g["sigma"], g["v"], g["delta"], False)
+    np.testing.assert_allclose(rep, g["report"], rtol=1e-6)
+    rep = O.accuracy_report(g["a_sq"], g["v_sq"], g["lam_sq"], g["v_sq"], None, True)
+    assert np.isnan(rep[2]) and np.isnan(g["report_paper"][2])
+    np.testing.assert_allclose(np.delete(rep, 2), np.delete(g["report_paper"], 2), rtol=1e-6)
