@@ -565,11 +565,22 @@ def main():
                             "measured": "CUDA events around each GEMM launch (on its own stream) in a "
                                         "second pass of the same steps (events in the value pass would "
                                         "block PDL); achieved = flops / union of the launch intervals"}
+        if kst.get("dag_seconds", 0) > 0:
+            # the second kernel of the step: the persistent tile-DAG Cholesky-and-inverse
+            # (chol_dag_kernel), algorithmic 2/3 n^3 per n x n factorisation + inverse
+            da = kst["dag_flops"] / kst["dag_seconds"] / 1e12
+            line["roofline"]["second_kernel"] = {
+                "kernel": "chol_dag_kernel (persistent tile-DAG Cholesky-and-inverse, DMMA.8x8x4)",
+                "achieved": da, "frac": da / FP64_PEAK_TFLOPS,
+                "launches_per_step": kst["dag_timed_launches"] / args.steps,
+                "share_of_step": kst["dag_seconds"] / prof_t,
+                "bound": "latency (leaf-tile chain) / tensor"}
         # DRAM bytes per GEMM launch from the committed `ncu --set full` capture of
         # this config's solve (tools/ncu_gemm_traffic.py), when present
-        tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                          f"r01_gemm_traffic_cfg{args.config}.json")
-        if os.path.exists(tp):
+        pdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+        cands = sorted(f for f in os.listdir(pdir) if f.endswith(f"_gemm_traffic_cfg{args.config}.json"))
+        tp = os.path.join(pdir, cands[-1]) if cands else ""
+        if tp and os.path.exists(tp):
             tr = json.load(open(tp))
             line["roofline"]["traffic"] = tr["traffic_bytes_per_launch_time_weighted"]
             line["roofline"]["traffic_note"] = (
@@ -650,6 +661,15 @@ def verify(inp, res):
         vals = np.array(res.sigma1)
     n = A.shape[1]
     out["gate_sqrt_n"] = 1e-12 * float(np.sqrt(n))
+    # the reference's own accuracy report (metrics.cpp, Eq. 5-7: ||I - U^T U||_F / n and
+    # max per-pair residual 2-norms), computed on the device by qdwhg_accuracy_report
+    from paper_2104_14186_b200 import qdwh
+    if inp["kind"] == "eig":
+        rep = qdwh.accuracy_report(A, V, vals, V)
+    else:
+        rep = qdwh.accuracy_report(A, U, vals, V)
+    out["eq5_7"] = {"orth_left": rep.orth_left, "orth_right": rep.orth_right,
+                    "resid_right": rep.resid_right, "resid_left": rep.resid_left}
     if inp.get("truth") is not None and len(inp["truth"]) == k:
         out["max_rel_err_vs_planted"] = float(np.max(np.abs(vals - inp["truth"]) / np.abs(inp["truth"])))
     return out

@@ -178,6 +178,9 @@ typedef struct qdwhg_kernel_stats {
   double gemm_seconds;          /* sum of event-timed GEMM durations */
   double gemm_flops;            /* sum of algorithmic flops of those launches */
   double gemm_busy_seconds;     /* union of the launch intervals (concurrent launches counted once) */
+  uint64_t dag_timed_launches;  /* tile-DAG Cholesky-and-inverse launches, since the last call */
+  double dag_seconds;           /* their event-timed durations */
+  double dag_flops;             /* algorithmic flops: 2/3 n^3 per n x n factorisation + inverse */
 } qdwhg_kernel_stats;
 qdwhg_status qdwhg_profile(qdwhg_handle* h, int32_t enable);
 /* Toggle QDWHG_FLAG_DETERMINISTIC on an existing handle. */

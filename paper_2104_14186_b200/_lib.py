@@ -63,7 +63,8 @@ class PolarInfo(ctypes.Structure):
 
 class KernelStats(ctypes.Structure):
     _fields_ = [("gemm_launches", _U64), ("other_launches", _U64), ("gemm_timed_launches", _U64),
-                ("gemm_seconds", _D), ("gemm_flops", _D), ("gemm_busy_seconds", _D)]
+                ("gemm_seconds", _D), ("gemm_flops", _D), ("gemm_busy_seconds", _D),
+                ("dag_timed_launches", _U64), ("dag_seconds", _D), ("dag_flops", _D)]
 
 
 class EigRequest(ctypes.Structure):

@@ -101,9 +101,11 @@ DMat Arena::alloc(int64_t rows, int64_t cols) {
   return m;
 }
 
-void Ctx::prof_begin(double flops, const std::string& tag) {
+void Ctx::prof_begin(double flops, const std::string& tag, int kind) {
   ev_tag.resize(ev_used + 1);
   ev_tag[ev_used] = tag;
+  ev_kind.resize(ev_used + 1);
+  ev_kind[ev_used] = kind;
   if (ev_pool.size() < 2 * (ev_used + 1)) {
     for (int i = 0; i < 512; ++i) {
       cudaEvent_t e;
@@ -125,15 +127,18 @@ void Ctx::prof_collect() {
   QDWHG_CUDA(cudaEventSynchronize(ev_pool[2 * ev_used - 1]));
   static const char* log_path = getenv("QDWHG_PROFILE_LOG");
   FILE* log = log_path ? fopen(log_path, "a") : nullptr;
-  // union of the launch intervals (GEMMs on the main and side streams may run
-  // concurrently: the busy time must not count the overlap twice)
-  std::vector<std::pair<float, float>> iv(ev_used);
+  // union of the GEMM launch intervals (GEMMs on the main and side streams may
+  // run concurrently: the busy time must not count the overlap twice)
+  std::vector<std::pair<float, float>> iv;
   for (size_t i = 0; i < ev_used; ++i) {
-    QDWHG_CUDA(cudaEventElapsedTime(&iv[i].first, ev_pool[0], ev_pool[2 * i]));
-    QDWHG_CUDA(cudaEventElapsedTime(&iv[i].second, ev_pool[0], ev_pool[2 * i + 1]));
+    if (ev_kind[i] != 0) continue;
+    float s = 0.f, e = 0.f;
+    QDWHG_CUDA(cudaEventElapsedTime(&s, ev_pool[0], ev_pool[2 * i]));
+    QDWHG_CUDA(cudaEventElapsedTime(&e, ev_pool[0], ev_pool[2 * i + 1]));
+    iv.emplace_back(s, e);
   }
   std::sort(iv.begin(), iv.end());
-  {
+  if (!iv.empty()) {
     float cs = iv[0].first, ce = iv[0].second;
     for (size_t i = 1; i < iv.size(); ++i) {
       if (iv[i].first > ce) {
@@ -149,14 +154,20 @@ void Ctx::prof_collect() {
   for (size_t i = 0; i < ev_used; ++i) {
     float ms = 0.f;
     QDWHG_CUDA(cudaEventElapsedTime(&ms, ev_pool[2 * i], ev_pool[2 * i + 1]));
-    gemm_ms += ms;
-    gemm_flops += ev_flops[i];
+    if (ev_kind[i] == 0) {
+      gemm_ms += ms;
+      gemm_flops += ev_flops[i];
+      ++gemm_timed;
+    } else {
+      dag_ms += ms;
+      dag_flops += ev_flops[i];
+      ++dag_timed;
+    }
     if (log)
       fprintf(log, "%s ms=%.4f gflop=%.4f tf=%.2f\n", ev_tag[i].c_str(), ms, ev_flops[i] * 1e-9,
               ms > 0 ? ev_flops[i] / ms * 1e-9 : 0.0);
   }
   if (log) fclose(log);
-  gemm_timed += ev_used;
   ev_used = 0;
 }
 
@@ -405,6 +416,12 @@ qdwhg_status qdwhg_get_kernel_stats(qdwhg_handle* h, qdwhg_kernel_stats* out) {
     out->gemm_seconds = h->ctx.gemm_ms * 1e-3;
     out->gemm_flops = h->ctx.gemm_flops;
     out->gemm_busy_seconds = h->ctx.gemm_busy_ms * 1e-3;
+    out->dag_timed_launches = h->ctx.dag_timed;
+    out->dag_seconds = h->ctx.dag_ms * 1e-3;
+    out->dag_flops = h->ctx.dag_flops;
+    h->ctx.dag_timed = 0;
+    h->ctx.dag_ms = 0.0;
+    h->ctx.dag_flops = 0.0;
     h->ctx.gemm_timed = 0;
     h->ctx.gemm_ms = 0.0;
     h->ctx.gemm_busy_ms = 0.0;

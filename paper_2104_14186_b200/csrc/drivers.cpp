@@ -467,8 +467,6 @@ static int64_t eig_full_rec(Ctx& ctx, const DMat& A, int64_t base, std::vector<d
     symmetrize_scale(ctx, Up, -0.5, 0.5, Up);  // C = sym((I - Up)/2)
     const double tr = device_trace(ctx, Up);
     k = std::llround(tr);
-    static const bool dbg = getenv("QDWHG_DEBUG_FULL") != nullptr;
-    if (dbg) fprintf(stderr, "eig_full n=%ld attempt=%d sigma=%.17g trace(C)=%.17g\n", (long)n, attempt, sigma, tr);
     // a clean split leaves trace(C) an integer to rounding; an eigenvalue within
     // ~l0 ||A|| of the shift is only partly mapped by QDWH (C keeps a fractional
     // eigenvalue, 0.046 measured on a singular shift) and splits its vector

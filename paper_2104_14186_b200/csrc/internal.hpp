@@ -129,10 +129,13 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<double> ev_flops;  // algorithmic flops of launch i (events 2i, 2i+1)
   std::vector<std::string> ev_tag;  // per-launch shape tag (QDWHG_PROFILE_LOG)
+  std::vector<int> ev_kind;          // 0 GEMM engine, 1 tile-DAG Cholesky
   size_t ev_used = 0;
   double gemm_ms = 0.0, gemm_flops = 0.0, gemm_busy_ms = 0.0;
   uint64_t gemm_timed = 0;
-  void prof_begin(double flops, const std::string& tag = std::string());
+  double dag_ms = 0.0, dag_flops = 0.0;
+  uint64_t dag_timed = 0;
+  void prof_begin(double flops, const std::string& tag = std::string(), int kind = 0);
   void prof_end();
   void prof_collect();
 };

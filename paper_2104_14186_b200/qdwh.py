@@ -95,7 +95,9 @@ class Handle:
         self.check(self.lib.qdwhg_get_kernel_stats(self.h, ctypes.byref(st)))
         return dict(gemm_launches=st.gemm_launches, other_launches=st.other_launches,
                     gemm_timed_launches=st.gemm_timed_launches, gemm_seconds=st.gemm_seconds,
-                    gemm_flops=st.gemm_flops, gemm_busy_seconds=st.gemm_busy_seconds)
+                    gemm_flops=st.gemm_flops, gemm_busy_seconds=st.gemm_busy_seconds,
+                    dag_timed_launches=st.dag_timed_launches, dag_seconds=st.dag_seconds,
+                    dag_flops=st.dag_flops)
 
     def close(self):
         if self.h:

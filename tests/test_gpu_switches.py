@@ -66,7 +66,12 @@ out["syev"] = dict(err=float(np.max(np.abs(vals - np.sort(ls)))),
 print(json.dumps(out))
 """
 
-SWITCHES = [("QDWHG_CHOL_NO_LAUUM", "1"), ("QDWHG_CHOL_NO_OVERLAP", "1"), ("QDWHG_CHOL_STABLE", "1"),
+SWITCHES = [("QDWHG_CHOL_NO_LAUUM", "1"), ("QDWHG_CHOL_STABLE", "1"),
+            # the recursive Cholesky-and-inverse with the Z22 side-stream overlap (n = 3072
+            # runs the tile-DAG kernel by default), with and without the overlap; DAG
+            # sub-trees of <= 8 tiles under the recursion
+            ("QDWHG_CHOL_NO_DAG", "1"), ("QDWHG_CHOL_NO_DAG,QDWHG_CHOL_NO_OVERLAP", "1"),
+            ("QDWHG_CHOL_DAG_TMAX", "8"),
             ("QDWHG_GEMM_NO_BALANCE", "1"), ("QDWHG_JACOBI_MAX", "8"), ("QDWHG_NO_PDL", "1"),
             ("QDWHG_NO_PRIORITY", "1"), ("QDWHG_PANEL_CAP", "32"), ("QDWHG_PANEL_SMEM", "1"),
             ("QDWHG_POTRF_NB", "64"), ("QDWHG_QR_NBO", "128"), ("QDWHG_QR_NO_LOOKAHEAD", "1"),
@@ -76,7 +81,7 @@ SWITCHES = [("QDWHG_CHOL_NO_LAUUM", "1"), ("QDWHG_CHOL_NO_OVERLAP", "1"), ("QDWH
 
 @pytest.mark.parametrize("var,val", SWITCHES)
 def test_switched_path(var, val):
-    env = dict(os.environ, PYTHONPATH=ROOT, **{var: val})
+    env = dict(os.environ, PYTHONPATH=ROOT, **{v: val for v in var.split(",")})
     p = subprocess.run([sys.executable, "-c", SNIPPET], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
