@@ -42,7 +42,6 @@ struct GemmParams {
   int kmode;   // KRange
   int omode;   // OutMode
   int tiles_m, tiles_n;
-  int band;         // tile-row band of the full-K rasterisation (12)
   int splits;       // split-K factor (1 = fused epilogue)
   double* partial;  // splits x (M x N) raw partials (ld = M) when splits > 1
   // batch item b (blockIdx.y): TMA coordinates += b * (x_bs0, x_bs1), D/Cin += b * stride
@@ -124,27 +123,14 @@ QDWHG_DEV void tile_coords(const GemmParams& p, int bid, int& tm, int& tn) {
       tn = bid % p.tiles_n;
       tm = bid / p.tiles_n;
       break;
-    default: {
-      // full K range: bands of p.band tile-rows, column-major inside a band, so a
-      // wave of ~148 CTAs reads ~12 row tiles of A and ~12 column tiles of B
-      // instead of every row tile of A (L2 reuse).  ncu, 4096^3 (0.27 GB of
-      // operands): DRAM reads 1.10 GB column-major, 0.84 GB with bands of 12
-      // (4: 1.17, 8: 0.88, 16: 0.82, 24: 0.96 GB); the time is unchanged (4.06 ms,
-      // compute-bound)
-      const int kBand = p.band;
-      const int full = p.tiles_m / kBand, per = kBand * p.tiles_n;
-      const int band = bid / per;
-      if (band < full) {
-        const int r = bid - band * per;
-        tm = band * kBand + r % kBand;
-        tn = r / kBand;
-      } else {
-        const int r = bid - full * per, rows = p.tiles_m - full * kBand;
-        tm = full * kBand + r % rows;
-        tn = r / rows;
-      }
+    default:
+      // column-major (a band-of-12-rows raster cut the DRAM reads of a 4096^3 GEMM
+      // from 1.10 to 0.84 GB at the same time, compute-bound; it is not used because
+      // it moves which tiles form a wave-balanced tail, i.e. the rounding of those
+      // tiles, and with it the bytes of the pinned full-size inputs)
+      tm = bid % p.tiles_m;
+      tn = bid / p.tiles_m;
       break;
-    }
   }
 }
 
@@ -403,27 +389,48 @@ __global__ void splitk_reduce_kernel(const GemmParams p) {
   griddep_launch_dependents();
 }
 
-// Reduction of a compact split-K tail launch: block t sums the partials of
-// tile tile0 + t and applies the epilogue (alpha, beta Cin, diag, lower/mirror).
+// Reduction of a compact split-K tail launch: one block per 32 x 32 sub-block of
+// the tail tiles (tile tile0 + t, sub-block sbk) sums the partials and applies the
+// epilogue (alpha, beta Cin, diag, lower/mirror).  The mirrored (transposed)
+// writes of LowerMirror outputs go through shared memory, so they are coalesced
+// too.  (One block per tile, element by element, was latency-bound at ~90 us per
+// 84-tile tail at n = 4096: four loads in flight per thread.)
 template <int BM>
-__global__ void splitk_reduce_tiles_kernel(const GemmParams p, int ntail) {
-  const int t = blockIdx.x;
+__global__ void __launch_bounds__(256) splitk_reduce_tiles_kernel(const GemmParams p, int ntail) {
+  __shared__ double sb[32][33];
+  constexpr int NS = (BM / 32) * (BM / 32);
+  const int t = blockIdx.x / NS, sbk = blockIdx.x % NS;
   int tm, tn;
   tile_coords(p, p.tile0 + t, tm, tn);
-  const int m0 = tm * BM, n0 = tn * BM;
+  const int m0 = tm * BM + (sbk % (BM / 32)) * 32, n0 = tn * BM + (sbk / (BM / 32)) * 32;
+  const int e0 = (sbk % (BM / 32)) * 32 + (sbk / (BM / 32)) * 32 * BM;  // sub-block origin in the tile
   const bool lower = p.omode != (int)OutMode::Full;
   const bool mirror = p.omode == (int)OutMode::LowerMirror;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
   griddep_wait();
-  for (int e = threadIdx.x; e < BM * BM; e += blockDim.x) {
-    const int i = m0 + e % BM, j = n0 + e / BM;
-    if (i >= p.M || j >= p.N || (lower && i < j)) continue;
-    double s = 0.0;
-    for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * ntail + t) * (BM * BM) + e];
-    double v = p.alpha * s;
-    if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
-    if (i == j) v += p.diag_add;
-    p.D[i + (size_t)j * p.ldd] = v;
-    if (mirror && i != j) p.D[j + (size_t)i * p.ldd] = v;
+  if (!(lower && m0 + 31 < n0)) {  // (sub-blocks strictly above the diagonal: nothing)
+    for (int r = ty; r < 32; r += 8) {
+      const int i = m0 + tx, j = n0 + r;
+      double v = 0.0;
+      if (i < p.M && j < p.N && !(lower && i < j)) {
+        const int e = e0 + tx + r * BM;
+        double s = 0.0;
+        for (int z = 0; z < p.splits; ++z) s += p.partial[((int64_t)z * ntail + t) * (BM * BM) + e];
+        v = p.alpha * s;
+        if (p.beta != 0.0) v += p.beta * p.Cin[i + (size_t)j * p.ldcin];
+        if (i == j) v += p.diag_add;
+        p.D[i + (size_t)j * p.ldd] = v;
+      }
+      sb[r][tx] = v;
+    }
+    if (mirror) {
+      __syncthreads();
+      // D(j, i) = v(i, j) for i > j, coalesced along j
+      for (int r = ty; r < 32; r += 8) {
+        const int i = m0 + r, j = n0 + tx;
+        if (i < p.M && j < p.N && i > j) p.D[j + (size_t)i * p.ldd] = sb[tx][r];
+      }
+    }
   }
   griddep_launch_dependents();
 }
@@ -596,7 +603,6 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
 
   GemmParams p{};
   p.flop_frac = 1.0;
-  p.band = 12;
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
@@ -740,13 +746,13 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
         ctx.arena->alloc_bytes((size_t)tail_split * tail_tiles * BMt * BMt * 8));
     dispatch(p2);
     if (big)
-      launch_pdl(ctx, splitk_reduce_tiles_kernel<128>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
+      launch_pdl(ctx, splitk_reduce_tiles_kernel<128>, dim3((unsigned)(tail_tiles * 16)), dim3(256), 0, p2,
                  (int)tail_tiles);
     else if (tiny)
       launch_pdl(ctx, splitk_reduce_tiles_kernel<32>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
                  (int)tail_tiles);
     else
-      launch_pdl(ctx, splitk_reduce_tiles_kernel<64>, dim3((unsigned)tail_tiles), dim3(256), 0, p2,
+      launch_pdl(ctx, splitk_reduce_tiles_kernel<64>, dim3((unsigned)(tail_tiles * 4)), dim3(256), 0, p2,
                  (int)tail_tiles);
     ctx.count();
     ctx.arena->release_to(mark);
