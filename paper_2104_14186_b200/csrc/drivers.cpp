@@ -685,13 +685,13 @@ static void check_finite(Ctx& ctx, const DMat& A, const char* who, MatStats* out
 // (delta = 4 n u ||B||^2 only keeps the rank-deficient tail positive definite; it
 // moves the |R_ii| >= tol pivots by ~delta / R_ii), and Q2 is an orthonormal basis
 // of span(B1)^perp, B1 = B(:, 0:ind-1) — the subspace spanned by Q(:, ind-1:n)
-// of the Householder QR — from a projected Gaussian block
-//   Y = (I - B1 G11^{-1} B1^T)^2 Omega,  G11^{-1} = W11^{-1} W11^{-T}
-// (two passes: the delta-shifted projector leaves ~delta/sigma_min(B1)^2 per pass),
-// Q2 = the dominant l-dimensional range of Y (eigenvectors of Y^T Y), CholQR2.
-// Everything is GEMM-shaped plus the recursive Cholesky-and-inverse: ~1.7 n^3
-// instead of the latency-bound panel chain of GEQRF.  Used when l is small
-// (trace(I - B) <= n/16 and l + 16 <= n/8); returns false to fall back.
+// of the Householder QR — from a projected Gaussian block with exactly l columns
+//   Y = (I - B1 G11^{-1} B1^T)^3 Omega,  G11^{-1} = W11^{-1} W11^{-T}
+// (three passes: the delta-shifted projector leaves ~delta/sigma_min(B1)^2 per
+// pass), Q2 = CholQR2(Y).  Everything is GEMM-shaped plus the Cholesky-and-inverse
+// (the tile DAG): ~1.7 n^3 instead of the latency-bound panel chain of GEQRF.
+// Used when l is small (trace(I - B) <= n/16, n/6 for n <= 2048); returns false
+// to fall back.
 static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DMat& Q2out,
                             const DMat& Q2buf) {
   static const bool off = getenv("QDWHG_SUBSPACE_HOUSEHOLDER") != nullptr;
@@ -701,9 +701,10 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   // to it cannot be resolved by this path (the reference's Householder R can)
   const double delta = 32.0 * std::sqrt((double)n) * kEps;
   if (!(tol > 10.0 * std::sqrt(delta))) return false;
-  // (at cfg1's l / n = 0.13, n = 1024 this path measured 4.2 ms against 2.3 ms for
-  // the Householder QR: the r x r eigensolve and the DAG chain dominate)
-  if ((double)n - device_trace(ctx, B) > (double)n / 16.0) return false;  // l estimate
+  // l estimate from trace(B): small subspaces (the projection costs ~8 n^2 l per
+  // pass); up to n/6 where the Householder QR is latency-bound (n <= 2048, cfg1)
+  const double lmax = (n <= 2048) ? (double)n / 6.0 : (double)n / 16.0;
+  if ((double)n - device_trace(ctx, B) > lmax) return false;
   const Arena::Mark mark = ctx.arena->mark();
   DMat G = ctx.arena->alloc(n, n);
   DMat Winv = ctx.arena->alloc(n, n);
@@ -734,16 +735,17 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     return false;
   }
   const int64_t ell = n - (int64_t)ind + 1, k1 = (int64_t)ind - 1;
-  // >= 8 oversampling columns, rounded up to a multiple of 64 so the skinny
-  // projection GEMMs fill whole 64-wide tiles
-  const int64_t r = ((ell + 8 + 63) / 64) * 64;
-  if (r > Q2buf.cols || k1 < 1) {
+  if (ell > Q2buf.cols || k1 < 1) {
     ctx.arena->release_to(mark);
     return false;
   }
-  DMat Y = ctx.arena->alloc(n, r);
+  // exactly l columns: span(B1)^perp has dimension l, so the projection of l
+  // Gaussian columns spans it (no oversampling, hence no r x r eigensolve to
+  // drop rounding-level directions); CholQR2 orthonormalises
+  Q2out = Q2buf.col_block(0, ell);
+  DMat Y = Q2out;
   gaussian_fill(ctx, Y, 0x7375627370ull);  // fixed stream ("subsp")
-  DMat T1 = ctx.arena->alloc(k1, r), T2 = ctx.arena->alloc(k1, r);
+  DMat T1 = ctx.arena->alloc(k1, ell), T2 = ctx.arena->alloc(k1, ell);
   const DMat B1 = B.col_block(0, k1), W11i = Winv.sub(0, 0, k1, k1);
   // Richardson passes of the least-squares projection: each leaves ~delta /
   // sigma_min(B1)^2 (+ u kappa(B1)^2) of what is left in span(B1); three passes,
@@ -759,29 +761,10 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     gemm(ctx, Op::N, Op::N, 1.0, W11i, T2, 0.0, T1, up);
     gemm(ctx, Op::N, Op::N, -1.0, B1, T1, 1.0, Y);           // Y -= B1 G11^{-1} B1^T Y
   }
-  // dominant l-dimensional range of Y: eigenvectors of the r x r Gram
-  DMat E = ctx.arena->alloc(r, r), U = ctx.arena->alloc(r, r);
-  GemmExtra gm;
-  gm.out = OutMode::LowerMirror;
-  gemm(ctx, Op::T, Op::N, 1.0, Y, Y, 0.0, E, gm);
-  // the l kept eigenvalues are O(r) (a projected Gaussian Wishart block), the p
-  // projected-out ones at rounding level: vectors only above a threshold in the
-  // gap (the rounding-level cluster would defeat inverse iteration's Lowdin check)
-  std::vector<double> vals;
-  const double tr = device_trace(ctx, E);
-  int64_t sel0 = 0;
-  const int64_t cnt = syev_range(ctx, E, vals, U, 1e-8 * tr / (double)ell, INFINITY, &sel0);
-  if (cnt != ell || !(vals[r - ell] > 1e8 * std::max(std::abs(vals[r - ell - 1]), 1e-300))) {
-    ctx.arena->release_to(mark);
-    return false;
-  }
-  Q2out = Q2buf.col_block(0, ell);
-  gemm(ctx, Op::N, Op::N, 1.0, Y, U.col_block(0, ell), 0.0, Q2out);
-  // CholQR: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2).  Y U already has orthogonal columns
-  // (U: eigenvectors of Y^T Y, kappa(Y U) = sqrt(mu_max / mu_min) = O(10)), so one
-  // pass reaches rounding-level orthogonality
+  // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice (kappa(Y) of a projected
+  // Gaussian block is O(sqrt(l)): the second pass reaches rounding-level orthogonality)
   DMat F = ctx.arena->alloc(ell, ell), Fi = ctx.arena->alloc(ell, ell), Qt = ctx.arena->alloc(n, ell);
-  for (int pass = 0; pass < 1; ++pass) {
+  for (int pass = 0; pass < 2; ++pass) {
     GemmExtra fl;
     fl.out = OutMode::Lower;
     gemm(ctx, Op::T, Op::N, 1.0, Q2out, Q2out, 0.0, F, fl);
@@ -854,7 +837,7 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     size_t ind = 0;
     DMat Q2;
     const DMat Q2buf =
-        (randomize || attempt > 0) ? DMat{} : ctx.arena->alloc(n, std::max<int64_t>(1, n / 8));
+        (randomize || attempt > 0) ? DMat{} : ctx.arena->alloc(n, std::max<int64_t>(1, n <= 2048 ? n / 4 : n / 8));
     const bool chq = !randomize && attempt == 0 && subspace_cholqr(ctx, B, tol, ind, Q2, Q2buf);
     out.subspace_path = chq ? 1 : 0;
     QrWork qw;

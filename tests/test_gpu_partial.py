@@ -213,7 +213,7 @@ def test_soak_multistream_paths(cuda, seed):
 
 
 @pytest.mark.parametrize("n,k,family", [(2048, 20, "logsigned"), (4096, 41, "logsigned"),
-                                        (1536, 60, "uniform")])
+                                        (1536, 60, "uniform"), (1024, 103, "uniform")])
 def test_cholqr_subspace_matches_householder(n, k, family):
     """The small-subspace extraction (Cholesky QR of B, projected Gaussian block)
     against the reference's Householder QR path (QDWHG_SUBSPACE_HOUSEHOLDER, in a
