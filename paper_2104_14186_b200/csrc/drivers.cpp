@@ -762,14 +762,16 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     gemm(ctx, Op::N, Op::N, -1.0, B1, T1, 1.0, Y);           // Y -= B1 G11^{-1} B1^T Y
   }
   // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice (kappa(Y) of a projected
-  // Gaussian block is O(sqrt(l)): the second pass reaches rounding-level orthogonality)
+  // Gaussian block is O(sqrt(l)): the second pass reaches rounding-level
+  // orthogonality).  kappa(F) = kappa(Y)^2 is small, so the fast Cholesky-and-
+  // inverse is accurate here (the stable panel variant cost 0.15 ms per pass at l = 132)
   DMat F = ctx.arena->alloc(ell, ell), Fi = ctx.arena->alloc(ell, ell), Qt = ctx.arena->alloc(n, ell);
   for (int pass = 0; pass < 2; ++pass) {
     GemmExtra fl;
     fl.out = OutMode::Lower;
     gemm(ctx, Op::T, Op::N, 1.0, Q2out, Q2out, 0.0, F, fl);
     try {
-      potrf_upper_and_inverse(ctx, F, Fi, false, /*stable=*/true);
+      potrf_upper_and_inverse(ctx, F, Fi, false, /*stable=*/false);
     } catch (const NotPositiveDefinite&) {
       ctx.arena->release_to(mark);
       return false;

@@ -539,72 +539,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
   if (tid == 0) d[n - 1] = A[(size_t)(n - 1) * LD + n - 1];
 }
 
-// C (n x cnt) <- H_0 H_1 ... H_{n-2} C, H_j = I - tau_j v_j v_j^T acting on rows
-// j+1.. (v_j = V(j+1:, j), unit first entry): the back-transform of the small
-// tridiagonalisation, one CTA, C staged in shared memory.
-__global__ void __launch_bounds__(kSmallThreads, 1)
-    ormtr_small_kernel(const double* V, int64_t ldv, const double* tau, int n, double* C,
-                       int64_t ldc, int cnt) {
-  extern __shared__ double sm[];
-  const int LD = n | 1;
-  double* Cs = sm;                      // Cs[c * LD + r]
-  double* ws = Cs + (size_t)cnt * LD;   // v^T C (cnt)
-  double* vbuf = ws + cnt + 1;          // v ring: [3][n]
-  double* ts = vbuf + 3 * n;            // tau (n)
-  const int tid = threadIdx.x;
-  for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32))
-    for (int r = tid & 31; r < n; r += 32) Cs[c * LD + r] = C[r + (int64_t)c * ldc];
-  for (int r = tid; r < n - 1; r += blockDim.x) ts[r] = tau[r];
-  // v_j (rows j+1..) of the first two reflectors; later ones are prefetched into
-  // registers two steps ahead, so no step waits on a global load
-  for (int q = 0; q < 2 && n - 2 - q >= 0; ++q) {
-    const int j = n - 2 - q;
-    if (tid < n - j - 1) vbuf[q * n + tid] = V[(j + 1 + tid) + (int64_t)j * ldv];
-  }
-  __syncthreads();
-  for (int j = n - 2; j >= 0; --j) {
-    const int m = n - j - 1;
-    const int slot = (n - 2 - j) % 3;
-    double* vs = vbuf + slot * n;
-    double* vn = vbuf + ((slot + 2) % 3) * n;  // reflector j - 2
-    const double pre = (j > 1 && tid <= m + 1) ? V[(j - 1 + tid) + (int64_t)(j - 2) * ldv] : 0.0;
-    const double tj = ts[j];
-    // w_c = tau v^T C(j+1:, c): 8 threads per column
-    const int k = tid & 7;
-    for (int c0 = (tid >> 5) * 4; c0 < cnt; c0 += (int)(blockDim.x / 8)) {  // warp-uniform bound
-      const int c = c0 + ((tid >> 3) & 3);
-      const double* col = Cs + (size_t)c * LD + j + 1;
-      double acc = 0.0;
-      if (c < cnt)
-        for (int r = k; r < m; r += 8) acc = fma(vs[r], col[r], acc);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      if (k == 0 && c < cnt) ws[c] = tj * acc;
-    }
-    __syncthreads();
-    for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32)) {
-      double* col = Cs + (size_t)c * LD + j + 1;
-      const double wc = ws[c];
-      for (int r = tid & 31; r < m; r += 32) col[r] -= vs[r] * wc;
-    }
-    if (j > 1 && tid <= m + 1) vn[tid] = pre;
-    __syncthreads();
-  }
-  __syncthreads();
-  for (int c = tid >> 5; c < cnt; c += (int)(blockDim.x / 32))
-    for (int r = tid & 31; r < n; r += 32) C[r + (int64_t)c * ldc] = Cs[c * LD + r];
-}
-
 int small_threads() {
   static const int t = getenv("QDWHG_SMALL_THREADS") ? atoi(getenv("QDWHG_SMALL_THREADS")) : kSmallThreads;
   return (t == 256 || t == 512 || t == 1024) ? t : kSmallThreads;
 }
 
 size_t sytd2_small_smem(int n) { return ((size_t)n * (n | 1) + 2 * (n + 1) + 2) * sizeof(double); }
-size_t ormtr_small_smem(int n, int cnt) {
-  return ((size_t)cnt * (n | 1) + (cnt + 1) + 4 * n) * sizeof(double);
-}
 
 }  // namespace
 
@@ -638,8 +578,6 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   func_attr(sytrd_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrdDynSmem);
   if (small) {
     func_attr(sytd2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sytd2_small_smem(kSmallTrd));
-    func_attr(ormtr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-              (int)ormtr_small_smem(kSmallTrd, kSmallTrd));
     sytd2_small_kernel<<<1, small_threads(), sytd2_small_smem(n), ctx.stream>>>(S.ptr(), S.ld, n, dd, ee, tau,
                                                                              Vfull.ptr(), Vfull.ld);
     QDWHG_CUDA(cudaGetLastError());
@@ -750,18 +688,17 @@ bool syev_tridiag(Ctx& ctx, const DMat& S, std::vector<double>& vals, const DMat
   // ---- back-transform: Vout = Q Z F, Q = H_0 ... H_{n-2}, blocks applied last to first
   const DMat Vsel = Vout.sub(0, 0, n, cnt);
   gemm(ctx, Op::N, Op::N, 1.0, Z, F, 0.0, Vsel);
-  if (small) {
-    ormtr_small_kernel<<<1, small_threads(), ormtr_small_smem(n, cnt), ctx.stream>>>(
-        Vfull.ptr(), Vfull.ld, tau, n, Vsel.ptr(), Vsel.ld, cnt);
-    QDWHG_CUDA(cudaGetLastError());
-    ctx.count();
-    ctx.arena->release_to(mark);
-    return true;
-  }
-  DMat G = ctx.arena->alloc(nb, nb), Tb = ctx.arena->alloc(nb, nb);
-  for (int p = npan - 1; p >= 0; --p) {
-    const int j0 = p * nb;
-    const int b = std::min(nb, n - 1 - j0);
+  // (small blocks too: the sytd2_small reflectors use the same unit-lower layout;
+  // compact-WY blocks on the GEMM engine instead of the former one-CTA
+  // reflector-by-reflector back-transform: 0.30 ms at l = 132)
+  // blocks of 64 reflectors (the larft limit; twice the SYTRD panel width: half
+  // the launches, K = 64 GEMMs)
+  constexpr int bw = 64;
+  const int nbt = (n - 1 + bw - 1) / bw;
+  DMat G = ctx.arena->alloc(bw, bw), Tb = ctx.arena->alloc(bw, bw);
+  for (int p = nbt - 1; p >= 0; --p) {
+    const int j0 = p * bw;
+    const int b = std::min(bw, n - 1 - j0);
     const int r0 = j0 + 1;  // reflectors of this panel act on rows >= j0+1
     const int mp = n - r0;
     const DMat Vb = Vfull.sub(r0, j0, mp, b);
