@@ -921,14 +921,7 @@ qdwhg_status qdwhg_subspace_q2(qdwhg_handle* h, int64_t n, double* B, int64_t ld
     // partial.cpp:71-79: Householder QR of B, ind = first |R_ii| < tol, Q2 = Q(:, ind-1:n)
     QrWork qw;
     geqrf(ctx, Bd, qw);
-    std::vector<double> d;
-    diag_to_host(ctx, Bd, d);
-    size_t i0 = 0;
-    for (size_t i = 0; i < d.size(); ++i)
-      if (std::abs(d[i]) < tol) {
-        i0 = i + 1;
-        break;
-      }
+    const size_t i0 = (size_t)first_deficient(ctx, Bd, tol);
     *ind = (int64_t)i0;
     *ell = i0 ? n - (int64_t)i0 + 1 : 0;
     if (i0 == 0) return;

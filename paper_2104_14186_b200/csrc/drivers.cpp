@@ -720,15 +720,9 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     ctx.arena->release_to(mark);
     return false;
   }
-  // |R_ii| = W_ii = 1 / (W^{-1})_ii (triangular inverse: no need to write W out)
-  std::vector<double> d;
-  diag_to_host(ctx, Winv, d);
-  ind = 0;  // detect_deficiency_index, partial.cpp:32-38
-  for (size_t i = 0; i < d.size(); ++i)
-    if (!(1.0 / std::abs(d[i]) >= tol)) {
-      ind = i + 1;
-      break;
-    }
+  // |R_ii| = W_ii = 1 / (W^{-1})_ii (triangular inverse: no need to write W out);
+  // detect_deficiency_index, partial.cpp:32-38
+  ind = (size_t)first_deficient(ctx, Winv, tol, /*reciprocal=*/true);
   if (ind == 0) {
     // no deficient pivot: confirmed on the reference's Householder path (as for k == 0)
     ctx.arena->release_to(mark);
@@ -845,14 +839,7 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     QrWork qw;
     if (!chq) {
       geqrf(ctx, B, qw);
-      std::vector<double> d;
-      diag_to_host(ctx, B, d);
-      ind = 0;  // detect_deficiency_index, partial.cpp:32-38
-      for (size_t i = 0; i < d.size(); ++i)
-        if (std::abs(d[i]) < tol) {
-          ind = i + 1;
-          break;
-        }
+      ind = (size_t)first_deficient(ctx, B, tol);  // detect_deficiency_index, partial.cpp:32-38
     }
     if (clk) clk->mark(2);
     out.flops = it.iters_chol * (10.0 / 3.0) * nd * nd * nd + 4.0 / 3.0 * nd * nd * nd +
@@ -961,15 +948,8 @@ SvdOut partial_svd(Ctx& ctx, const DMat& A, double s, double s_abs, double tol, 
   }
   QrWork qw;
   geqrf(ctx, B, qw);
-  std::vector<double> d;
-  diag_to_host(ctx, B, d);
+  const size_t ind = (size_t)first_deficient(ctx, B, tol);  // partial.cpp:32-38
   if (clk) clk->mark(2);
-  size_t ind = 0;
-  for (size_t i = 0; i < d.size(); ++i)
-    if (std::abs(d[i]) < tol) {
-      ind = i + 1;
-      break;
-    }
   const double md = (double)m, nd = (double)n;
   out.flops = out.iters_qr * (6 * md * nd * nd + 8.0 / 3.0 * nd * nd * nd) +
               out.iters_chol * (3 * md * nd * nd + nd * nd * nd / 3) + md * nd * nd +

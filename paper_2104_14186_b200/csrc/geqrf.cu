@@ -1179,4 +1179,32 @@ void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d) {
   QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
+
+// detect_deficiency_index (partial.cpp:32-38) on the device: the 1-based index of
+// the first diagonal entry of R with |R_ii| < tol (reciprocal: R_ii = 1 / X_ii of
+// the given X, e.g. X = W^{-1}), 0 when none.  One int comes back to the host
+// instead of the whole diagonal.
+__global__ void first_deficient_kernel(const double* R, int64_t ld, int64_t n, double tol, int reciprocal,
+                                       unsigned long long* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = R[i + i * ld];
+    const bool hit = reciprocal ? !(1.0 / fabs(d) >= tol) : (fabs(d) < tol);
+    if (hit) atomicMin(out, (unsigned long long)(i + 1));
+  }
+}
+
+int64_t first_deficient(Ctx& ctx, const DMat& R, double tol, bool reciprocal) {
+  const int64_t n = std::min(R.rows, R.cols);
+  auto* dv = static_cast<unsigned long long*>(ctx.arena->alloc_bytes(sizeof(unsigned long long)));
+  auto* hv = reinterpret_cast<unsigned long long*>(ctx.hscratch);
+  QDWHG_CUDA(cudaMemsetAsync(dv, 0xff, sizeof(unsigned long long), ctx.stream));
+  first_deficient_kernel<<<std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148)), 256, 0, ctx.stream>>>(
+      R.ptr(), R.ld, n, tol, reciprocal ? 1 : 0, dv);
+  QDWHG_CUDA(cudaGetLastError());
+  ctx.count();
+  QDWHG_CUDA(cudaMemcpyAsync(hv, dv, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx.stream));
+  QDWHG_CUDA(cudaStreamSynchronize(ctx.stream));
+  return *hv == ~0ull ? 0 : (int64_t)*hv;
+}
+
 }  // namespace qdwhg

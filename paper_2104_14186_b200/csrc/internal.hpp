@@ -266,6 +266,9 @@ void orgqr_cols(Ctx& ctx, const QrWork& work, int64_t m, int64_t p, int64_t c0, 
 void ormqr_left(Ctx& ctx, const QrWork& work, int64_t m, int64_t n, const DMat& C);
 // diag(R) to host (n values).
 void diag_to_host(Ctx& ctx, const DMat& R, std::vector<double>& d);
+// detect_deficiency_index on the device: first i (1-based) with |R_ii| < tol
+// (reciprocal: with |1 / R_ii| < tol), 0 when none.
+int64_t first_deficient(Ctx& ctx, const DMat& R, double tol, bool reciprocal = false);
 
 // ------------------------------------------------------------------ syevj.cu
 // Symmetric eigendecomposition of S (n x n, device).  Ascending values to host
