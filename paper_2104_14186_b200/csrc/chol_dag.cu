@@ -47,6 +47,7 @@ enum : int { kLeafTask = 0, kPanelTask = 1, kUpdateTask = 2, kAccTask = 3, kFinT
 struct DagTask {
   int type, i, j, k;
   int r0, nr;         // row strip of the output tile
+  int nk;             // 128-column K steps (1, or 2: steps k and k + 1 in one task)
   int slot;           // completion counter this task increments
   int dep[3];         // tile indices (i * T + j) this task waits on, -1 = none
   unsigned cnt[3];    // ... until their completion counters reach these values
@@ -99,7 +100,9 @@ enum : int { kSet = 0, kSub = 1, kAdd = 2, kNeg = 3 };  // C = [C0] +/- A Bt^T
 // code small — the leaf runs from a warm instruction cache)
 template <int R>
 QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const double* A, int64_t lda,
-                         const double* Bt, int64_t ldb) {
+                         const double* Bt, int64_t ldb, const double* A1 = nullptr,
+                         const double* Bt1 = nullptr) {
+  // K = 128 (A, Bt), or 256 with the second step's (A1, Bt1) after the first
   // C0 - A Bt^T = -(-C0 + A Bt^T): the sign goes on the accumulators' first load
   // and last store, none in the DMMA loop
   const bool loadc = mode == kSub || mode == kAdd;
@@ -120,20 +123,23 @@ QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const dou
     double* as = sm + (ch % STAGES) * STAGE;
     double* bs = as + kKC * LDA;
     constexpr int AP = kKC * (R / 2), BP = kKC * (kTile / 2);
+    const int cs = ch & 3;  // chunk within its 128-column step
+    const double* Ap = (ch < 4) ? A : A1;
+    const double* Bp = (ch < 4) ? Bt : Bt1;
 #pragma unroll 4
     for (int idx = tid; idx < AP + BP; idx += leaf::kThreads) {
       if (idx < AP) {
         const int c = idx / (R / 2), r2 = idx % (R / 2);
-        cp_async16_cg(as + c * LDA + 2 * r2, A + 2 * r2 + (int64_t)(ch * kKC + c) * lda);
+        cp_async16_cg(as + c * LDA + 2 * r2, Ap + 2 * r2 + (int64_t)(cs * kKC + c) * lda);
       } else {
         const int b = idx - AP;
         const int c = b / (kTile / 2), r2 = b % (kTile / 2);
-        cp_async16_cg(bs + c * kLDB + 2 * r2, Bt + 2 * r2 + (int64_t)(ch * kKC + c) * ldb);
+        cp_async16_cg(bs + c * kLDB + 2 * r2, Bp + 2 * r2 + (int64_t)(cs * kKC + c) * ldb);
       }
     }
   };
 
-  constexpr int NCH = kTile / kKC;
+  const int NCH = (A1 != nullptr) ? 8 : 4;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < NCH) load_chunk(s);
@@ -297,7 +303,6 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         }
       }
       __syncthreads();
-      __syncthreads();
       const int64_t ld = p.ldz;
       {
         // one call site per strip height (the kernel's code stays small: the leaf
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         };
         int mode;
         double* C;
-        const double *A, *Bt;
+        const double *A, *Bt, *A1 = nullptr, *Bt1 = nullptr;  // (A1, Bt1): step k + 1 of a paired task
         int64_t ldc = ld, lda = ld;
         switch (tk.type) {
           case kPanelTask:  // L_ik = Z_ik L_kk^{-T}  (A aliases C row by row: read before written)
@@ -317,18 +322,26 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
             A = C;
             Bt = zt(tk.k, tk.k, 0);
             break;
-          case kUpdateTask:  // Z_ij -= L_ik L_jk^T
+          case kUpdateTask:  // Z_ij -= L_ik L_jk^T (+ L_i,k+1 L_j,k+1^T)
             mode = kSub;
             C = zt(tk.i, tk.j, tk.r0);
             A = zt(tk.i, tk.k, tk.r0);
             Bt = zt(tk.j, tk.k, 0);
+            if (tk.nk == 2) {
+              A1 = zt(tk.i, tk.k + 1, tk.r0);
+              Bt1 = zt(tk.j, tk.k + 1, 0);
+            }
             break;
-          case kAccTask:  // S_ij^T (+)= X_kj^T L_ik^T  (X = L^{-1}, X_kj^T = Winv tile (j, k)), S^T in Z tile (j, i)
+          case kAccTask:  // S_ij^T (+)= X_kj^T L_ik^T (+ the k + 1 term)  (X = L^{-1}, X_kj^T = Winv tile (j, k)), S^T in Z tile (j, i)
             mode = tk.k == tk.j ? kSet : kAdd;
             C = zt(tk.j, tk.i, tk.r0);
             A = wt(tk.j, tk.k, tk.r0);
             lda = p.ldw;
             Bt = zt(tk.i, tk.k, 0);
+            if (tk.nk == 2) {
+              A1 = wt(tk.j, tk.k + 1, tk.r0);
+              Bt1 = zt(tk.i, tk.k + 1, 0);
+            }
             break;
           default:  // kFinTask: Winv_ji = X_ij^T = -S_ij^T L_ii^{-T}
             mode = kNeg;
@@ -343,7 +356,7 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         else if (tk.nr == 32)
           tile_gemm<32>(sm, mode, C, ldc, A, lda, Bt, ld);
         else
-          tile_gemm<128>(sm, mode, C, ldc, A, lda, Bt, ld);
+          tile_gemm<128>(sm, mode, C, ldc, A, lda, Bt, ld, A1, Bt1);
       }
       __syncthreads();
       if (tid == 0) {
@@ -387,6 +400,7 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
   std::vector<unsigned> cnt((size_t)T * T, 0u);
   std::vector<std::vector<int>> last((size_t)T * T);  // task ids of the tile's latest step
   auto tile = [T](int i, int j) { return i * T + j; };
+  int nk = 1;  // K steps of the next task added (2: steps k and k + 1 paired)
   auto addx = [&](int type, int i, int j, int k, int nstrips, const int (&dt)[3], double d, int slot) {
     DagTask base{};
     base.type = type;
@@ -408,6 +422,7 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
     for (int s = 0; s < nstrips; ++s) {
       DagTask x = base;
       x.slot = slot;
+      x.nk = nk;
       x.nr = kTile / nstrips;
       x.r0 = s * x.nr;
       const int id = (int)tasks.size();
@@ -437,18 +452,38 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
     }
     for (int j = k + 1; j < T; ++j)
       for (int i = j; i < T; ++i) {
-        const int dt[3] = {tile(i, j), tile(i, k), i == j ? -1 : tile(j, k)};
         const bool c = (j == k + 1);  // the next tile column: on the leaf chain
         const bool chain = c && i == j;
+        if (!c) {
+          // bulk updates of a tile in pairs of steps (K = 256: half the tasks, half
+          // the C traffic): step k even with k + 1 also bulk waits for its pair
+          if (k % 2 == 0 && j >= k + 3) continue;
+          if (k % 2 == 1) {
+            // pair (k - 1, k): tile (i, j) through k - 2, panels (i, k), (j, k)
+            // (which imply those of step k - 1)
+            const int dt[3] = {tile(i, j), tile(i, k), i == j ? -1 : tile(j, k)};
+            nk = 2;
+            add(kUpdateTask, i, j, k - 1, 1, dt, 2.0 * kTileUs - 4.0);
+            nk = 1;
+            continue;
+          }
+        }
+        const int dt[3] = {tile(i, j), tile(i, k), i == j ? -1 : tile(j, k)};
         add(kUpdateTask, i, j, k, chain ? 8 : c ? 4 : 1, dt, chain ? kChainUs : c ? kStripUs : kTileUs);
       }
     // row k of X = L^{-1} (W^{-1} = X^T): X_kj = -L_kk^{-1} sum_{m=j}^{k-1} L_km X_mj,
     // accumulated (S_kj^T in Z's unused upper tile (j, k)) as soon as X_mj and
     // L_km exist; slot counters use the upper index (j, k)
     for (int j = 0; j < k; ++j) {
-      for (int m = j; m < k; ++m) {
-        const int dt[3] = {tile(j, k), tile(j, m), tile(k, m)};  // S, X_mj (leaf / FIN), L_km
-        addx(kAccTask, k, j, m, 1, dt, kTileUs, tile(j, k));
+      // accumulations in pairs of m (K = 256), the last one (m = k - 1, the one
+      // FIN(k, j) waits for) single
+      for (int m = j; m < k;) {
+        const int m2 = (m + 1 < k - 1) ? m + 1 : m;  // last step of this task
+        const int dt[3] = {tile(j, k), tile(j, m2), tile(k, m2)};  // S, X_m2,j (leaf / FIN), L_k,m2
+        nk = m2 - m + 1;
+        addx(kAccTask, k, j, m, 1, dt, nk == 2 ? 2.0 * kTileUs - 4.0 : kTileUs, tile(j, k));
+        nk = 1;
+        m = m2 + 1;
       }
       const int dt[3] = {tile(j, k), tile(k, k), -1};  // all of S, L_kk^{-1}
       addx(kFinTask, k, j, k, 4, dt, kStripUs, tile(j, k));
