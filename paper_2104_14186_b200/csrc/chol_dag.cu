@@ -100,9 +100,8 @@ enum : int { kSet = 0, kSub = 1, kAdd = 2, kNeg = 3 };  // C = [C0] +/- A Bt^T
 // code small — the leaf runs from a warm instruction cache)
 template <int R>
 QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const double* A, int64_t lda,
-                         const double* Bt, int64_t ldb, const double* A1 = nullptr,
-                         const double* Bt1 = nullptr) {
-  // K = 128 (A, Bt), or 256 with the second step's (A1, Bt1) after the first
+                         const double* Bt, int64_t ldb, int nk = 1) {
+  // K = 128 nk: step s reads the 128 columns of A and Bt that follow step s - 1
   // C0 - A Bt^T = -(-C0 + A Bt^T): the sign goes on the accumulators' first load
   // and last store, none in the DMMA loop
   const bool loadc = mode == kSub || mode == kAdd;
@@ -124,8 +123,8 @@ QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const dou
     double* bs = as + kKC * LDA;
     constexpr int AP = kKC * (R / 2), BP = kKC * (kTile / 2);
     const int cs = ch & 3;  // chunk within its 128-column step
-    const double* Ap = (ch < 4) ? A : A1;
-    const double* Bp = (ch < 4) ? Bt : Bt1;
+    const double* Ap = A + (int64_t)(ch >> 2) * kTile * lda;
+    const double* Bp = Bt + (int64_t)(ch >> 2) * kTile * ldb;
 #pragma unroll 4
     for (int idx = tid; idx < AP + BP; idx += leaf::kThreads) {
       if (idx < AP) {
@@ -139,7 +138,7 @@ QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const dou
     }
   };
 
-  const int NCH = (A1 != nullptr) ? 8 : 4;
+  const int NCH = 4 * nk;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < NCH) load_chunk(s);
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         };
         int mode;
         double* C;
-        const double *A, *Bt, *A1 = nullptr, *Bt1 = nullptr;  // (A1, Bt1): step k + 1 of a paired task
+        const double *A, *Bt;
         int64_t ldc = ld, lda = ld;
         switch (tk.type) {
           case kPanelTask:  // L_ik = Z_ik L_kk^{-T}  (A aliases C row by row: read before written)
@@ -322,26 +321,18 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
             A = C;
             Bt = zt(tk.k, tk.k, 0);
             break;
-          case kUpdateTask:  // Z_ij -= L_ik L_jk^T (+ L_i,k+1 L_j,k+1^T)
+          case kUpdateTask:  // Z_ij -= sum_{s < nk} L_i,k+s L_j,k+s^T
             mode = kSub;
             C = zt(tk.i, tk.j, tk.r0);
             A = zt(tk.i, tk.k, tk.r0);
             Bt = zt(tk.j, tk.k, 0);
-            if (tk.nk == 2) {
-              A1 = zt(tk.i, tk.k + 1, tk.r0);
-              Bt1 = zt(tk.j, tk.k + 1, 0);
-            }
             break;
-          case kAccTask:  // S_ij^T (+)= X_kj^T L_ik^T (+ the k + 1 term)  (X = L^{-1}, X_kj^T = Winv tile (j, k)), S^T in Z tile (j, i)
+          case kAccTask:  // S_ij^T (+)= sum_{s < nk} X_k+s,j^T L_i,k+s^T  (X = L^{-1}, X_kj^T = Winv tile (j, k)), S^T in Z tile (j, i)
             mode = tk.k == tk.j ? kSet : kAdd;
             C = zt(tk.j, tk.i, tk.r0);
             A = wt(tk.j, tk.k, tk.r0);
             lda = p.ldw;
             Bt = zt(tk.i, tk.k, 0);
-            if (tk.nk == 2) {
-              A1 = wt(tk.j, tk.k + 1, tk.r0);
-              Bt1 = zt(tk.i, tk.k + 1, 0);
-            }
             break;
           default:  // kFinTask: Winv_ji = X_ij^T = -S_ij^T L_ii^{-T}
             mode = kNeg;
@@ -356,7 +347,7 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
         else if (tk.nr == 32)
           tile_gemm<32>(sm, mode, C, ldc, A, lda, Bt, ld);
         else
-          tile_gemm<128>(sm, mode, C, ldc, A, lda, Bt, ld, A1, Bt1);
+          tile_gemm<128>(sm, mode, C, ldc, A, lda, Bt, ld, tk.nk);
       }
       __syncthreads();
       if (tid == 0) {
@@ -400,7 +391,11 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
   std::vector<unsigned> cnt((size_t)T * T, 0u);
   std::vector<std::vector<int>> last((size_t)T * T);  // task ids of the tile's latest step
   auto tile = [T](int i, int j) { return i * T + j; };
-  int nk = 1;  // K steps of the next task added (2: steps k and k + 1 paired)
+  int nk = 1;  // K steps of the next task added (bulk groups: steps k .. k + nk - 1)
+  // measured (n = 4096 DAG / n = 2048 DAG, us): 1 step 2651 / 913, 2: 2442 / 911,
+  // 3: 2386 / 973, 4: 2389 / 1034, 6: 2619 / 1208 — longer tasks pay where the
+  // trailing work is large, short ones where the leaf chain dominates
+  const int kGroup = (T >= 24) ? 3 : 2;
   auto addx = [&](int type, int i, int j, int k, int nstrips, const int (&dt)[3], double d, int slot) {
     DagTask base{};
     base.type = type;
@@ -455,15 +450,16 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
         const bool c = (j == k + 1);  // the next tile column: on the leaf chain
         const bool chain = c && i == j;
         if (!c) {
-          // bulk updates of a tile in pairs of steps (K = 256: half the tasks, half
-          // the C traffic): step k even with k + 1 also bulk waits for its pair
-          if (k % 2 == 0 && j >= k + 3) continue;
-          if (k % 2 == 1) {
-            // pair (k - 1, k): tile (i, j) through k - 2, panels (i, k), (j, k)
-            // (which imply those of step k - 1)
-            const int dt[3] = {tile(i, j), tile(i, k), i == j ? -1 : tile(j, k)};
-            nk = 2;
-            add(kUpdateTask, i, j, k - 1, 1, dt, 2.0 * kTileUs - 4.0);
+          // bulk updates of a tile in groups of kGroup steps (K = 128 kGroup: fewer
+          // tasks, less C traffic), aligned at multiples of kGroup and cut at the
+          // tile's last bulk step j - 2; emitted at the group's last step
+          const int gs = (k / kGroup) * kGroup, ge = std::min(gs + kGroup - 1, j - 2);
+          if (k != ge) continue;
+          if (ge > gs) {
+            // tile (i, j) through gs - 1, panels (i, ge), (j, ge) (which imply the earlier ones)
+            const int dt[3] = {tile(i, j), tile(i, ge), i == j ? -1 : tile(j, ge)};
+            nk = ge - gs + 1;
+            add(kUpdateTask, i, j, gs, 1, dt, nk * (kTileUs - 4.0) + 4.0);
             nk = 1;
             continue;
           }
@@ -475,13 +471,13 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
     // accumulated (S_kj^T in Z's unused upper tile (j, k)) as soon as X_mj and
     // L_km exist; slot counters use the upper index (j, k)
     for (int j = 0; j < k; ++j) {
-      // accumulations in pairs of m (K = 256), the last one (m = k - 1, the one
-      // FIN(k, j) waits for) single
+      // accumulations in groups of kGroup m (K = 128 kGroup), the last one
+      // (m = k - 1, the one FIN(k, j) waits for) alone
       for (int m = j; m < k;) {
-        const int m2 = (m + 1 < k - 1) ? m + 1 : m;  // last step of this task
+        const int m2 = (m == k - 1) ? m : std::min(m + kGroup - 1, k - 2);  // last step of this task
         const int dt[3] = {tile(j, k), tile(j, m2), tile(k, m2)};  // S, X_m2,j (leaf / FIN), L_k,m2
         nk = m2 - m + 1;
-        addx(kAccTask, k, j, m, 1, dt, nk == 2 ? 2.0 * kTileUs - 4.0 : kTileUs, tile(j, k));
+        addx(kAccTask, k, j, m, 1, dt, nk * (kTileUs - 4.0) + 4.0, tile(j, k));
         nk = 1;
         m = m2 + 1;
       }
