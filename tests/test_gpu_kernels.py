@@ -364,3 +364,23 @@ def test_device_gaussian_reference_stream_determinism_and_moments(cuda):
     assert abs(x.var() - 1.0) < 5.0 * np.sqrt(2.0 / N)
     assert abs(np.mean(x ** 4) - 3.0) < 5.0 * np.sqrt(96.0 / N)
     assert abs(np.mean(x ** 3)) < 5.0 * np.sqrt(15.0 / N)
+
+
+@pytest.mark.parametrize("n", [256, 384, 1024, 3072, 4096, 4224, 8192])
+def test_cholesky_inverse_fast_dag_sizes(cuda, n):
+    """The tile-DAG Cholesky-and-inverse (chol_dag.cu) at every shape class: pure DAG
+    launches (n = 128 T, T = 2 .. 32, K-step groups of 2 and 3), the recursion with a DAG
+    sub-tree plus a non-DAG remainder (4224 = 4096 + 128), and two DAG sub-trees under
+    the recursion (8192): W^{-1} against LAPACK on the kappa(Z) <= 1 + c class of the
+    QDWH step (Z = I + c X^T X with c = 50)."""
+    import torch
+    x = torch.randn(n, n, dtype=torch.float64, device=cuda,
+                    generator=torch.Generator(device=cuda).manual_seed(n))
+    x = x / torch.linalg.matrix_norm(x, 2)
+    z = (torch.eye(n, dtype=torch.float64, device=cuda) + 50.0 * (x.T @ x)).t().contiguous().t()
+    wi = qdwh.cholesky_inverse_fast(z)
+    ref = torch.linalg.inv(torch.linalg.cholesky(z).T)
+    assert float((wi - ref).abs().max() / ref.abs().max()) <= 1e-13
+    assert float(torch.tril(wi, -1).abs().max()) == 0.0
+    r = wi.T @ z @ wi - torch.eye(n, dtype=torch.float64, device=cuda)
+    assert float(torch.linalg.matrix_norm(r)) <= 1e-13 * n
