@@ -139,6 +139,7 @@ __global__ void sub_qh_kernel(const double* Q, int64_t ldq, int64_t n, int kcoun
 // step (two CGS passes, the norm), no host round trips, no kernel launches.
 // Partial sums are combined in fixed order (deterministic).
 constexpr int kLzThreads = 512;
+constexpr int kLzSlotsPerLane = 5;  // 160 >= the grid (<= 148 CTAs)
 struct LanczosArgs {
   const double* A;
   int64_t lda;
@@ -262,11 +263,29 @@ __global__ void __launch_bounds__(kLzThreads, 1) lanczos_kernel(LanczosArgs a) {
         if (lane == 0) sl[g * 64 + t] = sm;
       }
       grid_sync(a.bar, epoch);
-      for (int t = warp; t <= j; t += NW) {
-        double sm = 0.0;
-        for (int gg = lane; gg < G; gg += 32) sm += __ldcg(&sl[gg * 64 + t]);
-        sm = warp_sum(sm);
-        if (lane == 0) hsm[t] = sm;
+      // h_t = sum over the G CTAs' slots: every load of a warp's (up to two) t issued
+      // before any add (the reduction is L2-latency bound: one round trip, not five)
+      for (int t = warp; t <= j; t += 2 * NW) {
+        const int t2 = t + NW;
+        double v[2][kLzSlotsPerLane];
+#pragma unroll
+        for (int u = 0; u < kLzSlotsPerLane; ++u) {
+          const int gg = lane + 32 * u;
+          v[0][u] = gg < G ? __ldcg(&sl[gg * 64 + t]) : 0.0;
+          v[1][u] = (gg < G && t2 <= j) ? __ldcg(&sl[gg * 64 + t2]) : 0.0;
+        }
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int u = 0; u < kLzSlotsPerLane; ++u) {
+          s0 += v[0][u];
+          s1 += v[1][u];
+        }
+        s0 = warp_sum(s0);
+        s1 = warp_sum(s1);
+        if (lane == 0) {
+          hsm[t] = s0;
+          if (t2 <= j) hsm[t2] = s1;
+        }
       }
       __syncthreads();
       for (int ii = tid; ii < nown; ii += kLzThreads) {
@@ -289,8 +308,12 @@ __global__ void __launch_bounds__(kLzThreads, 1) lanczos_kernel(LanczosArgs a) {
     if (tid == 0) bs[g] = b2;
     grid_sync(a.bar, epoch);
     if (warp == 0) {
+      double v[kLzSlotsPerLane];
+#pragma unroll
+      for (int u = 0; u < kLzSlotsPerLane; ++u) v[u] = (lane + 32 * u < G) ? __ldcg(&bs[lane + 32 * u]) : 0.0;
       double sm = 0.0;
-      for (int gg = lane; gg < G; gg += 32) sm += __ldcg(&bs[gg]);
+#pragma unroll
+      for (int u = 0; u < kLzSlotsPerLane; ++u) sm += v[u];
       sm = warp_sum(sm);
       if (lane == 0) hsm[0] = sm;
     }
@@ -406,7 +429,7 @@ double lanczos_min_bound(Ctx& ctx, const DMat& A, int steps, const MatStats* pre
   // truncated there, exactly like the reference's early exit (later entries
   // are never read).
   // one CTA per SM (co-resident for the grid barriers), at least 16 rows each
-  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, n / 16));
+  const int G = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(ctx.num_sms, 32 * kLzSlotsPerLane), n / 16));
   const int chunk = (int)((n + G - 1) / G);
   const size_t smem = (size_t)(chunk + 96 + (kLzThreads / 32) * chunk) * 8;
   if (smem > 200 * 1024) throw InvalidArgument("lanczos_min_bound: matrix too large");
