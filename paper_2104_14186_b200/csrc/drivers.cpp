@@ -210,7 +210,7 @@ void qdwh_qr_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xout
   axpby_identity(ctx, X, sc, 0.0, S.sub(0, 0, m, n));
   fill(ctx, S.sub(m, 0, n, n), 0.0, 1.0);
   QrWork qw;
-  geqrf(ctx, S, qw);
+  geqrf(ctx, S, qw, /*top_rows=*/m);  // the identity block: row-limited panels and updates
   DMat Q = ctx.arena->alloc(m + n, n);
   orgqr_cols(ctx, qw, m + n, n, 0, Q);
   const double bc = w.b / w.c;

@@ -922,9 +922,18 @@ void larft_launch(Ctx& ctx, const DMat& G, const double* tau_dev, const DMat& T)
   ctx.count();
 }
 
-void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
+void geqrf(Ctx& ctx, const DMat& A, QrWork& w, int64_t top_rows) {
   const int64_t m = A.rows, n = A.cols;
   if (m < n) throw InvalidArgument("geqrf: requires rows >= cols");
+  if (top_rows < 0 || top_rows > m) throw InvalidArgument("geqrf: bad structure");
+  // Structured stack [T; U] (top_rows > 0: rows [top_rows, m) upper triangular,
+  // e.g. the QDWH QR step's [sqrt(c) X; I], polar.cpp:56-72): a reflector of
+  // column c touches rows < top_rows + c + 1 only, and the rows below stay zero
+  // in every column to its right, so every panel and update of columns
+  // [j0, j0 + b) runs on rows [j0, top_rows + j0 + b) — for m = 2n, (n + b) rows
+  // instead of (2n - j0): ~40 % fewer flops, shorter panels.  Same reflectors.
+  w.top_rows = top_rows;
+  auto rend = [&](int64_t c) { return top_rows > 0 ? std::min<int64_t>(m, top_rows + c) : m; };
   // Two-level blocking: 64-column panels (one cooperative/cluster kernel each)
   // inside 256-column outer blocks.  Inner updates touch only the outer block;
   // the outer T (256 x 256) is assembled by merging the panel T's
@@ -940,6 +949,7 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   w.nb = nbo;
   const int64_t nout = (n + nbo - 1) / nbo;
   w.V = ctx.arena->alloc(m, n);
+  if (top_rows > 0) fill(ctx, w.V, 0.0, 0.0);  // V below each panel's row range stays zero
   w.T = ctx.arena->alloc(nbo, nout * nbo);
   fill(ctx, w.T, 0.0, 0.0);
   double* tau_dev = static_cast<double*>(ctx.arena->alloc_bytes(sizeof(double) * (n + 64)));
@@ -978,13 +988,13 @@ void geqrf(Ctx& ctx, const DMat& A, QrWork& w) {
   for (int64_t po = 0; po < nout; ++po) {
     const int64_t jo = po * nbo;
     const int64_t bo = std::min<int64_t>(nbo, n - jo);
-    const int64_t mo = m - jo;
+    const int64_t mo = rend(jo + bo) - jo;
     const DMat To = w.T.sub(0, po * nbo, bo, bo);
     std::vector<std::pair<int64_t, int64_t>> blocks;  // (offset in outer block, width)
     for (int64_t ji = 0; ji < bo; ji += nbi) {
       const int64_t bi = std::min<int64_t>(nbi, bo - ji);
       const int64_t j0 = jo + ji;
-      const int64_t mp = m - j0;
+      const int64_t mp = rend(j0 + bi) - j0;
       const DMat Vp = w.V.sub(j0, j0, mp, bi);
       const DMat Ti = To.sub(ji, ji, bi, bi);
       PanelTail tl;
@@ -1123,7 +1133,8 @@ void orgqr_cols(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, int64_t c0, con
   for (int64_t p = npan - 1; p >= 0; --p) {
     const int64_t j0 = p * nb;
     const int64_t b = std::min<int64_t>(nb, n - j0);
-    const int64_t mp = m - j0;
+    // (structured stacks: the block's reflectors act on rows < top_rows + j0 + b)
+    const int64_t mp = (w.top_rows > 0 ? std::min<int64_t>(m, w.top_rows + j0 + b) : m) - j0;
     const int64_t i0 = std::max<int64_t>(0, j0 - c0);  // first affected Q column
     if (i0 >= ncols) continue;
     const int64_t nc = ncols - i0;
@@ -1152,7 +1163,7 @@ void ormqr_left(Ctx& ctx, const QrWork& w, int64_t m, int64_t n, const DMat& C) 
   for (int64_t p = npan - 1; p >= 0; --p) {
     const int64_t j0 = p * nb;
     const int64_t b = std::min<int64_t>(nb, n - j0);
-    const int64_t mp = m - j0;
+    const int64_t mp = (w.top_rows > 0 ? std::min<int64_t>(m, w.top_rows + j0 + b) : m) - j0;
     const DMat Vp = w.V.sub(j0, j0, mp, b);
     const DMat Tp = w.T.sub(0, p * nb, b, b);
     const DMat Cp = C.sub(j0, 0, mp, nc);

@@ -255,11 +255,12 @@ struct QrWork {
   DMat T;               // nb x n: compact-WY T factors per panel, packed
   std::vector<double> taus;
   int nb = 64;
+  int64_t top_rows = 0;  // > 0: structured [T; upper-triangular] stack (geqrf's top_rows)
 };
 // In place Householder QR of A (m x n, m >= n): R in the upper triangle of A,
 // reflectors in work.V / work.T.  Reference convention (kernels.cpp:41-80):
 // p = min(m-1, n) reflectors, R_jj = -sign(x0) ||x||.
-void geqrf(Ctx& ctx, const DMat& A, QrWork& work);
+void geqrf(Ctx& ctx, const DMat& A, QrWork& work, int64_t top_rows = 0);
 // Q(:, c0 : c0+ncols) of the m x m Q = H_0 H_1 ... H_{p-1} into Qout (m x ncols).
 void orgqr_cols(Ctx& ctx, const QrWork& work, int64_t m, int64_t p, int64_t c0, const DMat& Qout);
 // C <- Q C (C is m x ncols, Q = H_0 ... H_{p-1} of an m x n geqrf).
