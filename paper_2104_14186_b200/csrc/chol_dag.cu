@@ -64,6 +64,7 @@ struct DagParams {
   unsigned* done;  // T*T completion counters (zero on entry, reset on exit)
   unsigned* ctrl;  // [0] queue head, [1] CTAs exited
   int* flag;       // set on a non-positive pivot
+  int fused_leaf;  // pipelined factor-and-invert leaf (QDWHG_LEAF_NO_FUSED unset)
   unsigned long long* trace;  // QDWHG_DAG_TRACE: per task {grab, ready, end, smid} (ns), clocks at ready/end
   unsigned long long* ltrace; // ... and per leaf {loaded, factored, inverted, written}
 };
@@ -193,6 +194,7 @@ QDWHG_DEV void tile_gemm(double* sm, int mode, double* C, int64_t ldc, const dou
 constexpr int kGemmSmemDoubles = 3 * kKC * (2 * kTile + 8);  // the 128-row ring (> the strips' 4 stages)
 constexpr int kDagSmemDoubles =
     (kGemmSmemDoubles > leaf::kSmemDoubles) ? kGemmSmemDoubles : leaf::kSmemDoubles;
+static_assert(kDagSmemDoubles >= leaf::kFusedSmemDoubles, "fused leaf scratch");
 
 // LEAF(k): factor and invert the (fully updated) diagonal tile.
 QDWHG_DEV void leaf_task(double* sm, const DagParams& p, int k, int* bad_s) {
@@ -215,9 +217,14 @@ QDWHG_DEV void leaf_task(double* sm, const DagParams& p, int k, int* bad_s) {
   }
   __syncthreads();
   if (p.ltrace && tid == 0) p.ltrace[4 * k] = globaltimer();
-  leaf::factor(A, Sinv, kTile, bad_s);
-  if (p.ltrace && tid == 0) p.ltrace[4 * k + 1] = globaltimer();
-  leaf::invert(A, Tm, Sinv, kTile);
+  if (p.fused_leaf) {
+    leaf::factor_invert_fused(A, Tm, bad_s);  // Tm: the 192 x kLDS scratch
+    if (p.ltrace && tid == 0) p.ltrace[4 * k + 1] = globaltimer();
+  } else {
+    leaf::factor(A, Sinv, kTile, bad_s);
+    if (p.ltrace && tid == 0) p.ltrace[4 * k + 1] = globaltimer();
+    leaf::invert(A, Tm, Sinv, kTile);
+  }
   if (p.ltrace && tid == 0) p.ltrace[4 * k + 2] = globaltimer();
   // Winv_kk = L^{-T} (upper; the strict lower of Winv is pre-zeroed), transposed
   // shared reads with 8 lanes per column (conflict-free for kLDA = 132)
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(leaf::kThreads, 1) chol_dag_kernel(const DagPa
 // dependency, so the order is topological (required: a CTA blocks on the tasks
 // taken before its own).
 std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
-  const double kLeafUs = 50.0, kChainUs = 6.0, kStripUs = 8.6, kTileUs = 27.5;
+  const double kLeafUs = 34.0, kChainUs = 6.0, kStripUs = 8.6, kTileUs = 24.0;
   std::vector<DagTask> tasks;
   std::vector<double> dur;
   std::vector<std::vector<int>> succ;
@@ -616,6 +623,8 @@ void chol_dag(Ctx& ctx, const DMat& Z, const DMat& Winv) {
   p.done = dc.d_done;
   p.ctrl = dc.d_done + (size_t)dc.tmax * dc.tmax;
   p.flag = ctx.dflag;
+  static const bool no_fused = getenv("QDWHG_LEAF_NO_FUSED") != nullptr;
+  p.fused_leaf = no_fused ? 0 : 1;
   static const char* trace_path = getenv("QDWHG_DAG_TRACE");
   p.trace = p.ltrace = nullptr;
   if (trace_path) {

@@ -17,6 +17,18 @@
 
 #include "common.cuh"
 #include "internal.hpp"
+#ifdef QDWHG_DIAG_TRACE  // tools/bench_src/diag_bench: per-phase clock64 marks
+namespace qdwhg {
+namespace {
+__device__ long long g_diag_trace[64];
+}
+}  // namespace qdwhg
+#define DIAG_MARK(i) \
+  if (threadIdx.x == 0) g_diag_trace[i] = clock64()
+#define QDWHG_LEAF_MARK(i) DIAG_MARK(i)
+#else
+#define DIAG_MARK(i)
+#endif
 #include "potrf_leaf.cuh"
 
 namespace qdwhg {
@@ -27,13 +39,6 @@ using leaf::kDiagThreads;
 using leaf::kLDA;
 using leaf::kLDT;
 using leaf::kSB;
-#ifdef QDWHG_DIAG_TRACE
-__device__ long long g_diag_trace[64];
-#define DIAG_MARK(i) \
-  if (threadIdx.x == 0) g_diag_trace[i] = clock64()
-#else
-#define DIAG_MARK(i)
-#endif
 
 // Factor the nb x nb diagonal block (nb <= 128, reads the lower triangle of Z)
 // -> W_kk = L^T (upper, to W) and W_kk^{-1} = L^{-T} (upper, to Winv), one CTA,
@@ -137,7 +142,64 @@ __global__ void __launch_bounds__(kDiagThreads, 1)
   DIAG_MARK(16);
 }
 
+// The 128 x 128 leaf of the fast path when W itself is not wanted: the fused,
+// pipelined factor-and-invert (potrf_leaf.cuh: factor_invert_fused).
+__global__ void __launch_bounds__(kDiagThreads, 1)
+    potrf_diag_fused_kernel(const double* Z, int64_t ldz, double* Winv, int64_t ldwi, int* flag, int flags) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* S = A + 128 * kLDA;
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int nb = 128;
+  if (tid == 0) bad_s = 0;
+  DIAG_MARK(20);
+  griddep_wait();
+  for (int c = warp; c < nb; c += kDiagThreads / 32) {
+    double* col = A + c * kLDA;
+    for (int r = lane; r < nb; r += 32) {
+      if (r >= c)
+        cp_async8(col + r, Z + r + (int64_t)c * ldz);
+      else
+        col[r] = 0.0;
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  DIAG_MARK(0);
+  leaf::factor_invert_fused(A, S, &bad_s);
+  DIAG_MARK(15);
+  if (tid == 0 && bad_s) atomicExch(flag, 1);
+  griddep_launch_dependents();
+  {
+    const int rend = (flags & kDiagUpperOnly) ? 0 : nb;
+    const int j = lane >> 3, rr = lane & 7;
+    for (int c0 = 4 * warp; c0 < nb; c0 += 4 * (kDiagThreads / 32)) {
+      const int c = c0 + j;
+      const int rmax = max(c0 + 4, rend);  // warp-uniform trip count
+      double* wc = Winv + (int64_t)c * ldwi;
+#pragma unroll 4
+      for (int r = rr; r < rmax; r += 8)
+        if (r < max(c + 1, rend)) wc[r] = (r <= c) ? A[r * kLDA + c] : 0.0;
+    }
+  }
+  DIAG_MARK(16);
+}
+
+void launch_diag_fused(Ctx& ctx, const DMat& Zkk, const DMat& Wikk, int flags) {
+  const size_t fsmem = (size_t)leaf::kFusedSmemDoubles * 8;
+  func_attr(potrf_diag_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem);
+  launch_pdl(ctx, potrf_diag_fused_kernel, dim3(1), dim3(kDiagThreads), fsmem, Zkk.ptr(), Zkk.ld,
+             Wikk.ptr(), Wikk.ld, ctx.dflag, flags);
+  ctx.count();
+}
+
 void launch_diag(Ctx& ctx, const DMat& Zkk, const DMat& Wkk, const DMat& Wikk, int flags = 0) {
+  static const bool no_fused = getenv("QDWHG_LEAF_NO_FUSED") != nullptr;
+  if (Zkk.rows == 128 && (flags & kDiagNoW) && !(flags & kDiagInvertOnly) && !no_fused) {
+    launch_diag_fused(ctx, Zkk, Wikk, flags);
+    return;
+  }
   const size_t smem = (size_t)(128 * kLDA + 64 * kLDT + 128) * 8;
   func_attr(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(ctx, potrf_diag_kernel, dim3(1), dim3(kDiagThreads), smem, Zkk.ptr(), Zkk.ld, Wkk.ptr(),

@@ -6,6 +6,9 @@
 #include "common.cuh"
 
 namespace qdwhg {
+#ifndef QDWHG_LEAF_MARK
+#define QDWHG_LEAF_MARK(i)
+#endif
 namespace leaf {
 
 constexpr int kThreads = 256;
@@ -257,6 +260,245 @@ QDWHG_DEV void invert(double* A, double* T, const double* Sinv, int nbp) {
     }
     __syncthreads();
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused, software-pipelined factor-and-invert of a 128 x 128 tile for the fast
+// path (kappa(Z) small: the QDWH step's Z = I + c X^T X, Gram matrices of
+// well-conditioned blocks).  Same result as factor() + invert() up to rounding,
+// but the latency-bound chain of the four 32 x 32 diagonal-block factorisations
+// is the only thing left on the critical path:
+//   * warp 0 factors diagonal block kb in registers and gets D_kb^{-1} from the
+//     SAME column operations (lane i's registers hold row i of L below the
+//     diagonal and row i of L^{-T} from the diagonal on: the two never overlap,
+//     so the unpredicated update loop serves both — no extra flops);
+//   * the panel below is one DMMA product with D_kb^{-T} (no forward
+//     substitution), the next diagonal block's update runs first (all warps,
+//     ~2 x 400 cycles), then warp 0 goes on with block kb + 1;
+//   * meanwhile warps 1-3, 5-7 (warp 4 shares warp 0's sub-partition and FP64
+//     pipe: it only joins the all-warp phases) finish the trailing update and
+//     build block row kb of L^{-1}:  S_kb,j = sum_m L_kb,m X_m,j (ahead of D_kb),
+//     X_kb,j = -D_kb^{-1} S_kb,j, in place over the dead L blocks.
+// A: 128 x kLDA tile (lower triangle = Z, strict upper zero) -> L^{-1} (lower,
+// strict upper zero).  S: 192 x kLDS scratch.  256 threads, barriers 1 and 2.
+constexpr int kLDS = 36;  // = 4 (mod 16): conflict-free DMMA fragment loads
+constexpr int kFusedSmemDoubles = 128 * kLDA + 192 * kLDS;
+
+QDWHG_DEV void bar_all() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+QDWHG_DEV void bar_workers() { asm volatile("bar.sync 2, 224;\n" ::: "memory"); }
+
+template <int J>
+struct CholInvStep {
+  // v[c], c < lane: row `lane` of the block being factored (-> L); v[lane]: its
+  // diagonal; v[c], c > lane: junk until step `lane` zeroes it, then row `lane`
+  // of U = L^{-T} (column operations applied to the identity)
+  static QDWHG_DEV void run(double (&v)[kSB], double* L, int lane, bool& bad, double djj) {
+    if (!(djj > 0.0)) bad = true;
+    const double inv = rsqrt_newton(djj);
+    const double piv = djj * inv;
+    // (measured: a branch around the zeroing 8.3K cycles per block, selects 9.0K)
+#ifndef QDWHG_LEAF_EXPERIMENT_NOZERO
+    if (lane == J) {
+#pragma unroll
+      for (int c = J + 1; c < kSB; ++c) v[c] = 0.0;
+    }
+#endif
+    v[J] = (lane == J) ? inv : v[J] * inv;
+    double dnext = 0.0;
+    if (J + 1 < kSB) {
+      // lane J + 1: L(J+1, J) is in v[J], its diagonal in v[J + 1]
+      dnext = __shfl_sync(0xffffffffu, fma(-v[J], v[J], v[(J + 1) % kSB]), (J + 1) % kSB);
+    }
+    if (lane >= J) L[J * kLDA + lane] = (lane == J) ? piv : v[J];
+    __syncwarp();
+#pragma unroll
+    for (int c = J + 1; c < kSB; ++c) v[c] -= v[J] * L[J * kLDA + c];
+    CholInvStep<J + 1>::run(v, L, lane, bad, dnext);
+  }
+};
+template <>
+struct CholInvStep<kSB> {
+  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double) {}
+};
+
+// L(r0 .. r0+8, b0 .. b0+32) = Z(same) * D^{-T}, D^{-1} lower in the diagonal block at b0
+QDWHG_DEV void fused_panel_tile(double* A, int b0, int r0, int g, int q) {
+  double c[4][2] = {};
+#pragma unroll
+  for (int k4 = 0; k4 < kSB / 4; ++k4) {
+    const double* col = A + (b0 + 4 * k4 + q) * kLDA;
+    const double a = col[r0 + g];
+#pragma unroll
+    for (int tj = 0; tj < 4; ++tj)
+      if (k4 <= 2 * tj + 1) dmma_8x8x4(c[tj][0], c[tj][1], a, col[b0 + 8 * tj + g]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int tj = 0; tj < 4; ++tj) {
+    A[(b0 + 8 * tj + 2 * q) * kLDA + r0 + g] = c[tj][0];
+    A[(b0 + 8 * tj + 2 * q + 1) * kLDA + r0 + g] = c[tj][1];
+  }
+}
+
+// rank-32 update of one 8 x 8 tile (ti >= tj) of the trailing lower triangle at p0
+QDWHG_DEV void fused_update_tile(double* A, int b0, int p0, int ti, int tj, int g, int q) {
+  const int i0 = p0 + 8 * ti, j0 = p0 + 8 * tj;
+  double c0 = A[(j0 + 2 * q) * kLDA + i0 + g], c1 = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
+#pragma unroll
+  for (int k4 = 0; k4 < kSB / 4; ++k4) {
+    const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
+    dmma_8x8x4(c0, c1, -lc[i0 + g], lc[j0 + g]);
+  }
+  if (ti != tj || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c0;
+  if (ti != tj || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c1;
+}
+
+// trailing update of the rows below the next diagonal block (row tiles >= 4 of
+// the trailing matrix at p0), units of one row tile x up to 4 column tiles
+QDWHG_DEV void fused_rest_update(double* A, int b0, int p0, int nt, int w, int nw, int g, int q) {
+  int nunits = 0;
+  for (int ti = 4; ti < nt; ++ti) nunits += ti / 4 + 1;
+  for (int u = w; u < nunits; u += nw) {
+    int ti = 4, rem = u;
+    while (rem >= ti / 4 + 1) {
+      rem -= ti / 4 + 1;
+      ++ti;
+    }
+    const int tj0 = 4 * rem, i0 = p0 + 8 * ti;
+    double c[4][2];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int j0 = p0 + 8 * min(tj0 + v, ti);
+      c[v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
+      c[v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
+    }
+#pragma unroll
+    for (int k4 = 0; k4 < kSB / 4; ++k4) {
+      const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
+      const double a = -lc[i0 + g];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dmma_8x8x4(c[v][0], c[v][1], a, lc[p0 + 8 * min(tj0 + v, ti) + g]);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int tj = tj0 + v;
+      if (tj > ti) break;
+      const int j0 = p0 + 8 * tj;
+      if (tj != ti || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[v][0];
+      if (tj != ti || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[v][1];
+    }
+  }
+}
+
+// S_kn,j = sum_{m = j}^{kn-1} L_kn,m X_m,j for j < kn (X = L^{-1}: diagonal blocks
+// D_m^{-1}, finished rows below), into Sk (32 rows x 32 kn columns).  Units of one
+// 8-row tile x 16 columns, heaviest (smallest j) first.
+QDWHG_DEV void fused_inv_sums(const double* A, double* Sk, int kn, int w, int nw, int g, int q) {
+  const int nunits = kn * 8;
+  for (int u = w; u < nunits; u += nw) {
+    const int j = u >> 3, ri = (u & 7) >> 1, h = u & 1;
+    const int c0 = kSB * j + 16 * h;
+    double c[2][2] = {};
+    for (int k4 = 8 * j + 4 * h; k4 < 8 * kn; ++k4) {
+      const int k = 4 * k4 + q;
+      const double a = A[k * kLDA + kSB * kn + 8 * ri + g];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) dmma_8x8x4(c[v][0], c[v][1], a, A[(c0 + 8 * v + g) * kLDA + k]);
+    }
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      Sk[(c0 + 8 * v + 2 * q) * kLDS + 8 * ri + g] = c[v][0];
+      Sk[(c0 + 8 * v + 2 * q + 1) * kLDS + 8 * ri + g] = c[v][1];
+    }
+  }
+}
+
+// X_kb,j = -D_kb^{-1} S_kb,j for j < kb, in place over block row kb of A.  Units
+// of one 8-row tile x 8 NV columns, heaviest (last row tile) first.
+template <int NV>
+QDWHG_DEV void fused_inv_rows(double* A, const double* Sk, int kb, int w, int nw, int g, int q) {
+  const int b0 = kSB * kb, ncg = 4 * kb / NV;
+  for (int u = w; u < 4 * ncg; u += nw) {
+    const int ri = 3 - u / ncg, cg = u % ncg;
+    double c[NV][2] = {};
+#pragma unroll 2
+    for (int k4 = 0; k4 <= 2 * ri + 1; ++k4) {
+      const int k = 4 * k4 + q;
+      const double a = -A[(b0 + k) * kLDA + b0 + 8 * ri + g];
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        dmma_8x8x4(c[v][0], c[v][1], a, Sk[(8 * NV * cg + 8 * v + g) * kLDS + k]);
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      A[(8 * NV * cg + 8 * v + 2 * q) * kLDA + b0 + 8 * ri + g] = c[v][0];
+      A[(8 * NV * cg + 8 * v + 2 * q + 1) * kLDA + b0 + 8 * ri + g] = c[v][1];
+    }
+  }
+}
+
+QDWHG_DEV double* fused_s_region(double* S, int kb) {  // S_kb: 32 kb columns after S_1 .. S_kb-1
+  return S + kLDS * kSB * (kb * (kb - 1) / 2);
+}
+
+QDWHG_DEV void factor_invert_fused(double* A, double* S, int* bad_s) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  constexpr int NA = 6;  // background workers: warps 1, 2, 3, 5, 6, 7
+  const int ai = (warp == 0 || warp == 4) ? -1 : (warp < 4 ? warp - 1 : warp - 2);
+  constexpr int nblk = 128 / kSB;
+#pragma unroll 1
+  for (int kb = 0; kb < nblk; ++kb) {
+    const int b0 = kSB * kb, p0 = b0 + kSB, R = 128 - p0;
+    if (warp == 0) {
+      // ---- diagonal block kb: L in place (column broadcasts), then D^{-1} over it
+      double v[kSB];
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) v[c] = A[(b0 + c) * kLDA + b0 + lane];
+      bool bad = false;
+      CholInvStep<0>::run(v, A + b0 * kLDA + b0, lane, bad, __shfl_sync(0xffffffffu, v[0], 0));
+      if (bad && lane == 0) *bad_s = 1;
+      __syncwarp();
+      double* D = A + (b0 + lane) * kLDA + b0;  // column `lane` of D^{-1}: U(lane, c) = D^{-1}(c, lane)
+#pragma unroll
+      for (int c = 0; c < kSB; ++c)
+        if (c >= lane) D[c] = v[c];
+      QDWHG_LEAF_MARK(24 + 4 * kb);
+    } else if (kb > 0) {
+      // ---- background of step kp = kb - 1, while warp 0 factors block kb
+      const int kp = kb - 1, pb0 = kSB * kp, pp0 = pb0 + kSB, pnt = (128 - pp0) / 8;
+      if (ai >= 0) {
+        for (int t = 8 + ai; t < pnt; t += NA) fused_panel_tile(A, pb0, pp0 + 8 * t, g, q);
+        if (kp > 0) fused_inv_rows<2>(A, fused_s_region(S, kp), kp, ai, NA, g, q);
+      }
+      bar_workers();
+      if (ai >= 0) {
+        fused_rest_update(A, pb0, pp0, pnt, ai, NA, g, q);
+        fused_inv_sums(A, fused_s_region(S, kb), kb, ai, NA, g, q);
+      }
+    }
+    bar_all();
+    QDWHG_LEAF_MARK(25 + 4 * kb);
+    if (R > 0) {
+      // ---- panel row tiles 0-7 (0-3 feed the next diagonal block), one per warp
+      if (8 * warp < R) fused_panel_tile(A, b0, p0 + 8 * warp, g, q);
+      bar_all();
+      QDWHG_LEAF_MARK(26 + 4 * kb);
+      // ---- next diagonal block's rank-32 update: 10 tiles over 8 warps
+      {
+        // tile u -> (ti, tj), row-major over the lower triangle: u = ti (ti + 1) / 2 + tj
+        const int ti = (warp >= 6) ? 3 : (warp >= 3) ? 2 : (warp >= 1) ? 1 : 0;
+        fused_update_tile(A, b0, p0, ti, warp - ti * (ti + 1) / 2, g, q);
+        if (warp == 2 || warp == 3) fused_update_tile(A, b0, p0, 3, warp, g, q);  // u = 8, 9
+      }
+      bar_all();
+      QDWHG_LEAF_MARK(27 + 4 * kb);
+    }
+  }
+  // ---- last block row of L^{-1}: S_3 is ready, D_3^{-1} just arrived
+  fused_inv_rows<6>(A, fused_s_region(S, nblk - 1), nblk - 1, warp, 8, g, q);
+  bar_all();
 }
 
 }  // namespace leaf

@@ -1,7 +1,15 @@
 // Microbenchmark of the POTRF leaf kernel (potrf_diag_kernel) with per-phase
 // clock64 marks.  Build: make -C tools/bench_src diag_bench
 #define QDWHG_DIAG_TRACE 1
+// kernels compiled into this binary are registered with ITS runtime: their
+// attributes must be set here, not through libqdwhg's (statically linked) one
+#define func_attr bench_func_attr
 #include "../../paper_2104_14186_b200/csrc/potrf.cu"
+namespace qdwhg {
+void bench_func_attr(const void* kern, cudaFuncAttribute attr, int value) {
+  cudaFuncSetAttribute(kern, attr, value);
+}
+}  // namespace qdwhg
 
 #include <cmath>
 #include <cstdint>
@@ -12,7 +20,7 @@ using namespace qdwhg;
 
 __global__ void rsqrt_probe(const double* d, double* y, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) y[i] = rsqrt_newton(d[i]);
+  if (i < n) y[i] = leaf::rsqrt_newton(d[i]);
 }
 
 static void check_rsqrt() {
@@ -46,8 +54,21 @@ int main() {
   const int64_t ld = 128;
   std::vector<double> h(ld * nb);
   // SPD: Z = I*nb + small symmetric
-  for (int j = 0; j < nb; ++j)
-    for (int i = 0; i < nb; ++i) h[i + j * ld] = (i == j ? nb : 0.0) + 1.0 / (1.0 + i + j);
+  // SPD like the QDWH step's Z = I + c X^T X (c = 17: kappa up to ~18 .. 100)
+  {
+    std::vector<double> x(ld * nb);
+    uint64_t st = 777;
+    for (auto& v : x) {
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      v = ((double)(st >> 11) / 9007199254740992.0 - 0.5) * 0.35;
+    }
+    for (int j = 0; j < nb; ++j)
+      for (int i = 0; i < nb; ++i) {
+        double s = 0;
+        for (int k = 0; k < nb; ++k) s += x[k + i * ld] * x[k + j * ld];
+        h[i + j * ld] = (i == j ? 1.0 : 0.0) + 17.0 * s;
+      }
+  }
   double *Z, *W, *Wi;
   int* flag;
   cudaMalloc(&Z, 8 * ld * nb);
@@ -78,6 +99,39 @@ int main() {
   cudaEventSynchronize(e1);
   cudaEventElapsedTime(&ms, e0, e1);
   printf("potrf_diag nb=%d (no W, upper only): %.2f us/launch\n", nb, 1e3 * ms / reps);
+  // the fused, pipelined leaf (kDiagNoW path) against the classic one's W^{-1}
+  {
+    std::vector<double> wi0(ld * nb), wi1(ld * nb);
+    cudaMemset(Wi, 0, 8 * ld * nb);
+    launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
+    cudaMemcpy(wi0.data(), Wi, 8 * ld * nb, cudaMemcpyDeviceToHost);
+    cudaMemset(Wi, 0xff, 8 * ld * nb);
+    launch_diag_fused(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb}, 0);
+    cudaMemcpy(wi1.data(), Wi, 8 * ld * nb, cudaMemcpyDeviceToHost);
+    printf("fused launch: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+    double d = 0, mx = 0;
+    for (size_t i = 0; i < wi0.size(); ++i) {
+      d = std::max(d, std::abs(wi0[i] - wi1[i]));
+      mx = std::max(mx, std::abs(wi0[i]));
+    }
+    printf("fused vs classic W^-1: max abs diff %.3e (max |W^-1| %.3e)\n", d, mx);
+    for (int it = 0; it < 5; ++it) launch_diag_fused(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb}, kDiagUpperOnly);
+    cudaEventRecord(e0);
+    for (int it = 0; it < reps; ++it) launch_diag_fused(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb}, kDiagUpperOnly);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("potrf_diag_fused nb=%d (upper only): %.2f us/launch (%s)\n", nb, 1e3 * ms / reps,
+           cudaGetErrorString(cudaGetLastError()));
+    cudaDeviceSynchronize();
+    long long tf[64];
+    cudaMemcpyFromSymbol(tf, g_diag_trace, sizeof(tf));
+    printf("  fused: load %lld  factor+invert %lld  write %lld  total %lld cycles\n", tf[0] - tf[20],
+           tf[15] - tf[0], tf[16] - tf[15], tf[16] - tf[20]);
+    printf("  fused steps:");
+    for (int i = 24; i < 40; ++i) printf(" %lld", tf[i] - tf[0]);
+    printf("\n");
+  }
   for (int it = 0; it < 2; ++it) launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
   cudaDeviceSynchronize();
   long long t[64];

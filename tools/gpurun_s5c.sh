@@ -1,0 +1,10 @@
+cd $GRAFT_REPO_ROOT
+tools/bench_src/diag_bench | grep -A3 "potrf_diag_fused"
+echo "=== cfg1"; timeout 300 python tools/profile_solve.py --config 1 2>&1 | head -14
+rm -f gpurun_out/dag4096.trace
+QDWHG_DAG_TRACE=gpurun_out/dag4096.trace timeout 120 python tools/timeline.py fast 4096 > /dev/null 2>&1
+python tools/dag_trace.py gpurun_out/dag4096.trace | head -3
+for c in 2 1; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline > gpurun_out/s5c_bench_cfg$c.json 2> gpurun_out/s5c_bench_cfg$c.err
+  python -c "import json; d=json.loads(open('gpurun_out/s5c_bench_cfg$c.json').read().strip().splitlines()[-1]); print($c, round(d['ms_per_step'],3), round(d['value'],2), d['result'].get('oracle_match'), d['result']['stage_seconds'], round(d['roofline'].get('second_kernel',{}).get('achieved',0),2))"
+done
