@@ -226,6 +226,18 @@ QDWHG_DEV void leaf_task(double* sm, const DagParams& p, int k, int* bad_s) {
     leaf::invert(A, Tm, Sinv, kTile);
   }
   if (p.ltrace && tid == 0) p.ltrace[4 * k + 2] = globaltimer();
+  // L_kk^{-1} (lower, zeros above) over Z_kk: the PANEL / FIN tasks' B operand.
+  // Released first (the leaf chain continues through PANEL(k+1, k)); the tile's
+  // counter is released a second time by the caller once Winv_kk is out (ACC tasks)
+  for (int idx = tid; idx < kTile * kTile; idx += leaf::kThreads) {
+    const int c = idx / kTile, r = idx % kTile;
+    Zkk[r + (int64_t)c * p.ldz] = (r >= c) ? A[c * leaf::kLDA + r] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    red_release_add_gpu(&p.done[k * p.T + k], 1u);
+  }
   // Winv_kk = L^{-T} (upper; the strict lower of Winv is pre-zeroed), transposed
   // shared reads with 8 lanes per column (conflict-free for kLDA = 132)
   {
@@ -237,11 +249,6 @@ QDWHG_DEV void leaf_task(double* sm, const DagParams& p, int k, int* bad_s) {
       for (int r = rr; r < c0 + 4; r += 8)
         if (r <= c) wc[r] = A[r * leaf::kLDA + c];
     }
-  }
-  // L_kk^{-1} (lower, zeros above) over Z_kk: the PANEL tasks' B operand
-  for (int idx = tid; idx < kTile * kTile; idx += leaf::kThreads) {
-    const int c = idx / kTile, r = idx % kTile;
-    Zkk[r + (int64_t)c * p.ldz] = (r >= c) ? A[c * leaf::kLDA + r] : 0.0;
   }
   if (p.ltrace) {
     __syncthreads();
@@ -399,10 +406,12 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
   std::vector<std::vector<int>> last((size_t)T * T);  // task ids of the tile's latest step
   auto tile = [T](int i, int j) { return i * T + j; };
   int nk = 1;  // K steps of the next task added (bulk groups: steps k .. k + nk - 1)
-  // measured (n = 4096 DAG / n = 2048 DAG, us): 1 step 2651 / 913, 2: 2442 / 911,
-  // 3: 2386 / 973, 4: 2389 / 1034, 6: 2619 / 1208 — longer tasks pay where the
-  // trailing work is large, short ones where the leaf chain dominates
-  const int kGroup = (T >= 24) ? 3 : 2;
+  // measured with the fused leaf (n = 4096 / 2048 / 1024 DAG, us): 1 step 2640 / 754 /
+  // 361, 2: 2406 / 800 / 384, 3: 2340 / 881 / 416, 4: 2333 / 955 / 455, 6: 2412 /
+  // 1123 / 510 — longer tasks pay where the trailing work is large, short ones
+  // where the leaf chain dominates
+  static const int group_env = getenv("QDWHG_DAG_GROUP") ? atoi(getenv("QDWHG_DAG_GROUP")) : 0;
+  const int kGroup = group_env > 0 ? group_env : (T >= 24) ? 3 : (T >= 20) ? 2 : 1;
   auto addx = [&](int type, int i, int j, int k, int nstrips, const int (&dt)[3], double d, int slot) {
     DagTask base{};
     base.type = type;
@@ -445,12 +454,19 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
     {
       const int dt[3] = {tile(k, k), -1, -1};
       add(kLeafTask, k, k, k, 1, dt, kLeafUs);
+      // the leaf releases its tile twice: L_kk^{-1} (in Z_kk) first, Winv_kk second
+      cnt[tile(k, k)] += 1;
     }
+    // tasks that read only L_kk^{-1} (dependency 1 = tile (k, k)) wait for the first release
+    auto first_release_only = [&](int nstrips) {
+      for (int s = 1; s <= nstrips; ++s) tasks[tasks.size() - s].cnt[1] -= 1;
+    };
     for (int i = k + 1; i < T; ++i) {
       const int dt[3] = {tile(i, k), tile(k, k), -1};
       // the leaf chain LEAF(k) -> PANEL(k+1, k) -> UPDATE(k+1, k+1, k) -> LEAF(k+1)
       // crosses the machine in 16-row strips, the rest of the next column in 32
       add(kPanelTask, i, k, k, i == k + 1 ? 8 : 4, dt, i == k + 1 ? kChainUs : kStripUs);
+      first_release_only(i == k + 1 ? 8 : 4);
     }
     for (int j = k + 1; j < T; ++j)
       for (int i = j; i < T; ++i) {
@@ -490,6 +506,7 @@ std::vector<DagTask> build_tasks(int T, int P, int* nqueue) {
       }
       const int dt[3] = {tile(j, k), tile(k, k), -1};  // all of S, L_kk^{-1}
       addx(kFinTask, k, j, k, 4, dt, kStripUs, tile(j, k));
+      first_release_only(4);
     }
   }
   const int N = (int)tasks.size();

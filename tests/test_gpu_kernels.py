@@ -366,12 +366,13 @@ def test_device_gaussian_reference_stream_determinism_and_moments(cuda):
     assert abs(np.mean(x ** 3)) < 5.0 * np.sqrt(15.0 / N)
 
 
-@pytest.mark.parametrize("n", [256, 384, 1024, 3072, 4096, 4224, 8192])
+@pytest.mark.parametrize("n", [128, 200, 256, 384, 640, 1024, 3072, 4096, 4224, 8192])
 def test_cholesky_inverse_fast_dag_sizes(cuda, n):
     """The tile-DAG Cholesky-and-inverse (chol_dag.cu) at every shape class: pure DAG
     launches (n = 128 T, T = 2 .. 32, K-step groups of 2 and 3), the recursion with a DAG
     sub-tree plus a non-DAG remainder (4224 = 4096 + 128), and two DAG sub-trees under
-    the recursion (8192): W^{-1} against LAPACK on the kappa(Z) <= 1 + c class of the
+    the recursion (8192), a single fused leaf launch (128), a padded classic leaf under
+    the recursion (200): W^{-1} against LAPACK on the kappa(Z) <= 1 + c class of the
     QDWH step (Z = I + c X^T X with c = 50)."""
     import torch
     x = torch.randn(n, n, dtype=torch.float64, device=cuda,
