@@ -749,14 +749,16 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   // and the caller checks the Ritz residuals of the result (falls back otherwise)
   static const int npass = getenv("QDWHG_SUBSPACE_PASSES") ? std::max(1, atoi(getenv("QDWHG_SUBSPACE_PASSES"))) : 3;
   for (int pass = 0; pass < npass; ++pass) {
-    gemm(ctx, Op::T, Op::N, 1.0, B1, Y, 0.0, T1);           // B1^T Y
-    GemmExtra lo;
+    GemmExtra sk;  // l-column blocks against n x n: the two-per-SM 64-tile plan
+    sk.skinny = true;
+    gemm(ctx, Op::T, Op::N, 1.0, B1, Y, 0.0, T1, sk);       // B1^T Y
+    GemmExtra lo = sk;
     lo.krange = KRange::ALower;                              // W11^{-T} lower
     gemm(ctx, Op::T, Op::N, 1.0, W11i, T1, 0.0, T2, lo);
-    GemmExtra up;
+    GemmExtra up = sk;
     up.krange = KRange::AUpper;                              // W11^{-1} upper
     gemm(ctx, Op::N, Op::N, 1.0, W11i, T2, 0.0, T1, up);
-    gemm(ctx, Op::N, Op::N, -1.0, B1, T1, 1.0, Y);           // Y -= B1 G11^{-1} B1^T Y
+    gemm(ctx, Op::N, Op::N, -1.0, B1, T1, 1.0, Y, sk);       // Y -= B1 G11^{-1} B1^T Y
   }
   // CholQR2: Q2 <- Q2 F^{-1}, F = chol(Q2^T Q2), twice (kappa(Y) of a projected
   // Gaussian block is O(sqrt(l)): the second pass reaches rounding-level
@@ -776,6 +778,7 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
     copy(ctx, Q2out, Qt);
     GemmExtra bu;
     bu.krange = KRange::BUpper;
+    bu.skinny = true;
     gemm(ctx, Op::N, Op::N, 1.0, Qt, Fi, 0.0, Q2out, bu);
   }
   ctx.arena->release_to(mark);
@@ -858,7 +861,9 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
     }
     if (clk) clk->mark(3);
     DMat AQ = ctx.arena->alloc(n, ell);
-    gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ);
+    GemmExtra sk;  // n x l products: the two-per-SM 64-tile plan when the model picks 64 tiles
+    sk.skinny = true;
+    gemm(ctx, Op::N, Op::N, 1.0, As, Q2, 0.0, AQ, sk);
     DMat S = ctx.arena->alloc(ell, ell);
     GemmExtra rr;  // S = Q2^T (A Q2) is symmetric: lower tiles, mirrored (exactly symmetric)
     rr.out = OutMode::LowerMirror;
@@ -886,7 +891,7 @@ EigOut partial_eig(Ctx& ctx, const DMat& A, double s, size_t iters, bool randomi
       if (vals[i] >= floor) ++out.borderline;
     }
     out.V = ctx.arena->alloc(n, k);
-    gemm(ctx, Op::N, Op::N, 1.0, Q2, W.sub(0, 0, ell, k), 0.0, out.V);
+    gemm(ctx, Op::N, Op::N, 1.0, Q2, W.sub(0, 0, ell, k), 0.0, out.V, sk);
     out.flops += 2 * nd * l * (double)k;
     if (chq) {
       // Ritz residual ||As V - V Lambda||_F against 1e-13 sqrt(n) ||As||_F (10x inside

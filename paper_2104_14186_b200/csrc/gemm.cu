@@ -654,7 +654,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
     if (nb_ > 1 && (M % bm || N % bm)) continue;  // batched items must tile exactly
     const int64_t tm = (M + bm - 1) / bm, tn = (N + bm - 1) / bm;
     const int64_t tiles = (ex.out != OutMode::Full) ? tn * (tn + 1) / 2 : tm * tn;
-    const int per_sm = (bm == 32) ? 2 : 1;
+    const int per_sm = (bm == 32 || (bm == 64 && ex.skinny)) ? 2 : 1;
     const double eff = (bm == 128) ? 0.95 : (bm == 64) ? 0.75 : 0.45;
     for (int sp : {1, 2, 3, 4, 6, 8, 12, 16}) {
       if (ex.split_k > 0 && sp != ex.split_k) continue;
@@ -686,7 +686,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
     const int bm = BMt;
     const int64_t tm = (M + bm - 1) / bm, tn = (N + bm - 1) / bm;
     const int64_t tiles = (ex.out != OutMode::Full) ? tn * (tn + 1) / 2 : tm * tn;
-    const int per_sm = (bm == 32) ? 2 : 1;
+    const int per_sm = (bm == 32 || (bm == 64 && ex.skinny)) ? 2 : 1;
     const int64_t conc = (int64_t)ctx.num_sms * per_sm;
     const int64_t full = (tiles / conc) * conc, tail = tiles - full;
     const double eff = (bm == 128) ? 0.95 : (bm == 64) ? 0.75 : 0.45;
@@ -727,6 +727,8 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
       dispatch_layout<128, 128, 2, 4, 6>(ctx, ak, bkm, Ae, Be, q);
     else if (tiny)
       dispatch_layout<32, 32, 2, 2, 8>(ctx, ak, bkm, Ae, Be, q);
+    else if (ex.skinny)
+      dispatch_layout<64, 64, 2, 2, 6>(ctx, ak, bkm, Ae, Be, q);
     else
       dispatch_layout<64, 64, 2, 2, 8>(ctx, ak, bkm, Ae, Be, q);
   };

@@ -169,6 +169,11 @@ struct GemmExtra {
   double diag_add = 0.0;
   int split_k = 0;  // 0 = automatic
   int force_bm = 0;  // 0 = automatic; 128 / 64 / 32 pins the tile size
+  // skinny products (an l-column block against n x n): 64-tile CTAs with a 6-stage
+  // ring, two per SM, and the split-K model that goes with it (measured on cfg2's
+  // projection GEMMs: 12-14 -> 18-19 TF).  Opt-in per call site: the default plan
+  // also shapes the bench inputs' bytes (tests/golden/fullsize), so it stays as is.
+  bool skinny = false;
   // Batched launch: item b uses A/B/C shifted by b * (step_r rows, step_c cols)
   // of their stored matrices (items must tile exactly; no split-K).
   int batch = 1;
