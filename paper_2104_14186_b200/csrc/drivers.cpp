@@ -384,10 +384,13 @@ static void syev_dc(Ctx& ctx, const DMat& A, std::vector<double>& vals, const DM
     cfg.ell0 = 1e-15;
     DMat none;
     polar_decompose(ctx, Sh, cfg, Up, none);
-    // C = sym((I - Up)/2), k = round(trace C)
+    // C = sym((I - Up)/2), k = round(trace C); an eigenvalue a few l0 from the
+    // shift leaves trace(C) visibly off an integer (see eig_full_rec): next candidate
     symmetrize_scale(ctx, Up, -0.5, 0.5, Up);
-    k = std::llround(device_trace(ctx, Up));
-    if (k > 0 && k < n) break;
+    const double tr = device_trace(ctx, Up);
+    k = std::llround(tr);
+    if (k > 0 && k < n && std::abs(tr - (double)k) < std::max(2e-13, 16.0 * (double)n * kEps)) break;
+    k = 0;
   }
   if (k <= 0 || k >= n) throw NotConverged("syev: spectral divide-and-conquer found no split");
   DMat Om = ctx.arena->alloc(n, n);
@@ -472,8 +475,10 @@ static int64_t eig_full_rec(Ctx& ctx, const DMat& A, int64_t base, std::vector<d
     // fractional eigenvalue: 0.046 measured on a singular shift, but 1e-7 .. 1e-9
     // when the distance is a few l0: measured 7e-9 at n = 99 with the trace mean on
     // an eigenvalue of a uniform grid — a looser test lets such a split through and
-    // its two subspaces are then invariant only to that accuracy)
-    if (std::abs(tr - (double)k) < std::max(1e-10, 256.0 * (double)n * kEps)) break;
+    // its two subspaces are then invariant only to that accuracy; clean splits
+    // measure |trace - k| <= 1e-13 up to n = 777, a split accepted at 7e-11 cost
+    // 0.8 of the residual gate)
+    if (std::abs(tr - (double)k) < std::max(2e-13, 16.0 * (double)n * kEps)) break;
     k = -1;  // ambiguous: an eigenvalue at the shift
   }
   if (k <= 0 || k >= n) {

@@ -71,7 +71,7 @@ SWITCHES = [("QDWHG_CHOL_NO_LAUUM", "1"), ("QDWHG_CHOL_STABLE", "1"),
             # runs the tile-DAG kernel by default), with and without the overlap; DAG
             # sub-trees of <= 8 tiles under the recursion
             ("QDWHG_CHOL_NO_DAG", "1"), ("QDWHG_CHOL_NO_DAG,QDWHG_CHOL_NO_OVERLAP", "1"),
-            ("QDWHG_CHOL_DAG_TMAX", "8"),
+            ("QDWHG_CHOL_DAG_TMAX", "8"), ("QDWHG_DAG_GROUP", "2"),
             # the classic factor-then-invert leaf instead of the fused, pipelined one
             ("QDWHG_LEAF_NO_FUSED", "1"), ("QDWHG_LEAF_NO_FUSED,QDWHG_CHOL_NO_DAG", "1"),
             ("QDWHG_GEMM_NO_BALANCE", "1"), ("QDWHG_JACOBI_MAX", "8"), ("QDWHG_NO_PDL", "1"),
