@@ -442,6 +442,26 @@ QDWHG_DEV double* fused_s_region(double* S, int kb) {  // S_kb: 32 kb columns af
   return S + kLDS * kSB * (kb * (kb - 1) / 2);
 }
 
+// Warp 0's part of a block step, as a function of its own: its 32-step unrolled
+// chain is sensitive to register allocation, and inlined into the 255-register
+// kernels any edit elsewhere reshuffles it (measured 8.2K <-> 10.2K cycles per block).
+// (Two passes in this warp — the plain Cholesky, 5.7K, then the column operations on
+// the identity — measured 9.7K: the second pass exposes its broadcast loads.)
+static __device__ __noinline__ void fused_factor_block(double* Ablk, int lane, int* bad_s) {
+  // diagonal block: L in place (column broadcasts), then D^{-1} over it
+  double v[kSB];
+#pragma unroll
+  for (int c = 0; c < kSB; ++c) v[c] = Ablk[c * kLDA + lane];
+  bool bad = false;
+  CholInvStep<0>::run(v, Ablk, lane, bad, __shfl_sync(0xffffffffu, v[0], 0));
+  if (bad && lane == 0) *bad_s = 1;
+  __syncwarp();
+  double* D = Ablk + lane * kLDA;  // column `lane` of D^{-1}: U(lane, c) = D^{-1}(c, lane)
+#pragma unroll
+  for (int c = 0; c < kSB; ++c)
+    if (c >= lane) D[c] = v[c];
+}
+
 QDWHG_DEV void factor_invert_fused(double* A, double* S, int* bad_s) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
@@ -452,18 +472,7 @@ QDWHG_DEV void factor_invert_fused(double* A, double* S, int* bad_s) {
   for (int kb = 0; kb < nblk; ++kb) {
     const int b0 = kSB * kb, p0 = b0 + kSB, R = 128 - p0;
     if (warp == 0) {
-      // ---- diagonal block kb: L in place (column broadcasts), then D^{-1} over it
-      double v[kSB];
-#pragma unroll
-      for (int c = 0; c < kSB; ++c) v[c] = A[(b0 + c) * kLDA + b0 + lane];
-      bool bad = false;
-      CholInvStep<0>::run(v, A + b0 * kLDA + b0, lane, bad, __shfl_sync(0xffffffffu, v[0], 0));
-      if (bad && lane == 0) *bad_s = 1;
-      __syncwarp();
-      double* D = A + (b0 + lane) * kLDA + b0;  // column `lane` of D^{-1}: U(lane, c) = D^{-1}(c, lane)
-#pragma unroll
-      for (int c = 0; c < kSB; ++c)
-        if (c >= lane) D[c] = v[c];
+      fused_factor_block(A + b0 * kLDA + b0, lane, bad_s);
       QDWHG_LEAF_MARK(24 + 4 * kb);
     } else if (kb > 0) {
       // ---- background of step kp = kb - 1, while warp 0 factors block kb
