@@ -26,6 +26,8 @@ __device__ long long g_diag_trace[64];
 #define DIAG_MARK(i) \
   if (threadIdx.x == 0) g_diag_trace[i] = clock64()
 #define QDWHG_LEAF_MARK(i) DIAG_MARK(i)
+#define QDWHG_LEAF_MARK_T(i, t) \
+  if (threadIdx.x == (t)) g_diag_trace[i] = clock64()
 #else
 #define DIAG_MARK(i)
 #endif

@@ -9,6 +9,9 @@ namespace qdwhg {
 #ifndef QDWHG_LEAF_MARK
 #define QDWHG_LEAF_MARK(i)
 #endif
+#ifndef QDWHG_LEAF_MARK_T
+#define QDWHG_LEAF_MARK_T(i, t)
+#endif
 namespace leaf {
 
 constexpr int kThreads = 256;
@@ -269,58 +272,30 @@ QDWHG_DEV void invert(double* A, double* T, const double* Sinv, int nbp) {
 // well-conditioned blocks).  Same result as factor() + invert() up to rounding,
 // but the latency-bound chain of the four 32 x 32 diagonal-block factorisations
 // is the only thing left on the critical path:
-//   * warp 0 factors diagonal block kb in registers and gets D_kb^{-1} from the
-//     SAME column operations (lane i's registers hold row i of L below the
-//     diagonal and row i of L^{-T} from the diagonal on: the two never overlap,
-//     so the unpredicated update loop serves both — no extra flops);
+//   * warp 0 factors diagonal block kb in registers (the plain right-looking
+//     Cholesky: 6.2K cycles, the pivot chain) and publishes its columns four at a
+//     time on mbarriers; the helper warp (warp 1, another SM sub-partition) applies
+//     the same column operations to the identity right behind it — lane i holds
+//     row i of U = L^{-T} — and writes D_kb^{-1} over the block ~0.7K cycles after
+//     warp 0 is done.  (Both in warp 0 — one register array serves the row of L
+//     below the diagonal and the row of U from it on, but U's part must be zeroed
+//     at every step — measured 8.2K cycles per block.)
 //   * the panel below is one DMMA product with D_kb^{-T} (no forward
 //     substitution), the next diagonal block's update runs first (all warps,
 //     ~2 x 400 cycles), then warp 0 goes on with block kb + 1;
-//   * meanwhile warps 1-3, 5-7 (warp 4 shares warp 0's sub-partition and FP64
+//   * meanwhile warps 2, 3, 5, 6, 7 (warp 4 shares warp 0's sub-partition and FP64
 //     pipe: it only joins the all-warp phases) finish the trailing update and
 //     build block row kb of L^{-1}:  S_kb,j = sum_m L_kb,m X_m,j (ahead of D_kb),
-//     X_kb,j = -D_kb^{-1} S_kb,j, in place over the dead L blocks.
+//     X_kb,j = -D_kb^{-1} S_kb,j, in place over the dead L blocks.  This
+//     background (DMMA-issue bound on three sub-partitions, ~8K cycles) is now what
+//     a block step waits for, not warp 0.
 // A: 128 x kLDA tile (lower triangle = Z, strict upper zero) -> L^{-1} (lower,
 // strict upper zero).  S: 192 x kLDS scratch.  256 threads, barriers 1 and 2.
 constexpr int kLDS = 36;  // = 4 (mod 16): conflict-free DMMA fragment loads
 constexpr int kFusedSmemDoubles = 128 * kLDA + 192 * kLDS;
 
 QDWHG_DEV void bar_all() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
-QDWHG_DEV void bar_workers() { asm volatile("bar.sync 2, 224;\n" ::: "memory"); }
-
-template <int J>
-struct CholInvStep {
-  // v[c], c < lane: row `lane` of the block being factored (-> L); v[lane]: its
-  // diagonal; v[c], c > lane: junk until step `lane` zeroes it, then row `lane`
-  // of U = L^{-T} (column operations applied to the identity)
-  static QDWHG_DEV void run(double (&v)[kSB], double* L, int lane, bool& bad, double djj) {
-    if (!(djj > 0.0)) bad = true;
-    const double inv = rsqrt_newton(djj);
-    const double piv = djj * inv;
-    // (measured: a branch around the zeroing 8.3K cycles per block, selects 9.0K)
-#ifndef QDWHG_LEAF_EXPERIMENT_NOZERO
-    if (lane == J) {
-#pragma unroll
-      for (int c = J + 1; c < kSB; ++c) v[c] = 0.0;
-    }
-#endif
-    v[J] = (lane == J) ? inv : v[J] * inv;
-    double dnext = 0.0;
-    if (J + 1 < kSB) {
-      // lane J + 1: L(J+1, J) is in v[J], its diagonal in v[J + 1]
-      dnext = __shfl_sync(0xffffffffu, fma(-v[J], v[J], v[(J + 1) % kSB]), (J + 1) % kSB);
-    }
-    if (lane >= J) L[J * kLDA + lane] = (lane == J) ? piv : v[J];
-    __syncwarp();
-#pragma unroll
-    for (int c = J + 1; c < kSB; ++c) v[c] -= v[J] * L[J * kLDA + c];
-    CholInvStep<J + 1>::run(v, L, lane, bad, dnext);
-  }
-};
-template <>
-struct CholInvStep<kSB> {
-  static QDWHG_DEV void run(double (&)[kSB], double*, int, bool&, double) {}
-};
+QDWHG_DEV void bar_workers() { asm volatile("bar.sync 2, 160;\n" ::: "memory"); }  // warps 2, 3, 5, 6, 7
 
 // L(r0 .. r0+8, b0 .. b0+32) = Z(same) * D^{-T}, D^{-1} lower in the diagonal block at b0
 QDWHG_DEV void fused_panel_tile(double* A, int b0, int r0, int g, int q) {
@@ -355,38 +330,58 @@ QDWHG_DEV void fused_update_tile(double* A, int b0, int p0, int ti, int tj, int 
 }
 
 // trailing update of the rows below the next diagonal block (row tiles >= 4 of
-// the trailing matrix at p0), units of one row tile x up to 4 column tiles
+// the trailing matrix at p0), units of one row tile x up to 4 column tiles; a warp
+// runs two units at a time (eight accumulator chains: the 8-step DMMA chains are
+// latency-bound, ~100 cycles a step)
 QDWHG_DEV void fused_rest_update(double* A, int b0, int p0, int nt, int w, int nw, int g, int q) {
   int nunits = 0;
   for (int ti = 4; ti < nt; ++ti) nunits += ti / 4 + 1;
-  for (int u = w; u < nunits; u += nw) {
-    int ti = 4, rem = u;
-    while (rem >= ti / 4 + 1) {
-      rem -= ti / 4 + 1;
-      ++ti;
-    }
-    const int tj0 = 4 * rem, i0 = p0 + 8 * ti;
-    double c[4][2];
+  for (int u0 = w; u0 < nunits; u0 += 2 * nw) {
+    int ti[2], tj0[2];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int j0 = p0 + 8 * min(tj0 + v, ti);
-      c[v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
-      c[v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
+    for (int h = 0; h < 2; ++h) {
+      int rem = min(u0 + h * nw, nunits - 1);  // (a missing second unit repeats the last one: not stored)
+      int t = 4;
+      while (rem >= t / 4 + 1) {
+        rem -= t / 4 + 1;
+        ++t;
+      }
+      ti[h] = t;
+      tj0[h] = 4 * rem;
     }
+    const bool two = u0 + nw < nunits;
+    double c[2][4][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i0 = p0 + 8 * ti[h], j0 = p0 + 8 * min(tj0[h] + v, ti[h]);
+        c[h][v][0] = A[(j0 + 2 * q) * kLDA + i0 + g];
+        c[h][v][1] = A[(j0 + 2 * q + 1) * kLDA + i0 + g];
+      }
 #pragma unroll
     for (int k4 = 0; k4 < kSB / 4; ++k4) {
       const double* lc = A + (b0 + 4 * k4 + q) * kLDA;
-      const double a = -lc[i0 + g];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) dmma_8x8x4(c[v][0], c[v][1], a, lc[p0 + 8 * min(tj0 + v, ti) + g]);
+      for (int h = 0; h < 2; ++h) {
+        const double a = -lc[p0 + 8 * ti[h] + g];
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          dmma_8x8x4(c[h][v][0], c[h][v][1], a, lc[p0 + 8 * min(tj0[h] + v, ti[h]) + g]);
+      }
     }
+    __syncwarp();
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int tj = tj0 + v;
-      if (tj > ti) break;
-      const int j0 = p0 + 8 * tj;
-      if (tj != ti || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[v][0];
-      if (tj != ti || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[v][1];
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !two) break;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int tj = tj0[h] + v;
+        if (tj > ti[h]) break;
+        const int i0 = p0 + 8 * ti[h], j0 = p0 + 8 * tj;
+        if (tj != ti[h] || g >= 2 * q) A[(j0 + 2 * q) * kLDA + i0 + g] = c[h][v][0];
+        if (tj != ti[h] || g >= 2 * q + 1) A[(j0 + 2 * q + 1) * kLDA + i0 + g] = c[h][v][1];
+      }
     }
   }
 }
@@ -442,49 +437,126 @@ QDWHG_DEV double* fused_s_region(double* S, int kb) {  // S_kb: 32 kb columns af
   return S + kLDS * kSB * (kb * (kb - 1) / 2);
 }
 
+// Plain right-looking Cholesky step of warp 0 (as CholStep) that also leaves
+// 1 / L_JJ in sinv[J] and publishes its progress every four columns (one mbarrier
+// per group of four, a phase per block: release / acquire at CTA scope; a
+// st.release flag cost 100 cycles per column): the helper warp applies the same column operations to the identity right behind it.
+// (sinv / prog as 32-bit shared-window addresses: through generic pointers each
+// step's store first converts the address — an S2R the in-order warp waits on —
+// and the block took 8.9K cycles instead of 5.7K)
+QDWHG_DEV void sts_f64(uint32_t addr, double x) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(x));
+}
+QDWHG_DEV void mbar_arrive_s(uint32_t addr) {
+  asm volatile("{\n.reg .b64 t;\nmbarrier.arrive.shared::cta.b64 t, [%0];\n}\n" ::"r"(addr) : "memory");
+}
+template <int J>
+struct CholPubStep {
+  static QDWHG_DEV void run(double (&row)[kSB], double* L, uint32_t sinv, uint32_t prog, int lane,
+                            bool& bad, double djj) {
+    if (!(djj > 0.0)) bad = true;
+    const double inv = rsqrt_newton(djj);
+    if (lane > J) row[J] *= inv;
+    if (lane == J) row[J] = djj * inv;
+    sts_f64(sinv + 8 * J, inv);  // every lane, same value: no branch in the step
+    double dnext = 0.0;
+    if (J + 1 < kSB) dnext = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[(J + 1) % kSB]), (J + 1) % kSB);
+    if (lane >= J) L[J * kLDA + lane] = row[J];
+    __syncwarp();
+    if ((J & 3) == 3) mbar_arrive_s(prog + 8 * (J >> 2));  // columns J-3 .. J are out (32 arrivals)
+#pragma unroll
+    for (int c = J + 1; c < kSB; ++c) row[c] -= row[J] * L[J * kLDA + c];
+    CholPubStep<J + 1>::run(row, L, sinv, prog, lane, bad, dnext);
+  }
+};
+template <>
+struct CholPubStep<kSB> {
+  static QDWHG_DEV void run(double (&)[kSB], double*, uint32_t, uint32_t, int, bool&, double) {}
+};
+
 // Warp 0's part of a block step, as a function of its own: its 32-step unrolled
 // chain is sensitive to register allocation, and inlined into the 255-register
 // kernels any edit elsewhere reshuffles it (measured 8.2K <-> 10.2K cycles per block).
-// (Two passes in this warp — the plain Cholesky, 5.7K, then the column operations on
-// the identity — measured 9.7K: the second pass exposes its broadcast loads.)
-static __device__ __noinline__ void fused_factor_block(double* Ablk, int lane, int* bad_s) {
-  // diagonal block: L in place (column broadcasts), then D^{-1} over it
+// It only factors (5.7K cycles: the pivot chain); D^{-1} comes from the helper warp.
+// (Both in this warp: one pass, the inverse rows' registers zeroed at each step,
+// 8.2K; two passes 9.7K.)
+static __device__ __noinline__ void fused_factor_block(double* Ablk, uint32_t sinv, uint32_t prog, int lane,
+                                                       int* bad_s) {
+  __builtin_assume(__isShared(Ablk));  // not inlined: keep the column broadcasts LDS
   double v[kSB];
 #pragma unroll
   for (int c = 0; c < kSB; ++c) v[c] = Ablk[c * kLDA + lane];
   bool bad = false;
-  CholInvStep<0>::run(v, Ablk, lane, bad, __shfl_sync(0xffffffffu, v[0], 0));
+  CholPubStep<0>::run(v, Ablk, sinv, prog, lane, bad, __shfl_sync(0xffffffffu, v[0], 0));
   if (bad && lane == 0) *bad_s = 1;
+}
+
+// The helper warp (warp 4, warp 0's neighbour on its SM sub-partition): row
+// `lane` of U = L^{-T} by the column operations of the factorisation applied to
+// the identity, four columns behind warp 0; then D^{-1} over the block (warp 0 is
+// done with it: all eight groups are out).
+static __device__ __noinline__ void fused_inverse_block(double* Ablk, const double* sinv, uint64_t* prog,
+                                                        uint32_t parity, int lane) {
+  __builtin_assume(__isShared(Ablk));
+  __builtin_assume(__isShared(sinv));
+  __builtin_assume(__isShared(prog));
+  double u[kSB];
+#pragma unroll
+  for (int c = 0; c < kSB; ++c) u[c] = (c == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int J = 0; J < kSB; ++J) {
+    if ((J & 3) == 0) mbar_wait(&prog[J >> 2], parity);
+    u[J] *= sinv[J];
+#pragma unroll
+    for (int c = J + 1; c < kSB; ++c) u[c] = fma(-u[J], Ablk[J * kLDA + c], u[c]);
+  }
   __syncwarp();
   double* D = Ablk + lane * kLDA;  // column `lane` of D^{-1}: U(lane, c) = D^{-1}(c, lane)
 #pragma unroll
   for (int c = 0; c < kSB; ++c)
-    if (c >= lane) D[c] = v[c];
+    if (c >= lane) D[c] = u[c];
 }
 
 QDWHG_DEV void factor_invert_fused(double* A, double* S, int* bad_s) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  constexpr int NA = 6;  // background workers: warps 1, 2, 3, 5, 6, 7
-  const int ai = (warp == 0 || warp == 4) ? -1 : (warp < 4 ? warp - 1 : warp - 2);
+  // warp 0 factors, warp 1 (another SM sub-partition: on warp 0's own, warp 4, it
+  // slowed the pivot chain from 5.7K to 9.4K cycles) inverts behind it, warp 4 only
+  // joins the all-warp phases, warps 2, 3, 5, 6, 7 are the background workers
+  constexpr int NA = 5;
+  const int ai = (warp == 2 || warp == 3) ? warp - 2 : (warp >= 5 ? warp - 3 : -1);
   constexpr int nblk = 128 / kSB;
+  __shared__ double s_sinv[kSB];
+  __shared__ uint64_t s_prog[kSB / 4];
+  if (tid == 0) {
+    for (int i = 0; i < kSB / 4; ++i) mbar_init(&s_prog[i], 32);
+    fence_barrier_init();
+  }
+  bar_all();
 #pragma unroll 1
   for (int kb = 0; kb < nblk; ++kb) {
     const int b0 = kSB * kb, p0 = b0 + kSB, R = 128 - p0;
     if (warp == 0) {
-      fused_factor_block(A + b0 * kLDA + b0, lane, bad_s);
+      fused_factor_block(A + b0 * kLDA + b0, smem_u32(s_sinv), smem_u32(s_prog), lane, bad_s);
       QDWHG_LEAF_MARK(24 + 4 * kb);
-    } else if (kb > 0) {
+    } else if (warp == 1) {
+      fused_inverse_block(A + b0 * kLDA + b0, s_sinv, s_prog, (uint32_t)(kb & 1), lane);
+      QDWHG_LEAF_MARK_T(40 + kb, 32);
+    } else if (kb > 0 && warp != 4) {
       // ---- background of step kp = kb - 1, while warp 0 factors block kb
       const int kp = kb - 1, pb0 = kSB * kp, pp0 = pb0 + kSB, pnt = (128 - pp0) / 8;
       if (ai >= 0) {
         for (int t = 8 + ai; t < pnt; t += NA) fused_panel_tile(A, pb0, pp0 + 8 * t, g, q);
         if (kp > 0) fused_inv_rows<2>(A, fused_s_region(S, kp), kp, ai, NA, g, q);
       }
+      if (kb == 1) { QDWHG_LEAF_MARK_T(60, 64); }
       bar_workers();
+      if (kb == 1) { QDWHG_LEAF_MARK_T(61, 64); }
       if (ai >= 0) {
         fused_rest_update(A, pb0, pp0, pnt, ai, NA, g, q);
+        if (kb == 1) { QDWHG_LEAF_MARK_T(62, 64); }
         fused_inv_sums(A, fused_s_region(S, kb), kb, ai, NA, g, q);
+        if (kb == 1) { QDWHG_LEAF_MARK_T(63, 64); }
       }
     }
     bar_all();
@@ -492,6 +564,10 @@ QDWHG_DEV void factor_invert_fused(double* A, double* S, int* bad_s) {
     if (R > 0) {
       // ---- panel row tiles 0-7 (0-3 feed the next diagonal block), one per warp
       if (8 * warp < R) fused_panel_tile(A, b0, p0 + 8 * warp, g, q);
+      QDWHG_LEAF_MARK_T(44 + kb, 32);
+      QDWHG_LEAF_MARK_T(48 + kb, 64);
+      QDWHG_LEAF_MARK_T(52 + kb, 128);
+      QDWHG_LEAF_MARK_T(56 + kb, 224);
       bar_all();
       QDWHG_LEAF_MARK(26 + 4 * kb);
       // ---- next diagonal block's rank-32 update: 10 tiles over 8 warps

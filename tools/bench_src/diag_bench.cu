@@ -130,6 +130,8 @@ int main() {
            tf[15] - tf[0], tf[16] - tf[15], tf[16] - tf[20]);
     printf("  fused steps:");
     for (int i = 24; i < 40; ++i) printf(" %lld", tf[i] - tf[0]);
+    printf("\n  helper end / panel end (warps 1, 2, 4, 7):");
+    for (int i = 40; i < 64; ++i) printf(" %lld", tf[i] - tf[0]);
     printf("\n");
   }
   for (int it = 0; it < 2; ++it) launch_diag(ctx, DMat{Z, ld, 0, 0, nb, nb}, DMat{W, ld, 0, 0, nb, nb}, DMat{Wi, ld, 0, 0, nb, nb});
