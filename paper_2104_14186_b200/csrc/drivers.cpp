@@ -157,6 +157,7 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
     GemmExtra syrk;
     syrk.out = OutMode::Lower;  // POTRF reads the lower triangle only
     syrk.diag_add = 1.0;
+    syrk.fine_tail = true;
     gemm(ctx, Op::T, Op::N, w.c, X, X, 0.0, Z, syrk);
     try {
       // kappa(Z) <= 1 + c: the fast recursive Cholesky-and-inverse is accurate here
@@ -188,6 +189,7 @@ void qdwh_chol_step(Ctx& ctx, const DMat& X, const WeightStep& w, const DMat& Xo
     GemmExtra g;
     g.cin = &X;  // fused weight update (b/c) X + (a - b/c) G
     g.out = OutMode::LowerMirror;
+    g.fine_tail = true;
     const bool alias = Xout.base == X.base && Xout.r0 == X.r0 && Xout.c0 == X.c0;
     const DMat dst = alias ? Y : Xout;
     gemm(ctx, Op::N, Op::N, coef, X, Zi, bc, dst, g);
@@ -721,6 +723,7 @@ static bool subspace_cholqr(Ctx& ctx, const DMat& B, double tol, size_t& ind, DM
   // ||B||_2 <= 1 (B = (X + I)/2, |eig(X)| <= 1): delta a few times the rounding
   // noise of the Gram's entries keeps the deficient tail positive definite
   syrk.diag_add = delta;
+  syrk.fine_tail = true;
   gemm(ctx, Op::T, Op::N, 1.0, B, B, 0.0, G, syrk);
   try {
     potrf_upper_and_inverse(ctx, G, Winv, /*want_w=*/false, /*stable=*/false);

@@ -699,7 +699,7 @@ void gemm(Ctx& ctx, Op ta, Op tb, double alpha, const DMat& A, const DMat& B, do
         const double th = (double)(full / conc) * (t_full + 2e-6) +
                           std::ceil((double)tail * sp / conc) * (t_full / sp + 2e-6) +
                           (double)(sp + 2) * tail * bm * bm * 8.0 / 4e12 + 8e-6;
-        if (th < bt * 0.97) {
+        if (th < bt * (ex.fine_tail ? 1.0 : 0.97)) {
           bt = th;
           tail_split = sp;
         }

@@ -174,6 +174,11 @@ struct GemmExtra {
   // projection GEMMs: 12-14 -> 18-19 TF).  Opt-in per call site: the default plan
   // also shapes the bench inputs' bytes (tests/golden/fullsize), so it stays as is.
   bool skinny = false;
+  // wave-balanced tail: take the model's cheapest split factor outright instead of the
+  // first one that improves on the previous by 3 % (n = 4096 lower-triangle launches:
+  // 84 tail tiles split 7 ways, four waves of K/7, instead of 3 ways, two waves of K/3:
+  // cfg2 -0.4 ms).  Opt-in per call site like `skinny`.
+  bool fine_tail = false;
   // Batched launch: item b uses A/B/C shifted by b * (step_r rows, step_c cols)
   // of their stored matrices (items must tile exactly; no split-K).
   int batch = 1;
